@@ -1,0 +1,84 @@
+#ifndef BITSORT_BITSORT_H
+#define BITSORT_BITSORT_H
+
+/*
+ * bitsort C ABI — B200 build (drop-in for the reference's sort surface).
+ *
+ * Every declaration below keeps the reference's name, value and signature so a
+ * caller compiled against /root/reference/proj/include/bitsort/bitsort.h links
+ * against this libbitsort.so.1 unchanged:
+ *
+ *   bws_status      enum   <- proj/include/bitsort/bitsort.h:29-36
+ *   bws_algorithm   enum   <- proj/include/bitsort/bitsort.h:38-45
+ *   bws_version            <- proj/include/bitsort/bitsort.h:47   (impl capi.cpp:96)
+ *   bws_last_error         <- proj/include/bitsort/bitsort.h:49-52 (impl capi.cpp:98)
+ *   bws_algorithm_name     <- proj/include/bitsort/bitsort.h:83   (impl capi.cpp:164-174)
+ *   bws_algorithm_from_name<- proj/include/bitsort/bitsort.h:84   (impl capi.cpp:176-184)
+ *   bws_sort               <- proj/include/bitsort/bitsort.h:86-90 (impl capi.cpp:186-197)
+ *
+ * The reference's bit-utility (bitsort.h:54-79), trace (:92-99) and benchmark
+ * handle (:101-143) entry points are not on the sort path and are not part of
+ * this library.
+ *
+ * Domain of the GPU bws_sort: width 32, unsigned, BWS_ALG_BITWISE (or its
+ * BWS_ALG_BITWISE_SKIP_EMPTY variant), DISTINCT keys. Other (width,
+ * signedness, algorithm) combinations return BWS_ERROR_CONFIG; duplicate keys
+ * return BWS_ERROR_DATA and leave a host array unmodified. There is no CPU
+ * fallback. Additive GPU extensions live in bitsort_gpu.h.
+ */
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(_WIN32)
+#if defined(BITSORT_BUILD)
+#define BITSORT_API __declspec(dllexport)
+#else
+#define BITSORT_API __declspec(dllimport)
+#endif
+#else
+#define BITSORT_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum bws_status {
+    BWS_OK = 0,
+    BWS_ERROR_CONFIG = 1,    /* unsupported width/signedness/algorithm, bad API usage */
+    BWS_ERROR_DATA = 2,      /* null data, duplicate keys, key outside the range hint */
+    BWS_ERROR_INTEGRITY = 3, /* kept for ABI value parity; not produced by bws_sort */
+    BWS_ERROR_RANGE = 4,     /* range hint out of bounds */
+    BWS_ERROR_INTERNAL = 5   /* CUDA / NCCL failure (message in bws_last_error) */
+} bws_status;
+
+typedef enum bws_algorithm {
+    BWS_ALG_BITWISE = 0,
+    BWS_ALG_BITWISE_SKIP_EMPTY = 1,
+    BWS_ALG_INSERTION = 2,
+    BWS_ALG_MERGE = 3,
+    BWS_ALG_COUNTING = 4,
+    BWS_ALG_PLATFORM = 5
+} bws_algorithm;
+
+/* "1.0.0", the reference's library version (capi.cpp:96). */
+BITSORT_API const char* bws_version(void);
+
+/* Message of the most recent failing call on this thread; "" after a call
+ * that succeeded. Valid until the next call on the same thread. */
+BITSORT_API const char* bws_last_error(void);
+
+BITSORT_API const char* bws_algorithm_name(bws_algorithm algorithm);
+BITSORT_API bws_status bws_algorithm_from_name(const char* name, bws_algorithm* out);
+
+/* In-place ascending sort of `count` elements at `data`.
+ * `data` may be host memory (pageable or pinned) or CUDA device memory. */
+BITSORT_API bws_status bws_sort(void* data, size_t count, uint32_t width, int is_unsigned,
+                                bws_algorithm algorithm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITSORT_BITSORT_H */

@@ -1,0 +1,81 @@
+#ifndef BITSORT_BITSORT_GPU_H
+#define BITSORT_BITSORT_GPU_H
+
+/*
+ * Additive B200 extensions to the bitsort C ABI (SURVEY.md §8(b) "Extensions").
+ * None of these exist in the reference; they sit beside bws_sort
+ * (proj/include/bitsort/bitsort.h:89-90) without changing it, so an unmodified
+ * reference caller never sees them. All pointers are plain device or host
+ * addresses; `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream). Every function returns bws_status and sets bws_last_error() exactly
+ * like the reference entry points (capi.cpp:19-41).
+ *
+ * Keys are uint32, distinct, in [0, key_range). key_range is a power of two or
+ * any value in [1, 2^32]; 0 means "derive from the data" (max key + 1).
+ */
+
+#include "bitsort.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* bws_sort(data, count, 32, 1, BWS_ALG_BITWISE) with a key-range hint: skips
+ * the max-reduction pass. Keys >= key_range -> BWS_ERROR_DATA, data untouched. */
+BITSORT_API bws_status bws_sort_u32_range(void* data, size_t count, uint64_t key_range);
+
+/* Device-resident sort, stream-ordered, no host synchronisation. `keys` and
+ * `out` are device pointers (they may alias for an in-place sort). On return
+ * the work is queued on `stream`; bws_gpu_sort_check() synchronises and
+ * validates the most recent sort on this device. */
+BITSORT_API bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t count,
+                                                 uint32_t* out, uint64_t key_range,
+                                                 void* stream);
+
+/* Synchronises `stream` and validates the last bws_gpu_sort_device_async on
+ * the current device: BWS_ERROR_DATA on duplicates / out-of-range keys.
+ * *distinct_out (optional) receives the number of keys written. */
+BITSORT_API bws_status bws_gpu_sort_check(void* stream, uint64_t* distinct_out);
+
+/* Per-rank building blocks for the multi-GPU path (one process per GPU).
+ *   bitset_build: K1 clear of key_range/8 bytes at `bits` + K2 scatter of
+ *                 `count` keys (device) into it. `bits` must hold
+ *                 ceil(key_range/32) uint32 words.
+ *   bitset_scan:  K3 over n_words words at `bits` (a rank's slice), writing
+ *                 key_base + bit_index for every set bit, ascending, to `out`
+ *                 (capacity out_capacity keys). The number of keys is written
+ *                 to the device uint64 at `d_total`. */
+BITSORT_API bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bits,
+                                            uint64_t key_range, void* stream);
+BITSORT_API bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words,
+                                           uint32_t key_base, uint32_t* out,
+                                           uint64_t out_capacity, uint64_t* d_total,
+                                           void* stream);
+
+/* Scatter-kernel staging switches (tests / ablations; default BWS_SCATTER_AUTO). */
+typedef enum bws_scatter_mode {
+    BWS_SCATTER_AUTO = 0,      /* per tile: SMEM staging if the tile's span fits, else
+                                  warp-aggregated (match.any) when a warp's span is
+                                  narrow, else plain atomicOr */
+    BWS_SCATTER_PLAIN = 1,     /* one atomicOr per key */
+    BWS_SCATTER_WARP_AGG = 2,  /* always warp-aggregate */
+    BWS_SCATTER_SMEM = 3       /* SMEM staging when the span fits, else warp-aggregate */
+} bws_scatter_mode;
+BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
+
+/* GPUs used by bws_sort in this process (default 1, or env BITSORT_GPUS). */
+BITSORT_API bws_status bws_gpu_set_device_count(int count);
+BITSORT_API int bws_gpu_device_count(void);
+
+/* Number of kernels this library has launched in this process (evidence for
+ * bench.py's gpu_launches). */
+BITSORT_API uint64_t bws_gpu_launch_count(void);
+
+/* Releases cached device buffers, streams and communicators. */
+BITSORT_API void bws_gpu_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITSORT_BITSORT_GPU_H */

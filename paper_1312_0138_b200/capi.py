@@ -1,0 +1,196 @@
+"""ctypes mirror of the bitsort C ABI (B200 build).
+
+Names, argument meaning and status codes follow the reference interface
+(/root/reference/proj/include/bitsort/bitsort.h:29-90, proj/src/capi.cpp:19-41,
+:164-197) so the parity tests read like the reference's test_capi.cpp. Every
+call goes through ``lib/libbitsort.so.1``; if that library is missing the import
+fails loudly -- there is no Python or CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from typing import Optional
+
+import numpy as np
+
+from . import LIB_DIR
+
+LIB_PATH = LIB_DIR / "libbitsort.so.1"
+
+
+class Status(enum.IntEnum):
+    """bws_status (bitsort.h:29-36)."""
+
+    OK = 0
+    ERROR_CONFIG = 1
+    ERROR_DATA = 2
+    ERROR_INTEGRITY = 3
+    ERROR_RANGE = 4
+    ERROR_INTERNAL = 5
+
+
+class Algorithm(enum.IntEnum):
+    """bws_algorithm (bitsort.h:38-45)."""
+
+    BITWISE = 0
+    BITWISE_SKIP_EMPTY = 1
+    INSERTION = 2
+    MERGE = 3
+    COUNTING = 4
+    PLATFORM = 5
+
+
+class ScatterMode(enum.IntEnum):
+    """bws_scatter_mode (bitsort_gpu.h)."""
+
+    AUTO = 0
+    PLAIN = 1
+    WARP_AGG = 2
+    SMEM = 3
+
+
+class BitsortError(RuntimeError):
+    """A non-OK bws_status, with the thread's bws_last_error() text."""
+
+    def __init__(self, status: int, message: str):
+        self.status = Status(status)
+        self.message = message
+        super().__init__(f"{self.status.name}: {message}")
+
+
+def _load() -> ctypes.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 bitset sort has no fallback implementation)")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    u32, u64, sz, vp, i32 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int
+    sigs = {
+        "bws_version": (ctypes.c_char_p, []),
+        "bws_last_error": (ctypes.c_char_p, []),
+        "bws_algorithm_name": (ctypes.c_char_p, [i32]),
+        "bws_algorithm_from_name": (i32, [ctypes.c_char_p, ctypes.POINTER(i32)]),
+        "bws_sort": (i32, [vp, sz, u32, i32, i32]),
+        "bws_sort_u32_range": (i32, [vp, sz, u64]),
+        "bws_gpu_sort_device_async": (i32, [vp, sz, vp, u64, vp]),
+        "bws_gpu_sort_check": (i32, [vp, ctypes.POINTER(u64)]),
+        "bws_gpu_bitset_build": (i32, [vp, sz, vp, u64, vp]),
+        "bws_gpu_bitset_scan": (i32, [vp, u64, u32, vp, u64, vp, vp]),
+        "bws_gpu_set_scatter_mode": (i32, [i32]),
+        "bws_gpu_set_device_count": (i32, [i32]),
+        "bws_gpu_device_count": (i32, []),
+        "bws_gpu_launch_count": (u64, []),
+        "bws_gpu_shutdown": (None, []),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+#: every symbol include/bitsort/*.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "bws_version", "bws_last_error", "bws_algorithm_name", "bws_algorithm_from_name",
+    "bws_sort", "bws_sort_u32_range", "bws_gpu_sort_device_async", "bws_gpu_sort_check",
+    "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode",
+    "bws_gpu_set_device_count", "bws_gpu_device_count", "bws_gpu_launch_count",
+    "bws_gpu_shutdown",
+)
+
+
+def _check(status: int) -> None:
+    if status != Status.OK:
+        raise BitsortError(status, last_error())
+
+
+def version() -> str:
+    return lib.bws_version().decode()
+
+
+def last_error() -> str:
+    return lib.bws_last_error().decode()
+
+
+def algorithm_name(algorithm: int) -> str:
+    return lib.bws_algorithm_name(int(algorithm)).decode()
+
+
+def algorithm_from_name(name: str) -> Algorithm:
+    out = ctypes.c_int(-1)
+    _check(lib.bws_algorithm_from_name(name.encode(), ctypes.byref(out)))
+    return Algorithm(out.value)
+
+
+def sort_raw(ptr: Optional[int], count: int, width: int = 32, is_unsigned: int = 1,
+             algorithm: int = Algorithm.BITWISE) -> int:
+    """The bare ABI call: returns the bws_status integer."""
+    return lib.bws_sort(ptr, count, width, is_unsigned, int(algorithm))
+
+
+def _ptr_count(data) -> tuple[int, int]:
+    if isinstance(data, np.ndarray):
+        if data.dtype != np.uint32 or not data.flags.c_contiguous:
+            raise TypeError("expected a C-contiguous uint32 numpy array")
+        return data.ctypes.data, data.size
+    # torch tensor (host or CUDA)
+    if str(data.dtype) not in ("torch.uint32", "torch.int32"):
+        raise TypeError("expected a uint32/int32 torch tensor")
+    if not data.is_contiguous():
+        raise TypeError("expected a contiguous tensor")
+    return data.data_ptr(), data.numel()
+
+
+def sort(data, algorithm: int = Algorithm.BITWISE) -> None:
+    """In-place bws_sort(data, n, 32, 1, algorithm) of a uint32 array/tensor
+    (host numpy, pinned or pageable host tensor, or CUDA tensor)."""
+    ptr, n = _ptr_count(data)
+    _check(sort_raw(ptr, n, 32, 1, algorithm))
+
+
+def sort_u32_range(data, key_range: int) -> None:
+    ptr, n = _ptr_count(data)
+    _check(lib.bws_sort_u32_range(ptr, n, key_range))
+
+
+def sort_device_async(keys_ptr: int, count: int, out_ptr: int, key_range: int, stream: int = 0) -> None:
+    _check(lib.bws_gpu_sort_device_async(keys_ptr, count, out_ptr, key_range, stream or None))
+
+
+def sort_check(stream: int = 0) -> int:
+    out = ctypes.c_uint64(0)
+    _check(lib.bws_gpu_sort_check(stream or None, ctypes.byref(out)))
+    return out.value
+
+
+def bitset_build(keys_ptr: int, count: int, bits_ptr: int, key_range: int, stream: int = 0) -> None:
+    _check(lib.bws_gpu_bitset_build(keys_ptr, count, bits_ptr, key_range, stream or None))
+
+
+def bitset_scan(bits_ptr: int, n_words: int, key_base: int, out_ptr: int, out_capacity: int,
+                d_total_ptr: int, stream: int = 0) -> None:
+    _check(lib.bws_gpu_bitset_scan(bits_ptr, n_words, key_base, out_ptr, out_capacity,
+                                   d_total_ptr, stream or None))
+
+
+def set_scatter_mode(mode: int) -> None:
+    _check(lib.bws_gpu_set_scatter_mode(int(mode)))
+
+
+def set_device_count(count: int) -> None:
+    _check(lib.bws_gpu_set_device_count(count))
+
+
+def device_count() -> int:
+    return lib.bws_gpu_device_count()
+
+
+def launch_count() -> int:
+    return lib.bws_gpu_launch_count()
+
+
+def shutdown() -> None:
+    lib.bws_gpu_shutdown()

@@ -1,0 +1,467 @@
+// Host side of libbitsort.so (B200 build): the reference's C ABI entry points
+// (proj/src/capi.cpp) re-implemented over the sm_100a bitset kernels.
+//
+//   wrap()            <- proj/src/capi.cpp:19-41 (exception -> bws_status,
+//                        thread-local message cleared on success)
+//   bws_sort          <- proj/src/capi.cpp:186-197 -> dispatch.hpp:17-55
+//                        (only width 32 / unsigned / bitwise reaches a GPU;
+//                        every other combination is BWS_ERROR_CONFIG: there is
+//                        no CPU fallback)
+//   algorithm names   <- proj/src/capi.cpp:164-184, baselines.hpp:24-43
+//
+// Device state: one lazily created context per CUDA device holding a cached
+// 2^32-bit bitset that is all-zero between sorts (K3 clears every word it
+// consumes), the K3 control block + tile-status array, a key staging buffer for
+// host arrays and an internal stream. Calls on one device are serialised by the
+// context mutex; calls on different devices run concurrently.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "bitsort/bitsort.h"
+#include "bitsort/bitsort_gpu.h"
+#include "kernels.h"
+
+namespace {
+
+using bws_gpu::Ctrl;
+
+thread_local std::string g_last_error;
+
+struct config_error : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct data_error : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct internal_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+template <class F>
+bws_status wrap(F&& body) {
+    try {
+        body();
+        g_last_error.clear();
+        return BWS_OK;
+    } catch (const config_error& e) {
+        g_last_error = e.what();
+        return BWS_ERROR_CONFIG;
+    } catch (const std::out_of_range& e) {
+        g_last_error = e.what();
+        return BWS_ERROR_RANGE;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return BWS_ERROR_DATA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BWS_ERROR_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown failure";
+        return BWS_ERROR_INTERNAL;
+    }
+}
+
+void cuda_check(cudaError_t err, const char* what) {
+    if (err != cudaSuccess)
+        throw internal_error(std::string(what) + ": " + cudaGetErrorName(err) + " (" +
+                             cudaGetErrorString(err) + ")");
+}
+
+constexpr uint64_t kMaxKeyRange = 1ull << 32;
+constexpr uint64_t kMaxWords = kMaxKeyRange / 32;               // 2^27 words = 512 MiB
+constexpr size_t kMaxTiles = (kMaxWords + bws_gpu::SCAN_TILE_WORDS - 1) / bws_gpu::SCAN_TILE_WORDS;
+constexpr size_t kCtrlBytes = sizeof(Ctrl) + kMaxTiles * sizeof(unsigned long long);
+
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_scatter_mode{bws_gpu::kAuto};
+std::atomic<int> g_device_count{0};  // 0 = not yet resolved
+
+struct DeviceCtx {
+    std::mutex mu;
+    bool ready = false;
+    int device = -1;
+    bws_gpu::LaunchGeometry geo;
+    cudaStream_t stream = nullptr;
+    uint32_t* bits = nullptr;  // kMaxWords words; all-zero between sorts unless bits_dirty
+    bool bits_dirty = true;
+    unsigned char* ctrl_mem = nullptr;  // Ctrl followed by the K3 tile-status array
+    uint32_t* keys = nullptr;           // staging for host arrays
+    size_t keys_cap = 0;
+    size_t last_count = 0;        // count of the last async device sort (bws_gpu_sort_check)
+    uint64_t last_range = 0;      // its key range (0 = derived)
+    cudaEvent_t done = nullptr;   // recorded after every queued sort: orders the
+                                  // shared bitset/control block across streams
+
+    Ctrl* ctrl() { return reinterpret_cast<Ctrl*>(ctrl_mem); }
+    unsigned long long* status() {
+        return reinterpret_cast<unsigned long long*>(ctrl_mem + sizeof(Ctrl));
+    }
+
+    void init(int dev) {
+        if (ready) return;
+        device = dev;
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        cuda_check(bws_gpu::query_geometry(dev, &geo), "occupancy query");
+        cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaMalloc(&bits, kMaxWords * sizeof(uint32_t)), "cudaMalloc(bitset 512 MiB)");
+        cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes), "cudaMalloc(control block)");
+        cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
+        bits_dirty = true;
+        ready = true;
+    }
+
+    void ensure_keys(size_t n) {
+        if (n <= keys_cap) return;
+        if (keys) cuda_check(cudaFree(keys), "cudaFree(keys)");
+        keys = nullptr;
+        keys_cap = 0;
+        const size_t cap = n + n / 4;
+        cuda_check(cudaMalloc(&keys, cap * sizeof(uint32_t)), "cudaMalloc(key staging)");
+        keys_cap = cap;
+    }
+
+    void release() {
+        if (!ready) return;
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        cudaFree(bits);
+        cudaFree(ctrl_mem);
+        if (keys) cudaFree(keys);
+        if (stream) cudaStreamDestroy(stream);
+        if (done) cudaEventDestroy(done);
+        done = nullptr;
+        bits = nullptr;
+        ctrl_mem = nullptr;
+        keys = nullptr;
+        keys_cap = 0;
+        stream = nullptr;
+        ready = false;
+    }
+};
+
+constexpr int kMaxDevices = 64;
+DeviceCtx g_ctx[kMaxDevices];
+
+int visible_devices() {
+    int count = 0;
+    const cudaError_t err = cudaGetDeviceCount(&count);
+    if (err != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw internal_error(
+            std::string("no CUDA device available (") + cudaGetErrorString(err) +
+            "); the B200 bitset sort has no CPU fallback");
+    }
+    return count;
+}
+
+DeviceCtx& context_for(int device) {
+    if (device < 0 || device >= kMaxDevices) throw internal_error("device ordinal out of range");
+    return g_ctx[device];
+}
+
+int current_device() {
+    visible_devices();
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    return dev;
+}
+
+// Queues one complete sort of `count` device-resident keys into `out` on
+// `stream`: [bitset reset if dirty] -> control/status reset -> K2 -> K3.
+// Caller holds ctx.mu. key_range == 0 derives the range from the keys (K2
+// folds the max key; K3 scans (max >> 5) + 1 words).
+void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
+                  uint64_t key_range, cudaStream_t stream) {
+    const bool derived = key_range == 0;
+    const uint64_t words = derived ? 0 : (key_range + 31) / 32;
+    cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
+    if (ctx.bits_dirty) {
+        cuda_check(cudaMemsetAsync(ctx.bits, 0, kMaxWords * sizeof(uint32_t), stream),
+                   "bitset reset");
+        ctx.bits_dirty = false;
+    }
+    const size_t tiles = derived ? kMaxTiles : bws_gpu::scan_tiles(words);
+    cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl) + tiles * sizeof(unsigned long long),
+                               stream),
+               "control block reset");
+    ctx.bits_dirty = true;
+    cuda_check(bws_gpu::launch_scatter(keys, count, ctx.bits, derived ? kMaxKeyRange : key_range,
+                                       ctx.ctrl(), g_scatter_mode.load(), ctx.geo, stream),
+               "bitset_scatter launch");
+    g_launches.fetch_add(1);
+    cuda_check(bws_gpu::launch_scan(ctx.bits, words, 0u, out, count, ctx.ctrl(), ctx.status(),
+                                    nullptr, /*clear=*/1, ctx.geo, stream),
+               "bitset_scan launch");
+    g_launches.fetch_add(1);
+    ctx.bits_dirty = false;  // K3 zeroes every word it reads; all set bits lie in its range
+    cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
+}
+
+// Synchronises and turns the control block into a status: out-of-range keys
+// or duplicates (fewer set bits than keys) are BWS_ERROR_DATA.
+uint64_t validate(DeviceCtx& ctx, size_t count, uint64_t key_range, cudaStream_t stream) {
+    cuda_check(cudaStreamSynchronize(stream), "sort execution");
+    Ctrl c;
+    cuda_check(cudaMemcpy(&c, ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost),
+               "control block readback");
+    if (c.bad_keys != 0)
+        throw data_error(std::to_string(c.bad_keys) + " key(s) not below the key range " +
+                         std::to_string(key_range));
+    if (c.total != count)
+        throw data_error("keys are not distinct: " + std::to_string(count) + " keys, " +
+                         std::to_string(c.total) +
+                         " distinct (the bitset sort requires distinct keys)");
+    return c.total;
+}
+
+void check_range(uint64_t key_range) {
+    if (key_range > kMaxKeyRange)
+        throw std::out_of_range("key range " + std::to_string(key_range) +
+                                " exceeds 2^32 for 32-bit keys");
+}
+
+// The drop-in sort on the calling thread's current device (or the device
+// owning `data` when it is device memory). Host arrays are staged through the
+// context's device buffer; they are written back only after validation, so a
+// rejected input is left untouched.
+void sort_u32(void* data, size_t count, uint64_t key_range) {
+    check_range(key_range);
+    if (count == 0) return;
+    visible_devices();
+    cudaPointerAttributes attr{};
+    cudaError_t perr = cudaPointerGetAttributes(&attr, data);
+    if (perr != cudaSuccess) {
+        cudaGetLastError();
+        attr.type = cudaMemoryTypeUnregistered;
+    }
+    const bool on_device = attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+    int device = 0;
+    if (on_device) {
+        device = attr.device;
+    } else {
+        cuda_check(cudaGetDevice(&device), "cudaGetDevice");
+    }
+    DeviceCtx& ctx = context_for(device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    int prev = 0;
+    cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    struct restore_device {
+        int d;
+        ~restore_device() { cudaSetDevice(d); }
+    } restore{prev};
+    ctx.init(device);
+    uint32_t* keys = static_cast<uint32_t*>(data);
+    if (on_device) {
+        enqueue_sort(ctx, keys, count, keys, key_range, ctx.stream);
+        validate(ctx, count, key_range, ctx.stream);
+        return;
+    }
+    ctx.ensure_keys(count);
+    cuda_check(cudaMemcpyAsync(ctx.keys, data, count * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               ctx.stream),
+               "host-to-device copy");
+    enqueue_sort(ctx, ctx.keys, count, ctx.keys, key_range, ctx.stream);
+    validate(ctx, count, key_range, ctx.stream);
+    cuda_check(cudaMemcpyAsync(data, ctx.keys, count * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               ctx.stream),
+               "device-to-host copy");
+    cuda_check(cudaStreamSynchronize(ctx.stream), "device-to-host copy");
+}
+
+const char* algorithm_name_of(bws_algorithm a) {
+    switch (a) {
+        case BWS_ALG_BITWISE: return "bitwise";
+        case BWS_ALG_BITWISE_SKIP_EMPTY: return "bitwise_skip_empty";
+        case BWS_ALG_INSERTION: return "insertion";
+        case BWS_ALG_MERGE: return "merge";
+        case BWS_ALG_COUNTING: return "counting";
+        case BWS_ALG_PLATFORM: return "platform";
+    }
+    return "unknown";
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bws_version(void) { return "1.0.0"; }
+
+const char* bws_last_error(void) { return g_last_error.c_str(); }
+
+const char* bws_algorithm_name(bws_algorithm algorithm) { return algorithm_name_of(algorithm); }
+
+bws_status bws_algorithm_from_name(const char* name, bws_algorithm* out) {
+    return wrap([&] {
+        if (name == nullptr) throw config_error("null algorithm name");
+        if (out == nullptr) throw config_error("null output pointer");
+        for (int id = BWS_ALG_BITWISE; id <= BWS_ALG_PLATFORM; ++id) {
+            const auto a = static_cast<bws_algorithm>(id);
+            if (std::strcmp(name, algorithm_name_of(a)) == 0) {
+                *out = a;
+                return;
+            }
+        }
+        throw config_error("unknown algorithm '" + std::string(name) + "'");
+    });
+}
+
+bws_status bws_sort(void* data, size_t count, uint32_t width, int is_unsigned,
+                    bws_algorithm algorithm) {
+    return wrap([&] {
+        if (count > 0 && data == nullptr) throw data_error("null data with nonzero count");
+        if (static_cast<int>(algorithm) < BWS_ALG_BITWISE ||
+            static_cast<int>(algorithm) > BWS_ALG_PLATFORM)
+            throw config_error("unknown algorithm id");
+        if (width != 8 && width != 16 && width != 32 && width != 64)
+            throw config_error("unsupported width " + std::to_string(width) +
+                               " (expected 8, 16, 32, or 64)");
+        // Nothing to sort: the reference returns OK for any valid (width,
+        // signedness, algorithm) here (test_capi.cpp:95), so do we.
+        if (count == 0) return;
+        if (algorithm != BWS_ALG_BITWISE && algorithm != BWS_ALG_BITWISE_SKIP_EMPTY)
+            throw config_error(std::string("algorithm '") + algorithm_name_of(algorithm) +
+                               "' is not provided by the B200 build (bitwise only)");
+        if (width != 32 || is_unsigned == 0)
+            throw config_error("the B200 bitset sort supports width 32 unsigned keys only (got width " +
+                               std::to_string(width) + (is_unsigned ? " unsigned)" : " signed)"));
+        sort_u32(data, count, 0);
+    });
+}
+
+bws_status bws_sort_u32_range(void* data, size_t count, uint64_t key_range) {
+    return wrap([&] {
+        if (count > 0 && data == nullptr) throw data_error("null data with nonzero count");
+        if (key_range == 0 && count > 0) throw std::out_of_range("key range 0 holds no keys");
+        sort_u32(data, count, key_range);
+    });
+}
+
+bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t count, uint32_t* out,
+                                     uint64_t key_range, void* stream) {
+    return wrap([&] {
+        if (count > 0 && (keys == nullptr || out == nullptr))
+            throw data_error("null device pointer with nonzero count");
+        check_range(key_range);
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        ctx.last_count = count;
+        ctx.last_range = key_range;
+        if (count == 0) return;
+        enqueue_sort(ctx, keys, count, out, key_range, static_cast<cudaStream_t>(stream));
+    });
+}
+
+bws_status bws_gpu_sort_check(void* stream, uint64_t* distinct_out) {
+    return wrap([&] {
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        if (!ctx.ready || ctx.last_count == 0) {
+            if (distinct_out) *distinct_out = 0;
+            return;
+        }
+        const uint64_t total = validate(ctx, ctx.last_count, ctx.last_range ? ctx.last_range : kMaxKeyRange,
+                                        static_cast<cudaStream_t>(stream));
+        if (distinct_out) *distinct_out = total;
+    });
+}
+
+bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bits,
+                                uint64_t key_range, void* stream) {
+    return wrap([&] {
+        if (bits == nullptr || (count > 0 && keys == nullptr))
+            throw data_error("null device pointer");
+        check_range(key_range);
+        if (key_range == 0) throw std::out_of_range("bitset_build needs a key range");
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const uint64_t words = (key_range + 31) / 32;
+        cuda_check(cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), s), "bitset clear");
+        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
+        cuda_check(bws_gpu::launch_scatter(keys, count, bits, key_range, ctx.ctrl(),
+                                           g_scatter_mode.load(), ctx.geo, s),
+                   "bitset_scatter launch");
+        g_launches.fetch_add(1);
+        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+    });
+}
+
+bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t key_base,
+                               uint32_t* out, uint64_t out_capacity, uint64_t* d_total,
+                               void* stream) {
+    return wrap([&] {
+        if (d_total == nullptr) throw data_error("null total pointer");
+        if (n_words > 0 && (bits == nullptr || out == nullptr))
+            throw data_error("null device pointer");
+        if (n_words > kMaxWords) throw std::out_of_range("slice exceeds 2^27 words");
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (n_words == 0) {
+            cuda_check(cudaMemsetAsync(d_total, 0, sizeof(uint64_t), s), "total reset");
+            return;
+        }
+        const size_t tiles = bws_gpu::scan_tiles(n_words);
+        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0,
+                                   sizeof(Ctrl) + tiles * sizeof(unsigned long long), s),
+                   "control block reset");
+        cuda_check(bws_gpu::launch_scan(bits, n_words, key_base, out, out_capacity, ctx.ctrl(),
+                                        ctx.status(),
+                                        reinterpret_cast<unsigned long long*>(d_total),
+                                        /*clear=*/0, ctx.geo, s),
+                   "bitset_scan launch");
+        g_launches.fetch_add(1);
+        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+    });
+}
+
+bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode) {
+    return wrap([&] {
+        if (mode < BWS_SCATTER_AUTO || mode > BWS_SCATTER_SMEM)
+            throw config_error("unknown scatter mode");
+        g_scatter_mode.store(static_cast<int>(mode));
+    });
+}
+
+bws_status bws_gpu_set_device_count(int count) {
+    return wrap([&] {
+        if (count < 1) throw config_error("device count must be >= 1");
+        g_device_count.store(count);
+    });
+}
+
+int bws_gpu_device_count(void) {
+    int c = g_device_count.load();
+    if (c > 0) return c;
+    const char* env = std::getenv("BITSORT_GPUS");
+    c = env ? std::atoi(env) : 1;
+    return c > 0 ? c : 1;
+}
+
+uint64_t bws_gpu_launch_count(void) { return g_launches.load(); }
+
+void bws_gpu_shutdown(void) {
+    for (auto& ctx : g_ctx) {
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.release();
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""Multi-GPU bitset sort, one process per GPU.
+
+Rank r of G holds an input-position shard of the keys. Each rank
+  1. builds a FULL bitset of its shard          (K1 clear + K2 scatter, C ABI)
+  2. reduce-scatters the bitsets with SUM on 32-bit words -> rank r receives
+     words [r*W/G, (r+1)*W/G), i.e. keys [r*M/G, (r+1)*M/G). SUM is exact
+     because distinct keys set disjoint bits (NCCL has no bitwise OR).
+  3. scans its slice                             (K3, C ABI) -> c_r keys
+  4. all-gathers the counts c_r: offset_r = sum(c_<r); sum(c) must equal n,
+     otherwise keys were duplicated (cross-rank duplicates carry and lose bits,
+     so the total only drops) -> BWS_ERROR_DATA.
+The global sorted array is the rank-order concatenation of the local outputs.
+
+The collectives go through torch.distributed (NCCL on GPUs; gloo in the CPU
+tests). The per-rank compute is an injectable ``RankOps``: ``CudaRankOps``
+(the product, sm_100a kernels through libbitsort.so) or, in tests only, an
+oracle-backed CPU implementation that exercises this host logic on gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Protocol
+
+import torch
+import torch.distributed as dist
+
+
+class RankOps(Protocol):
+    def bitset_build(self, keys: torch.Tensor, key_range: int, words: int) -> torch.Tensor:
+        """Full bitset (``words`` int32 words, zero beyond key_range) of ``keys``."""
+
+    def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """(out[capacity] keys, count as a 1-element int64 tensor) of a slice."""
+
+
+@dataclass
+class SliceResult:
+    keys: torch.Tensor      # this rank's sorted keys (a view of length `count`)
+    count: int
+    offset: int             # position of keys[0] in the global sorted array
+    total: int              # keys over all ranks
+    key_lo: int             # this rank's key range [key_lo, key_hi)
+    key_hi: int
+
+
+def slice_words(key_range: int, world: int) -> tuple[int, int]:
+    """(padded total words, words per rank): the bitset is padded so every rank
+    owns the same number of whole words."""
+    words = (key_range + 31) // 32
+    per = (words + world - 1) // world
+    return per * world, per
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Input-position shard [lo, hi) of rank (balanced by construction)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+class CudaRankOps:
+    """Per-rank compute on this process's CUDA device through the C ABI."""
+
+    def __init__(self, device: Optional[torch.device] = None):
+        from . import capi  # loads libbitsort.so; raises if it is not built
+
+        self._capi = capi
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self._bits: Optional[torch.Tensor] = None
+        self._out: Optional[torch.Tensor] = None
+        self._total = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def bitset_build(self, keys: torch.Tensor, key_range: int, words: int) -> torch.Tensor:
+        if self._bits is None or self._bits.numel() < words:
+            self._bits = torch.empty(words, dtype=torch.int32, device=self.device)
+        bits = self._bits[:words]
+        if words * 32 > key_range:  # padding words beyond the key range stay zero
+            bits[(key_range + 31) // 32:].zero_()
+        self._capi.bitset_build(keys.data_ptr(), keys.numel(), bits.data_ptr(), key_range,
+                                self._stream())
+        return bits
+
+    def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int):
+        if self._out is None or self._out.numel() < capacity:
+            self._out = torch.empty(max(capacity, 1), dtype=torch.int32, device=self.device)
+        self._capi.bitset_scan(bits.data_ptr(), bits.numel(), key_base, self._out.data_ptr(),
+                               capacity, self._total.data_ptr(), self._stream())
+        return self._out, self._total
+
+
+def distributed_sort(keys: torch.Tensor, key_range: int, n_total: Optional[int] = None,
+                     ops: Optional[RankOps] = None, group=None) -> SliceResult:
+    """Sorts the union of every rank's ``keys`` shard (distinct uint32 keys in
+    [0, key_range)); returns this rank's slice of the sorted result."""
+    if not 0 < key_range <= 1 << 32:
+        raise ValueError("key_range must be in [1, 2^32]")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ops = ops or CudaRankOps(keys.device)
+    words, per = slice_words(key_range, world)
+    if n_total is None:
+        t = torch.tensor([keys.numel()], dtype=torch.int64, device=keys.device)
+        dist.all_reduce(t, group=group)
+        n_total = int(t.item())
+
+    bits = ops.bitset_build(keys, key_range, words)
+    slice_ = torch.empty(per, dtype=torch.int32, device=bits.device)
+    dist.reduce_scatter_tensor(slice_, bits, op=dist.ReduceOp.SUM, group=group)
+
+    key_lo = rank * per * 32
+    key_hi = min((rank + 1) * per * 32, key_range)
+    capacity = max(0, min(n_total, key_hi - key_lo))
+    out, count_t = ops.bitset_scan(slice_, key_lo, capacity)
+
+    counts = [torch.empty_like(count_t) for _ in range(world)]
+    dist.all_gather(counts, count_t, group=group)
+    counts_h = [int(c.item()) for c in counts]
+    total = sum(counts_h)
+    if total != n_total:
+        from .capi import BitsortError, Status
+
+        raise BitsortError(Status.ERROR_DATA,
+                           f"keys are not distinct or out of range: {n_total} keys, {total} distinct")
+    count = counts_h[rank]
+    return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
+                       key_lo=key_lo, key_hi=key_hi)

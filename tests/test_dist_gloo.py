@@ -1,0 +1,111 @@
+"""Multi-rank host logic of dist.distributed_sort on gloo, world_size 2 and 3.
+
+The per-rank compute is the CPU oracle's bitset restatement (test
+infrastructure); the collectives (reduce-scatter SUM, all-gather of counts),
+the slice/offset arithmetic and duplicate detection are the product code that
+runs unchanged over NCCL on GPUs.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1312_0138_b200.dist import distributed_sort, shard_bounds, slice_words
+
+
+class OracleRankOps:
+    def bitset_build(self, keys, key_range, words):
+        bits, _ = oracle.bitset_build(keys.numpy().view(np.uint32), key_range)
+        full = np.zeros(words, dtype=np.uint32)
+        full[: bits.size] = bits
+        return torch.from_numpy(full.view(np.int32))
+
+    def bitset_scan(self, bits, key_base, capacity):
+        b = bits.numpy().view(np.uint32)
+        out = np.zeros(max(capacity, 1), dtype=np.uint32)
+        cnt = oracle.ORACLE.oracle_bitset_scan(b.ctypes.data, b.size, key_base, out.ctypes.data, capacity)
+        return torch.from_numpy(out.view(np.int32)), torch.tensor([cnt], dtype=torch.int64)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, keys, key_range, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard_bounds(keys.size, rank, world)
+        shard = torch.from_numpy(keys[lo:hi].view(np.int32).copy())
+        try:
+            r = distributed_sort(shard, key_range, ops=OracleRankOps())
+            q.put((rank, "ok", r.keys.numpy().view(np.uint32).copy(), r.offset, r.total, r.key_lo, r.key_hi))
+        except Exception as e:  # noqa: BLE001
+            q.put((rank, type(e).__name__, getattr(e, "status", None), str(e), 0, 0, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_ranks(keys, key_range, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, key_range, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world,key_range,n", [(2, 1 << 20, 100_000), (3, 1000, 1000), (2, 1 << 32, 50_000)])
+def test_distributed_sort_gloo(world, key_range, n):
+    rng = np.random.default_rng(world * 31 + n)
+    if key_range <= 1 << 24:
+        keys = rng.choice(key_range, size=n, replace=False).astype(np.uint32)
+    else:
+        keys = np.unique(rng.integers(0, key_range, size=2 * n, dtype=np.uint64).astype(np.uint32))[:n]
+        rng.shuffle(keys)
+    res = run_ranks(keys, key_range, world)
+    expected = np.sort(keys)
+    words, per = slice_words(key_range, world)
+    parts = []
+    for rank, status, out, offset, total, lo, hi in res:
+        assert status == "ok"
+        assert total == n
+        assert lo == rank * per * 32
+        assert offset == sum(p.size for p in parts)
+        assert ((out >= lo) & (out < hi)).all()
+        parts.append(out)
+    assert np.array_equal(np.concatenate(parts), expected)
+
+
+def test_distributed_duplicates_across_ranks_rejected():
+    keys = np.arange(0, 2000, 2, dtype=np.uint32)
+    keys[-1] = keys[0]  # rank 1's last key duplicates rank 0's first key
+    res = run_ranks(keys, 1 << 12, 2)
+    for rank, status, code, msg, *_ in res:
+        assert status == "BitsortError"
+        assert int(code) == 2  # BWS_ERROR_DATA
+        assert "distinct" in msg
+
+
+def test_slice_and_shard_arithmetic():
+    assert slice_words(1 << 32, 8) == ((1 << 27), (1 << 24))
+    assert slice_words(1000, 3) == (33, 11)  # 32 words padded to 33
+    bounds = [shard_bounds(10, r, 4) for r in range(4)]
+    assert bounds == [(0, 2), (2, 5), (5, 7), (7, 10)]

@@ -1,0 +1,281 @@
+"""GPU parity: the sm_100a bitset sort through the C ABI vs the reference.
+
+Golden vectors come from the reference's own bws_sort (tests/golden/); small
+random cases are checked against the oracle (C restatement of
+bitsort.hpp:84-136); full-size configs against reference-generated hashes
+(tests/golden/anchors.json) and size-independent properties.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import bitwise_sort, fnv1a64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def capi(cuda):
+    from paper_1312_0138_b200 import capi as c
+
+    cuda.cuda.set_device(0)
+    return c
+
+
+@pytest.fixture(autouse=True)
+def _auto_mode(capi):
+    yield
+    capi.set_scatter_mode(capi.ScatterMode.AUTO)
+
+
+def gpu_sort_host(capi, keys: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(keys, dtype=np.uint32).copy()
+    capi.sort(a)
+    return a
+
+
+def gpu_sort_device(capi, torch, keys: np.ndarray, offset: int = 0) -> np.ndarray:
+    buf = torch.zeros(keys.size + offset + 4, dtype=torch.int32, device="cuda")
+    view = buf[offset: offset + keys.size]
+    view.copy_(torch.from_numpy(keys.view(np.int32)))
+    capi.sort(view)
+    torch.cuda.synchronize()
+    return view.cpu().numpy().view(np.uint32)
+
+
+# --- golden vectors from the reference ------------------------------------
+
+def test_acceptance_golden_vectors(capi, acceptance_records):
+    """acceptance.cpp:65-95 criterion-2 inputs (uint32 arm) vs the reference's
+    bws_sort output; inputs with duplicate draws must be rejected untouched."""
+    checked = rejected = 0
+    for rec in acceptance_records:
+        a = rec["input"].copy()
+        status = capi.sort_raw(a.ctypes.data, a.size, 32, 1, capi.Algorithm.BITWISE)
+        if rec["distinct"]:
+            assert status == capi.Status.OK, capi.last_error()
+            assert np.array_equal(a, rec["output"]), (rec["n"], rec["trial"])
+            checked += 1
+        else:
+            assert status == capi.Status.ERROR_DATA
+            assert np.array_equal(a, rec["input"])
+            rejected += 1
+    assert checked >= 60
+
+
+def test_edge_golden_vectors(capi, cuda, edge_records):
+    for rec in edge_records:
+        assert np.array_equal(gpu_sort_host(capi, rec["input"]), rec["output"])
+        assert np.array_equal(gpu_sort_device(capi, cuda, rec["input"]), rec["output"])
+
+
+def test_capi_uint8_vector_widened(capi):
+    """test_capi.cpp:78-82 {200,3,255,0} -> {0,3,200,255}, at width 32."""
+    a = np.array([200, 3, 255, 0], dtype=np.uint32)
+    capi.sort(a)
+    assert a.tolist() == [0, 3, 200, 255]
+
+
+# --- the ABI conventions on a GPU ----------------------------------------
+
+def test_status_conventions(capi):
+    a = np.array([5, 1, 5], dtype=np.uint32)
+    assert capi.sort_raw(a.ctypes.data, 3, 32, 1, 0) == capi.Status.ERROR_DATA
+    assert "distinct" in capi.last_error()
+    assert a.tolist() == [5, 1, 5]  # rejected input left unmodified
+    b = np.array([3, 1, 2], dtype=np.uint32)
+    assert capi.sort_raw(b.ctypes.data, 3, 32, 1, 0) == capi.Status.OK
+    assert capi.last_error() == ""
+    assert b.tolist() == [1, 2, 3]
+    assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.BITWISE_SKIP_EMPTY) == capi.Status.OK
+    assert capi.sort_raw(b.ctypes.data, 3, 32, 0, 0) == capi.Status.ERROR_CONFIG
+    assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.PLATFORM) == capi.Status.ERROR_CONFIG
+
+
+def test_range_hint(capi):
+    keys = np.array([9, 0, 15, 3], dtype=np.uint32)
+    a = keys.copy()
+    capi.sort_u32_range(a, 16)
+    assert a.tolist() == [0, 3, 9, 15]
+    b = keys.copy()
+    with pytest.raises(capi.BitsortError) as e:
+        capi.sort_u32_range(b, 15)  # 15 is not below 15
+    assert e.value.status == capi.Status.ERROR_DATA
+    assert b.tolist() == keys.tolist()
+    with pytest.raises(capi.BitsortError) as e:
+        capi.sort_u32_range(b, (1 << 32) + 1)
+    assert e.value.status == capi.Status.ERROR_RANGE
+    # the bitset cache stays clean after rejected sorts
+    c = np.array([2, 1], dtype=np.uint32)
+    capi.sort_u32_range(c, 1 << 32)
+    assert c.tolist() == [1, 2]
+
+
+# --- random / ragged / aligned cases vs the oracle -------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 31, 32, 33, 100, 1000, 4095, 4096, 4097, 65537])
+@pytest.mark.parametrize("key_range", [1 << 12, 1 << 20, 1 << 32])
+def test_random_distinct_vs_oracle(capi, cuda, n, key_range):
+    if n > key_range:
+        pytest.skip("n > key_range")
+    rng = np.random.default_rng(n * 7919 + key_range % 1000003)
+    keys = rng.choice(key_range, size=n, replace=False).astype(np.uint32) if key_range <= 1 << 24 \
+        else np.unique(rng.integers(0, key_range, size=2 * n, dtype=np.uint64).astype(np.uint32))[:n]
+    rng.shuffle(keys)
+    expected = bitwise_sort(keys)
+    assert np.array_equal(gpu_sort_host(capi, keys), expected)
+    for off in (0, 1, 2, 3):
+        assert np.array_equal(gpu_sort_device(capi, cuda, keys, off), expected)
+    a = keys.copy()
+    capi.sort_u32_range(a, key_range)
+    assert np.array_equal(a, expected)
+
+
+@pytest.mark.parametrize("mode", ["AUTO", "PLAIN", "WARP_AGG", "SMEM"])
+@pytest.mark.parametrize("layout", ["shuffled", "sorted", "reverse", "runs", "clustered"])
+def test_scatter_modes(capi, mode, layout):
+    """Warp aggregation and SMEM staging (K2 paths) give identical bitsets."""
+    rng = np.random.default_rng(5)
+    n = 300_000
+    if layout == "clustered":
+        # cluster-ordered keys (sorted within each of 16 windows): the case the
+        # SMEM staging path targets
+        centres = rng.choice((1 << 32) - (1 << 17), size=16, replace=False) + (1 << 16)
+        keys = np.unique(np.concatenate([
+            (c + rng.integers(-(1 << 16), 1 << 16, size=n // 12)) for c in centres]).astype(np.uint32))
+        keys = np.concatenate([np.sort(keys[i::16]) for i in range(16)])
+    else:
+        keys = rng.choice(1 << 26, size=n, replace=False).astype(np.uint32)
+        if layout == "sorted":
+            keys.sort()
+        elif layout == "reverse":
+            keys = np.sort(keys)[::-1].copy()
+        elif layout == "runs":
+            keys = np.arange(n, dtype=np.uint32) * 3 + 17
+            rng.shuffle(keys.reshape(-1, 1000))
+    capi.set_scatter_mode(getattr(capi.ScatterMode, mode))
+    expected = np.sort(keys)
+    assert np.array_equal(gpu_sort_host(capi, keys), expected)
+    a = keys.copy()
+    capi.sort_u32_range(a, 1 << 32)
+    assert np.array_equal(a, expected)
+
+
+def test_dense_identity(capi, cuda):
+    """n == M: every word full, output is the identity (dense extraction path)."""
+    n = 1 << 22
+    keys = np.random.default_rng(1).permutation(n).astype(np.uint32)
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    capi.sort_u32_range(t, n)
+    cuda.cuda.synchronize()
+    assert cuda.equal(t.cpu(), cuda.arange(n, dtype=cuda.int32))
+
+
+def test_top_of_range(capi):
+    keys = (np.uint32(0xFFFFFFFF) - np.arange(5000, dtype=np.uint32) * np.uint32(7)).astype(np.uint32)
+    a = keys[::-1].copy()
+    capi.sort(a)
+    assert np.array_equal(a, np.sort(keys))
+
+
+def test_duplicates_rejected_at_scale(capi):
+    keys = np.random.default_rng(3).choice(1 << 24, size=1 << 20, replace=False).astype(np.uint32)
+    keys[777] = keys[123456]
+    a = keys.copy()
+    assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.ERROR_DATA
+    assert np.array_equal(a, keys)
+
+
+# --- device-resident async API and the multi-rank building blocks ----------
+
+def test_device_async_and_check(capi, cuda):
+    keys = np.random.default_rng(11).choice(1 << 28, size=1 << 20, replace=False).astype(np.uint32)
+    src = cuda.from_numpy(keys.view(np.int32)).cuda()
+    out = cuda.empty_like(src)
+    stream = cuda.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        capi.sort_device_async(src.data_ptr(), src.numel(), out.data_ptr(), 1 << 28, stream)
+    assert capi.sort_check(stream) == keys.size
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
+    # derived key range
+    capi.sort_device_async(src.data_ptr(), src.numel(), out.data_ptr(), 0, stream)
+    assert capi.sort_check(stream) == keys.size
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_rank_building_blocks_emulated(capi, cuda, world):
+    """The per-rank K2/K3 calls of dist.py, with the reduce-scatter emulated by
+    a sum on one GPU (ranks run one after another; nothing waits on anything)."""
+    from paper_1312_0138_b200.dist import CudaRankOps, shard_bounds, slice_words
+
+    n, key_range = 200_000, 1 << 22
+    keys = np.random.default_rng(world).choice(key_range, size=n, replace=False).astype(np.uint32)
+    words, per = slice_words(key_range, world)
+    ops = CudaRankOps()
+    acc = cuda.zeros(words, dtype=cuda.int32, device="cuda")
+    for r in range(world):
+        lo, hi = shard_bounds(n, r, world)
+        shard = cuda.from_numpy(keys[lo:hi].view(np.int32)).cuda()
+        acc += ops.bitset_build(shard, key_range, words)
+    parts = []
+    for r in range(world):
+        out, cnt = ops.bitset_scan(acc[r * per:(r + 1) * per].contiguous(), r * per * 32, n)
+        parts.append(out[: int(cnt.item())].cpu().numpy().view(np.uint32).copy())
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+
+
+# --- full-size BASELINE configs -------------------------------------------
+
+def _config_sort(capi, cuda, name):
+    from paper_1312_0138_b200.configs import CONFIGS
+
+    cfg = CONFIGS[name]
+    keys = cfg.generate()
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    out = cuda.empty_like(t)
+    stream = cuda.cuda.current_stream().cuda_stream
+    capi.sort_device_async(t.data_ptr(), t.numel(), out.data_ptr(), cfg.key_range, stream)
+    assert capi.sort_check(stream) == cfg.n
+    return cfg, keys, out
+
+
+def test_c1_vs_reference(capi, cuda, anchors):
+    from paper_1312_0138_b200.configs import CONFIGS
+
+    cfg = CONFIGS["C1"]
+    keys = cfg.generate()
+    assert fnv1a64(keys) == anchors["C1"]["fnv1a64_input"]
+    a = keys.copy()
+    capi.sort(a)  # the drop-in call, host array, no range hint
+    assert fnv1a64(a) == anchors["C1"]["fnv1a64_sorted"]
+    assert np.array_equal(a, bitwise_sort(keys))
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_config_vs_reference_hash(capi, cuda, anchors, name):
+    cfg, keys, out = _config_sort(capi, cuda, name)
+    assert fnv1a64(keys) == anchors[name]["fnv1a64_input"]
+    got = out.cpu().numpy().view(np.uint32)
+    assert fnv1a64(got) == anchors[name]["fnv1a64_sorted"]
+
+
+def test_c3_dense_permutation(capi, cuda):
+    cfg, keys, out = _config_sort(capi, cuda, "C3")
+    del keys
+    assert cuda.equal(out, cuda.arange(cfg.n, dtype=cuda.int32, device="cuda"))
+
+
+def test_c5_clustered_properties(capi, cuda):
+    """Size-independent properties: strictly ascending, same count, and the same
+    sum and sum-of-squares (mod 2^64) as the input: together a permutation check
+    for a strictly ascending output."""
+    cfg, keys, out = _config_sort(capi, cuda, "C5")
+    u = out.to(cuda.int64) & 0xFFFFFFFF
+    assert u.numel() == cfg.n
+    assert bool((u[1:] > u[:-1]).all())
+    k = cuda.from_numpy(keys.view(np.int32)).cuda().to(cuda.int64) & 0xFFFFFFFF
+    assert int(u.sum()) == int(k.sum())
+    assert int((u * u).sum()) == int((k * k).sum())
+    assert int(u[0]) == int(keys.min()) and int(u[-1]) == int(keys.max())
