@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 bitset sort (BASELINE.json metric: sorted keys/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one complete sort of the workload's keys (device-resident, timed
+with CUDA events on the launching stream, L2 flushed by a 256 MiB write
+between steps outside the timed events). N > 1 runs under torchrun, one rank
+per GPU: every rank holds an input-position shard, and the step is the full
+multi-GPU sort (K1+K2 -> NCCL reduce-scatter -> K3 -> count all-gather),
+timed as the max over ranks. The default workload is BASELINE.json configs[1]
+(C2). Printed: ONE JSON line (rank 0). See DESIGN.md "Measurement".
+
+--impl reference times the reference's own CPU sort (oracle/_ref, the
+unmodified bws_sort compiled from /root/reference; the C restatement in
+oracle/ if that library is absent) on bounded samples of the same workload,
+on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sorted keys/sec (Gkeys/s) at 1/2/4/8 B200; achieved HBM GB/s fraction of roofline"
+UNIT = "Gkeys/s"
+FALLBACK_HBM_GBPS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2", help="C1..C5 (BASELINE.json configs[0..4]) or 'all'")
+    ap.add_argument("--path", choices=["AUTO", "DIRECT", "BUCKETED"], default="AUTO")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample-keys", type=int, default=1 << 25,
+                    help="keys in the cpu_baseline sample (about 10 s of reference CPU work)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def host_info():
+    model = platform.processor() or ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count()}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except (ValueError, KeyError):
+            pass
+    return FALLBACK_HBM_GBPS, "fallback (B200_PROFILING.md)"
+
+
+# --- per-kernel algorithmic bytes ----------------------
+def kernel_alg_bytes(kernel: str, n: int, key_range: int, world: int = 1) -> int:
+    words_bytes = (key_range + 31) // 32 * 4
+    return {
+        "bucket_hist": 4 * n,                 # read keys
+        "bucket_colscan": 0,
+        "bucket_partition": 8 * n,            # read keys, write bucketed keys
+        "bucket_sort": 8 * n,                 # read bucketed keys, write sorted keys
+        "bitset_scatter": 4 * n + words_bytes,          # read keys, write bitset
+        "bitset_scan": words_bytes // world + 4 * n,    # read (slice of) bitset, write keys
+    }.get(kernel, 0)
+
+
+class ClockSampler(threading.Thread):
+    """NVML poll of SM clock and clock-event reasons while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        super().__init__(daemon=True)
+        self.samples = []
+        self.stop_evt = threading.Event()
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def run(self):
+        while self.ok and not self.stop_evt.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def summary(self, t0: float, t1: float):
+        self.stop_evt.set()
+        self.join(timeout=1.0)
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "note": "NVML unavailable"}
+        win = [s for s in self.samples if t0 <= s[0] <= t1] or self.samples
+        mask = 0
+        for _, _, r in win:
+            mask |= r
+        reasons = sorted(name for bit, name in self.REASONS.items() if mask & bit)
+        return {"sm_mhz": statistics.median(m for _, m, _ in win), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(win)}
+
+
+# --- CPU reference --------------------------------------------------------
+def reference_sorter():
+    """(callable sorting a uint32 array in place, kind, what)."""
+    import oracle
+
+    if oracle.REFERENCE is not None:
+        lib = oracle.REFERENCE
+
+        def run(a):
+            rc = lib.bws_sort(a.ctypes.data, a.size, 32, 1, 0)
+            if rc != 0:
+                raise RuntimeError(lib.bws_last_error().decode())
+
+        return run, "reference", "oracle/_ref/libbitsort_ref.so bws_sort(…,32,1,BWS_ALG_BITWISE)"
+
+    def run_port(a):
+        a[:] = oracle.bitwise_sort(a)
+
+    return run_port, "port", "oracle/bitsort_oracle.c oracle_bitwise_sort_u32 (C restatement)"
+
+
+def cpu_baseline(keys: np.ndarray, sample: int, workload: str):
+    sort, kind, what = reference_sorter()
+    s = min(sample, keys.size)
+    a = keys[:s].copy()
+    t0 = time.perf_counter()
+    sort(a)
+    dt = time.perf_counter() - t0
+    assert np.all(a[1:] > a[:-1]), "reference output not strictly ascending"
+    return {"value": round(s / dt / 1e9, 6), "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"first {s} keys of {workload} ({what}), 1 call, {dt:.2f} s; "
+                      "the reference sort is single-threaded (bitsort.hpp:122-128)",
+            **host_info()}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    sort, kind, what = reference_sorter()
+    keys = cfg.generate()
+    # size each step so that W + K steps take about two minutes at ~4 Mkeys/s
+    budget_s = 120.0
+    sample = int(min(cfg.n, max(1 << 16, 4e6 * budget_s / max(1, args.steps + args.warmup))))
+    base = keys[:sample].copy()
+    for _ in range(args.warmup):
+        a = base.copy()
+        sort(a)
+    times = []
+    for _ in range(args.steps):
+        a = base.copy()
+        t0 = time.perf_counter()
+        sort(a)
+        times.append(time.perf_counter() - t0)
+    assert np.all(a[1:] > a[:-1])
+    ms = 1e3 * sum(times) / len(times)
+    value = sample / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "key_range": cfg.key_range,
+                   "recipe": cfg.recipe, "step_sample_keys": sample},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"first {sample} keys of {cfg.name} per step ({what}); "
+                                   "single-threaded reference (bitsort.hpp:122-128, SPEC.md:216)",
+                         **host_info()},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --- our GPU arm ------------------------------------------------------------
+def traffic_from_profiles(workload: str, kernel: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+    except ValueError:
+        return None
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1312_0138_b200 import capi
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    capi.set_path(getattr(capi.Path, args.path))
+
+    keys_h = cfg.generate()
+    n_total, M = cfg.n, cfg.key_range
+    if world > 1:
+        from paper_1312_0138_b200.dist import CudaRankOps, distributed_sort, shard_bounds
+
+        lo, hi = shard_bounds(n_total, rank, world)
+        shard_h = keys_h[lo:hi]
+    else:
+        shard_h = keys_h
+    keys_d = torch.from_numpy(shard_h.view(np.int32)).to(dev)
+    out_d = torch.empty_like(keys_d)
+    flush = torch.empty(1 << 26, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    if world > 1:
+        ops = CudaRankOps(dev)
+
+        def step():
+            return distributed_sort(keys_d, M, n_total=n_total, ops=ops)
+    else:
+        def step():
+            capi.sort_device_async(keys_d.data_ptr(), n_total, out_d.data_ptr(), M, sp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world == 1:
+        assert capi.sort_check(sp) == n_total
+        u = out_d.to(torch.int64) & 0xFFFFFFFF
+        assert bool((u[1:] > u[:-1]).all()), "output not strictly ascending"
+        del u
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    capi.set_kernel_timing(True)
+    capi.kernel_timings()  # drop anything recorded before the timed region
+    launches0 = capi.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t0 = time.perf_counter()
+    for a, b in evs:
+        flush.fill_(1)  # L2 flush, outside the step's events
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    launches = capi.launch_count() - launches0
+    ktimes = capi.kernel_timings()
+    capi.set_kernel_timing(False)
+    clocks = sampler.summary(t0, t1)
+    if world == 1:
+        assert capi.sort_check(sp) == n_total
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n_total / (ms_per_step / 1e3) / 1e9
+
+    # dominant kernel roofline (live CUDA-event durations from the timed region)
+    peak, peak_src = measured_peak()
+    dom = max(ktimes.items(), key=lambda kv: kv[1][1]) if ktimes else None
+    roofline = None
+    kernels = {}
+    n_local = shard_h.size
+    for name, (cnt, ms) in ktimes.items():
+        avg_s = ms / cnt / 1e3
+        bytes_ = kernel_alg_bytes(name, n_local, M, world)
+        kernels[name] = {"launches": cnt, "avg_us": round(avg_s * 1e6, 2),
+                         "alg_bytes": bytes_, "GBps": round(bytes_ / avg_s / 1e9, 1) if bytes_ else None,
+                         "share": round(ms / max(total_ms, 1e-9), 3)}
+    if dom:
+        name, (cnt, ms) = dom
+        avg_s = ms / cnt / 1e3
+        achieved = kernel_alg_bytes(name, n_local, M, world) / avg_s / 1e9
+        tr = traffic_from_profiles(cfg.name, name)
+        roofline = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1),
+                    "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "traffic": tr, "peak_source": peak_src,
+                    "alg_bytes_per_launch": kernel_alg_bytes(name, n_local, M, world)}
+    step_alg = 8 * n_total + M // 4
+    step_roofline = {"alg_bytes": step_alg,
+                     "achieved": round(step_alg / (ms_per_step / 1e3) / 1e9, 1),
+                     "frac": round(step_alg / (ms_per_step / 1e3) / 1e9 / (peak * world), 4),
+                     "formula": "8n + M/4 (key read + bitset write + bitset read + key write)"}
+
+    # end to end through the public API: pinned host keys -> sorted host keys
+    e2e_steps = max(1, args.e2e_steps)
+    pinned = torch.empty(shard_h.size, dtype=torch.int32, pin_memory=True)
+    host = pinned.numpy().view(np.uint32)
+    times = []
+    for i in range(e2e_steps + 1):
+        np.copyto(host, shard_h)  # restore the unsorted input (outside the timed region)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t_a = time.perf_counter()
+        if world > 1:
+            kd = pinned.to(dev, non_blocking=True)
+            res = distributed_sort(kd, M, n_total=n_total, ops=ops)
+            res.keys.view(torch.int32).cpu()  # D2H of this rank's sorted slice
+            torch.cuda.synchronize(dev)
+        else:
+            capi.sort(host)  # bws_sort(host, n, 32, 1, BWS_ALG_BITWISE): H2D + sort + D2H
+        if i > 0:
+            times.append(time.perf_counter() - t_a)
+    if world == 1:
+        assert np.all(host[1:] > host[:-1])
+    e2e_s = sum(times) / len(times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": round(n_total / e2e_s / 1e9, 4), "unit": UNIT,
+           "h2d_bytes_per_step": 4 * int(shard_h.size) * world,
+           "d2h_bytes_per_step": 4 * int(shard_h.size) * world,
+           "ms_per_step": round(e2e_s * 1e3, 3), "steps": e2e_steps,
+           "api": "bws_sort (C ABI) on a pinned host array" if world == 1
+           else "dist.distributed_sort on pinned host shards"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(keys_h, args.cpu_sample_keys, cfg.name)
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "n": n_total, "key_range": M, "recipe": cfg.recipe,
+                   "l2": "flushed between steps (256 MiB write, outside the step events)",
+                   "path": args.path, "parallelism": f"key shards x{world}" if world > 1 else "single GPU"},
+        "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+        "step_roofline": step_roofline, "kernels": kernels, "cpu_baseline": cpu, "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse_args()
+    from paper_1312_0138_b200.configs import CONFIGS
+
+    names = list(CONFIGS) if args.config == "all" else [args.config]
+    rc = 0
+    for name in names:
+        cfg = CONFIGS[name]
+        rc |= run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

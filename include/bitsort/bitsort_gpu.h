@@ -63,6 +63,19 @@ typedef enum bws_scatter_mode {
 } bws_scatter_mode;
 BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
 
+/* Sort pipeline for bws_sort / bws_sort_u32_range / bws_gpu_sort_device_async
+ * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed).
+ *   DIRECT   : K2 global-bitset scatter + K3 decoupled-lookback scan
+ *   BUCKETED : key-range bucketing (coalesced) + per-bucket SMEM bitset +
+ *              fused extraction; no global bitset
+ *   AUTO     : BUCKETED for n >= 2^21, DIRECT below */
+typedef enum bws_path {
+    BWS_PATH_AUTO = 0,
+    BWS_PATH_DIRECT = 1,
+    BWS_PATH_BUCKETED = 2
+} bws_path;
+BITSORT_API bws_status bws_gpu_set_path(bws_path path);
+
 /* GPUs used by bws_sort in this process (default 1, or env BITSORT_GPUS). */
 BITSORT_API bws_status bws_gpu_set_device_count(int count);
 BITSORT_API int bws_gpu_device_count(void);
@@ -70,6 +83,14 @@ BITSORT_API int bws_gpu_device_count(void);
 /* Number of kernels this library has launched in this process (evidence for
  * bench.py's gpu_launches). */
 BITSORT_API uint64_t bws_gpu_launch_count(void);
+
+/* Per-kernel CUDA-event timing for bench.py's live roofline. While enabled,
+ * every kernel this library launches is bracketed by events on its stream.
+ * bws_gpu_kernel_timings() synchronises those events and writes one line per
+ * kernel, "<name> <launches> <total_ms>\n", for the launches since the
+ * previous call. */
+BITSORT_API bws_status bws_gpu_set_kernel_timing(int enable);
+BITSORT_API bws_status bws_gpu_kernel_timings(char* buf, size_t buf_size);
 
 /* Releases cached device buffers, streams and communicators. */
 BITSORT_API void bws_gpu_shutdown(void);

@@ -50,6 +50,14 @@ class ScatterMode(enum.IntEnum):
     SMEM = 3
 
 
+class Path(enum.IntEnum):
+    """bws_path (bitsort_gpu.h)."""
+
+    AUTO = 0
+    DIRECT = 1
+    BUCKETED = 2
+
+
 class BitsortError(RuntimeError):
     """A non-OK bws_status, with the thread's bws_last_error() text."""
 
@@ -78,9 +86,12 @@ def _load() -> ctypes.CDLL:
         "bws_gpu_bitset_build": (i32, [vp, sz, vp, u64, vp]),
         "bws_gpu_bitset_scan": (i32, [vp, u64, u32, vp, u64, vp, vp]),
         "bws_gpu_set_scatter_mode": (i32, [i32]),
+        "bws_gpu_set_path": (i32, [i32]),
         "bws_gpu_set_device_count": (i32, [i32]),
         "bws_gpu_device_count": (i32, []),
         "bws_gpu_launch_count": (u64, []),
+        "bws_gpu_set_kernel_timing": (i32, [i32]),
+        "bws_gpu_kernel_timings": (i32, [ctypes.c_char_p, sz]),
         "bws_gpu_shutdown": (None, []),
     }
     for name, (res, args) in sigs.items():
@@ -96,8 +107,9 @@ lib = _load()
 EXPORTED = (
     "bws_version", "bws_last_error", "bws_algorithm_name", "bws_algorithm_from_name",
     "bws_sort", "bws_sort_u32_range", "bws_gpu_sort_device_async", "bws_gpu_sort_check",
-    "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode",
+    "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode", "bws_gpu_set_path",
     "bws_gpu_set_device_count", "bws_gpu_device_count", "bws_gpu_launch_count",
+    "bws_gpu_set_kernel_timing", "bws_gpu_kernel_timings",
     "bws_gpu_shutdown",
 )
 
@@ -180,6 +192,10 @@ def set_scatter_mode(mode: int) -> None:
     _check(lib.bws_gpu_set_scatter_mode(int(mode)))
 
 
+def set_path(path: int) -> None:
+    _check(lib.bws_gpu_set_path(int(path)))
+
+
 def set_device_count(count: int) -> None:
     _check(lib.bws_gpu_set_device_count(count))
 
@@ -190,6 +206,21 @@ def device_count() -> int:
 
 def launch_count() -> int:
     return lib.bws_gpu_launch_count()
+
+
+def set_kernel_timing(enable: bool) -> None:
+    _check(lib.bws_gpu_set_kernel_timing(int(enable)))
+
+
+def kernel_timings() -> dict[str, tuple[int, float]]:
+    """{kernel: (launches, total_ms)} since the previous call (synchronises)."""
+    buf = ctypes.create_string_buffer(1 << 14)
+    _check(lib.bws_gpu_kernel_timings(buf, len(buf)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out
 
 
 def shutdown() -> None:

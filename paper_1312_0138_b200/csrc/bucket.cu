@@ -1,0 +1,684 @@
+// Bucketed bitset sort (sm_100a): the K2 scatter with SHARED-MEMORY STAGING
+// made applicable to every input, including shuffled ones.
+//
+// Why: a random-address atomicOr (RED) to global memory costs one L2 request
+// per key. Measured on B200 (profiles/r01_microbench_primitives.jsonl) that
+// caps the direct scatter at ~188 G keys/s for an L2-resident bitset and
+// ~25 G keys/s for a 512 MiB one, while shared-memory atomicOr runs at
+// ~1.7 T keys/s. So the keys are first moved, with coalesced traffic, into
+// key-range buckets whose bitset fits in SMEM (2^shift bits, shift <= 20):
+//
+//   KB1 bucket_hist      per-CTA histogram of bucket ids over a contiguous
+//                        chunk of the keys                       (read 4n)
+//   KB2 bucket_colscan   column prefix over CTAs -> each CTA's first slot
+//                        in every bucket; bucket totals
+//   KB3 bucket_partition per tile: SMEM counting sort by bucket, then
+//                        coalesced run writes to the bucket slots (read 4n,
+//                        write 4n)
+//   KB4 bucket_sort      per bucket: SMEM bitset (atomicOr), popcount, and
+//                        set-bit extraction straight to the output; the
+//                        output offset of a bucket is the prefix of bucket
+//                        totals, so no cross-CTA scan is needed (read 4n,
+//                        write 4n)
+//
+// The global bitset is never materialised: 20n bytes of HBM traffic and no
+// M-proportional term. Duplicate keys are detected by sum(popcount) < n.
+#include "kernels.h"
+
+namespace bws_gpu {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, unsigned lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(kFull, v, off);
+        if (lane >= static_cast<unsigned>(off)) v += o;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of `count` (<= MAX_BUCKETS) uint32 values in
+// `vals` (SMEM), written as 64-bit prefixes to `out64` (SMEM or global) and
+// returning the total. blockDim.x must be a multiple of 32; `scratch` holds
+// 33 uint64.
+__device__ unsigned long long block_exclusive_scan_u64(const uint32_t* vals, int count,
+                                                       unsigned long long* out64,
+                                                       unsigned long long* scratch) {
+    const int per = (count + blockDim.x - 1) / blockDim.x;
+    const int begin = threadIdx.x * per;
+    unsigned long long local = 0;
+    for (int i = 0; i < per; ++i)
+        if (begin + i < count) local += vals[begin + i];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long o = __shfl_up_sync(kFull, incl, off);
+        if (lane >= static_cast<unsigned>(off)) incl += o;
+    }
+    if (lane == 31) scratch[warp] = incl;
+    __syncthreads();
+    const int nwarps = blockDim.x >> 5;
+    if (warp == 0) {
+        unsigned long long w = lane < static_cast<unsigned>(nwarps) ? scratch[lane] : 0ull;
+        unsigned long long wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long o = __shfl_up_sync(kFull, wi, off);
+            if (lane >= static_cast<unsigned>(off)) wi += o;
+        }
+        if (lane < static_cast<unsigned>(nwarps)) scratch[lane] = wi - w;
+        if (lane == 31) scratch[32] = wi;  // total (nwarps <= 32)
+    }
+    __syncthreads();
+    unsigned long long run = scratch[warp] + (incl - local);
+    const unsigned long long total = scratch[32];
+    for (int i = 0; i < per; ++i) {
+        if (begin + i < count) {
+            out64[begin + i] = run;
+            run += vals[begin + i];
+        }
+    }
+    __syncthreads();
+    return total;
+}
+
+// ---------------------------------------------------------------------------
+// KB1/KB3 see the keys as a 16-byte-aligned body of nv uint4 split evenly
+// over the P CTAs, plus <= 3 head keys (CTA 0) and <= 3 tail keys (CTA P-1),
+// so both kernels assign every key to the same CTA.
+
+// Slot of a key in KB1/KB3: its bucket, clamped to the spill slot `nb` for
+// keys beyond the last bucket; padding lanes (`in` false) also spill. KB1 and
+// KB3 apply the same rule, so slot counts always match. A key in
+// [key_range, nb << shift) (non-power-of-two ranges) lands in the last bucket;
+// KB1 counts it in ctrl->bad_keys exactly, and the host then rejects the sort.
+__device__ __forceinline__ uint32_t bucket_or_spill(uint32_t k, bool in, int shift, int nb) {
+    return in ? min(k >> shift, static_cast<uint32_t>(nb)) : static_cast<uint32_t>(nb);
+}
+
+// KB1: histogram of bucket ids over partition CTA c's share, computed by
+// HIST_SPLIT CTAs per share (more loads in flight) that add into the zeroed,
+// bucket-major H[b * P + c] (KB2 scans contiguous rows).
+__global__ void __launch_bounds__(BUCKET_HIST_THREADS)
+    bucket_hist_kernel(KeySplit ks, int shift, int nb, uint32_t limit, int check,
+                       uint32_t* __restrict__ H, Ctrl* __restrict__ ctrl) {
+    __shared__ uint32_t s_h[MAX_BUCKETS + 1];
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) s_h[b] = 0;
+    __syncthreads();
+    const unsigned P = gridDim.x / HIST_SPLIT, c = blockIdx.x / HIST_SPLIT;
+    const unsigned part = blockIdx.x % HIST_SPLIT;
+    const size_t clo = ks.nv * c / P, chi = ks.nv * (c + 1) / P;
+    const size_t vlo = clo + (chi - clo) * part / HIST_SPLIT;
+    const size_t vhi = clo + (chi - clo) * (part + 1) / HIST_SPLIT;
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t mx = 0, bad = 0;
+    constexpr int U = 4;  // uint4 per thread per step: 16 keys, 4 loads in flight
+    for (size_t base = vlo; base < vhi; base += static_cast<size_t>(blockDim.x) * U) {
+        uint4 v[U];
+        bool in[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t i = base + static_cast<size_t>(u) * blockDim.x + threadIdx.x;
+            in[u] = i < vhi;
+            v[u] = in[u] ? __ldcs(ks.body + i) : make_uint4(0, 0, 0, 0);
+        }
+        uint32_t bk[U * 4];
+        uint32_t kmin = 0xffffffffu, kmax = 0;
+        bool all_in = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t kk[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            all_in &= in[u];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bk[u * 4 + q] = bucket_or_spill(kk[q], in[u], shift, nb);
+                kmin = min(kmin, in[u] ? kk[q] : 0xffffffffu);
+                kmax = max(kmax, in[u] ? kk[q] : 0u);
+                bad += (check && in[u] && kk[q] >= limit) ? 1u : 0u;
+            }
+        }
+        mx = max(mx, kmax);
+        const uint32_t wlo = __reduce_min_sync(kFull, kmin);
+        const uint32_t whi = __reduce_max_sync(kFull, kmax);
+        const uint32_t blo = bucket_or_spill(wlo, true, shift, nb);
+        if (blo == bucket_or_spill(whi, true, shift, nb) && __all_sync(kFull, all_in)) {
+            // sorted / clustered input: one bucket for the whole warp step
+            if (lane == 0) atomicAdd(s_h + blo, 32u * U * 4);
+        } else {
+#pragma unroll
+            for (int q = 0; q < U * 4; ++q) atomicAdd(s_h + bk[q], 1u);
+        }
+    }
+    if (threadIdx.x == 0 && part == 0) {  // misaligned head (share 0) / tail (last share)
+        const uint32_t* extra = c == 0 ? ks.head : nullptr;
+        int ne = c == 0 ? ks.n_head : 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = 0; i < ne; ++i) {
+                atomicAdd(s_h + bucket_or_spill(extra[i], true, shift, nb), 1u);
+                mx = max(mx, extra[i]);
+                bad += (check && extra[i] >= limit) ? 1u : 0u;
+            }
+            extra = c == P - 1 ? ks.tail : nullptr;
+            ne = c == P - 1 ? ks.n_tail : 0;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (s_h[b]) atomicAdd(H + static_cast<size_t>(b) * P + c, s_h[b]);
+    const uint32_t wm = __reduce_max_sync(kFull, mx);
+    const uint32_t wb = __reduce_add_sync(kFull, bad);
+    if (lane == 0) {
+        if (wm) atomicMax(&ctrl->max_key, wm);
+        if (wb) atomicAdd(&ctrl->bad_keys, wb);
+    }
+}
+
+// KB2: one warp per bucket row: H[b][c] <- sum_{c' < c} H[b][c']; tot[b] <- row sum.
+__global__ void bucket_colscan_kernel(uint32_t* __restrict__ H, int P, int nb,
+                                      uint32_t* __restrict__ tot) {
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= nb) return;
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t* row = H + static_cast<size_t>(b) * P;
+    const int per = (P + 31) / 32;
+    const int begin = lane * per;
+    uint32_t local = 0;
+    for (int i = 0; i < per; ++i)
+        if (begin + i < P) local += row[begin + i];
+    uint32_t incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(kFull, incl, off);
+        if (lane >= static_cast<unsigned>(off)) incl += o;
+    }
+    uint32_t run = incl - local;
+    for (int i = 0; i < per; ++i) {
+        if (begin + i < P) {
+            const uint32_t v = row[begin + i];
+            row[begin + i] = run;
+            run += v;
+        }
+    }
+    if (lane == 31) tot[b] = incl;
+}
+
+// ---- TMA bulk copy + mbarrier helpers (PTX) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// One thread: expect `bytes` on `bar` and start a bulk global->shared copy.
+__device__ __forceinline__ void tma_load_bytes(void* dst, const void* src, unsigned bytes,
+                                               unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// KB3: partition, one persistent CTA per SM. CTA c streams its share in
+// 16384-key tiles through a double-buffered SMEM ring filled by TMA bulk copies
+// (the next tile lands while the current one is processed). Per tile: ranks
+// from SMEM atomicAdd on per-bucket counters (order inside a bucket is
+// irrelevant to a bitset; out-of-range keys rank in the spill slot nb, which
+// sorts last), an exclusive scan, an in-place counting-sort scatter into the
+// tile buffer, then thread i stores sorted key i to parted[delta[bucket] + i]:
+// consecutive threads write consecutive addresses within each bucket run.
+// Slot positions are 32-bit (the bucketed path requires n < 2^32).
+__global__ void __launch_bounds__(PART_THREADS, 1)
+    bucket_partition_kernel(KeySplit ks, int shift, int nb,
+                            const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
+                            uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int kSlots = MAX_BUCKETS + 1;
+    uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 x PART_TILE
+    uint32_t* s_cnt = s_buf + 2 * PART_TILE;                   // keys per bucket in the tile
+    uint32_t* s_start = s_cnt + kSlots;                        // tile-local bucket start
+    uint32_t* s_cur = s_start + kSlots;                        // next free global slot
+    uint32_t* s_delta = s_cur + kSlots;                        // global slot - local index
+    __shared__ unsigned long long s_scratch[33];
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    __shared__ uint32_t s_tile_valid;
+
+    const unsigned P = gridDim.x, c = blockIdx.x;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t vlo = ks.nv * c / P, vhi = ks.nv * (c + 1) / P;
+    constexpr size_t kTileVec = PART_TILE / 4;
+    const size_t ntiles = (vhi - vlo + kTileVec - 1) / kTileVec;
+    const uint32_t spill = static_cast<uint32_t>(nb);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (size_t t = 0; t < 2 && t < ntiles; ++t) {
+            const size_t v0 = vlo + t * kTileVec;
+            const size_t nvec = min(kTileVec, vhi - v0);
+            tma_load_bytes(s_buf + t * PART_TILE, ks.body + v0, static_cast<unsigned>(nvec * 16),
+                           &s_bar[t]);
+        }
+    }
+
+    // bucket bases (exclusive prefix of totals) + this CTA's first slot per bucket
+    unsigned long long* s_base64 = reinterpret_cast<unsigned long long*>(s_cnt);  // spans cnt+start
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cur[b] = tot[b];
+    __syncthreads();
+    const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        if (c == 0) g_base[b] = s_base64[b];
+        s_delta[b] = static_cast<uint32_t>(s_base64[b] + H[static_cast<size_t>(b) * P + c]);
+    }
+    if (c == 0 && threadIdx.x == 0) g_base[nb] = total;
+    __syncthreads();
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        s_cur[b] = b < nb ? s_delta[b] : 0u;
+        s_cnt[b] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // misaligned head (CTA 0) / tail (CTA P-1) keys
+        const uint32_t* extra = c == 0 ? ks.head : nullptr;
+        int ne = c == 0 ? ks.n_head : 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = 0; i < ne; ++i) {
+                const uint32_t b = bucket_or_spill(extra[i], true, shift, nb);
+                if (b != spill) parted[s_cur[b]++] = extra[i];
+            }
+            extra = c == P - 1 ? ks.tail : nullptr;
+            ne = c == P - 1 ? ks.n_tail : 0;
+        }
+    }
+    __syncthreads();
+
+    constexpr int VPT = PART_KPT / 4;
+    const int slots = nb + 1;
+    const int per = (slots + PART_THREADS - 1) / PART_THREADS;
+    const int sb = threadIdx.x * per;
+    for (size_t t = 0; t < ntiles; ++t) {
+        const int p = static_cast<int>(t & 1);
+        uint32_t* buf = s_buf + p * PART_TILE;
+        const size_t v0 = vlo + t * kTileVec;
+        const uint32_t nvec = static_cast<uint32_t>(min(kTileVec, vhi - v0));
+        mbar_wait(&s_bar[p], static_cast<unsigned>((t >> 1) & 1));
+
+        uint32_t k[PART_KPT];
+        uint32_t rb[PART_KPT];  // bucket << 16 | rank inside the bucket (rank < PART_TILE)
+        uint32_t kmin = 0xffffffffu, kmax = 0;
+        bool all_in = true;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const uint32_t vi = j * PART_THREADS + threadIdx.x;
+            const bool in = vi < nvec;
+            all_in &= in;
+            const uint4 v = in ? reinterpret_cast<const uint4*>(buf)[vi] : make_uint4(0, 0, 0, 0);
+            const uint32_t kk[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                k[4 * j + q] = kk[q];
+                rb[4 * j + q] = bucket_or_spill(kk[q], in, shift, nb);
+                kmin = min(kmin, kk[q]);
+                kmax = max(kmax, kk[q]);
+            }
+        }
+        const uint32_t blo = bucket_or_spill(__reduce_min_sync(kFull, kmin), true, shift, nb);
+        const uint32_t bhi = bucket_or_spill(__reduce_max_sync(kFull, kmax), true, shift, nb);
+        if (blo == bhi && __all_sync(kFull, all_in)) {
+            // the whole warp step lies in one bucket: one atomic, ranks by lane
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(s_cnt + blo, 32u * PART_KPT);
+            base = __shfl_sync(kFull, base, 0) + lane * PART_KPT;
+#pragma unroll
+            for (int q = 0; q < PART_KPT; ++q) rb[q] = (blo << 16) | (base + q);
+        } else {
+#pragma unroll
+            for (int q = 0; q < PART_KPT; ++q) rb[q] = (rb[q] << 16) | atomicAdd(s_cnt + rb[q], 1u);
+        }
+        __syncthreads();  // A: tile counts complete; every thread has read buf
+        {
+            uint32_t local = 0;
+            for (int q = 0; q < per; ++q)
+                if (sb + q < slots) local += s_cnt[sb + q];
+            const uint32_t incl = warp_incl_scan(local, lane);
+            if (lane == 31) s_scratch[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = static_cast<uint32_t>(s_scratch[lane]);  // 32 warps
+                const uint32_t wi = warp_incl_scan(w, lane);
+                s_scratch[lane] = wi - w;
+            }
+            __syncthreads();
+            uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
+            for (int q = 0; q < per; ++q) {
+                const int b = sb + q;
+                if (b < slots) {
+                    const uint32_t cb = s_cnt[b];
+                    s_start[b] = run;
+                    s_delta[b] = s_cur[b] - run;
+                    s_cur[b] += cb;
+                    s_cnt[b] = 0;
+                    if (b == nb) s_tile_valid = run;  // spill keys sort after every bucket
+                    run += cb;
+                }
+            }
+        }
+        __syncthreads();  // B
+#pragma unroll
+        for (int q = 0; q < PART_KPT; ++q) buf[s_start[rb[q] >> 16] + (rb[q] & 0xffffu)] = k[q];
+        __syncthreads();  // C
+        const uint32_t tile_valid = s_tile_valid;
+#pragma unroll 4
+        for (uint32_t i = threadIdx.x; i < tile_valid; i += PART_THREADS) {
+            const uint32_t key = buf[i];
+            parted[s_delta[key >> shift] + i] = key;
+        }
+        __syncthreads();  // D: buf free again
+        if (threadIdx.x == 0 && t + 2 < ntiles) {
+            const size_t v2 = vlo + (t + 2) * kTileVec;
+            const size_t nv2 = min(kTileVec, vhi - v2);
+            fence_proxy_async_smem();
+            tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
+        }
+    }
+}
+
+// Writes kb + bit for every set bit of x, ascending, to the padded stage.
+__device__ __forceinline__ void stage_bits(uint32_t x, uint32_t kb, uint32_t& p, uint32_t* stage) {
+    while (x) {
+        const int bt = __ffs(x) - 1;
+        x &= x - 1;
+        stage[p + (p >> 5)] = kb + static_cast<uint32_t>(bt);
+        ++p;
+    }
+}
+
+// Copies `count` staged keys to o[0, count) with coalesced stores.
+__device__ __forceinline__ void drain_stage(const uint32_t* stage, uint32_t count,
+                                            uint32_t* __restrict__ o, unsigned lane) {
+    __syncwarp();
+    for (uint32_t i = lane; i < count; i += 32) __stcs(o + i, stage[i + (i >> 5)]);
+    __syncwarp();
+}
+
+// Extracts the 32 words at s_bits[w .. w+32) (word per lane) to o[0 ..) and
+// returns the number of keys: a chunk with more than BUCKET_STAGE keys goes
+// word by word with a ballot (lane = bit, coalesced 128-byte stores), others
+// through the warp's stage.
+__device__ __forceinline__ uint32_t extract_words32(const uint32_t* s_bits, uint32_t w,
+                                                    uint32_t key_hi, uint32_t* __restrict__ o,
+                                                    uint32_t* s_stage, unsigned lane) {
+    const uint32_t x = s_bits[w + lane];
+    const uint32_t cx = __popc(x);
+    const uint32_t incl = warp_incl_scan(cx, lane);
+    const uint32_t ctot = __shfl_sync(kFull, incl, 31);
+    if (ctot == 0) return 0;
+    if (ctot > static_cast<uint32_t>(BUCKET_STAGE)) {
+        const unsigned lt = lanemask_lt();
+        uint32_t q = 0;
+        const uint32_t kb = key_hi + (w << 5) + lane;
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t xj = __shfl_sync(kFull, x, j);
+            const bool bit = (xj >> lane) & 1u;
+            const unsigned m = __ballot_sync(kFull, bit);
+            if (bit) __stcs(o + q + __popc(m & lt), kb + (static_cast<uint32_t>(j) << 5));
+            q += __popc(m);
+        }
+        return ctot;
+    }
+    uint32_t p = incl - cx;
+    stage_bits(x, key_hi + ((w + lane) << 5), p, s_stage);
+    drain_stage(s_stage, ctot, o, lane);
+    return ctot;
+}
+
+// KB4: one bucket per CTA iteration (dynamic ticket). SMEM bitset of 2^shift
+// bits; warp w owns words [w*W/32, (w+1)*W/32) and extracts them in order
+// (see phase 2) straight to the output slots of the bucket. Every key of a
+// bucket lands in [base_b, base_b + tot_b) (tot_b counts duplicates too), so
+// no output bounds checks are needed.
+__global__ void __launch_bounds__(BUCKET_THREADS, 2)
+    bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
+                       const unsigned long long* __restrict__ g_base, int shift, int nb,
+                       uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t W = 1u << (shift - 5);  // words per bucket bitset (>= 1024)
+    uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* s_stage_all = s_bits + W;  // BUCKET_THREADS/32 x (BUCKET_STAGE + BUCKET_STAGE/32)
+    __shared__ uint32_t s_warp[BUCKET_THREADS / 32];
+    __shared__ unsigned s_b;
+
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned warp = threadIdx.x >> 5;
+    constexpr int kStagePitch = BUCKET_STAGE + BUCKET_STAGE / 32;
+    uint32_t* s_stage = s_stage_all + warp * kStagePitch;
+    const uint32_t seg_words = W / (BUCKET_THREADS / 32);
+    const uint32_t lowmask = (1u << shift) - 1;
+    const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
+
+    for (;;) {
+        if (threadIdx.x == 0) s_b = atomicAdd(&ctrl->ticket, 1u);
+        // zero the bitset (the previous bucket's readers finished at the loop-end barrier)
+        uint4* b4 = reinterpret_cast<uint4*>(s_bits);
+        for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        const unsigned b = s_b;
+        if (b >= static_cast<unsigned>(nb)) break;
+        const unsigned long long base = g_base[b];
+        const uint32_t cnt = tot[b];
+        const uint32_t* src = parted + base;
+        {
+            constexpr int U = 8;
+            constexpr uint32_t kBatch = BUCKET_THREADS * U;
+            uint32_t i0 = 0;
+            for (; i0 + kBatch <= cnt; i0 += kBatch) {
+                uint32_t k[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) k[u] = __ldcs(src + i0 + u * BUCKET_THREADS + threadIdx.x);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t x = k[u] & lowmask;
+                    atomicOr(s_bits + (x >> 5), 1u << (x & 31));
+                }
+            }
+            for (uint32_t i = i0 + threadIdx.x; i < cnt; i += BUCKET_THREADS) {
+                const uint32_t x = __ldcs(src + i) & lowmask;
+                atomicOr(s_bits + (x >> 5), 1u << (x & 31));
+            }
+        }
+        __syncthreads();
+        // phase 1: per-warp popcount of its segment (128-bit SMEM reads)
+        const uint32_t seg = warp * seg_words;
+        uint32_t c = 0;
+        for (uint32_t i = lane; i < seg_words / 4; i += 32) {
+            const uint4 v = s4[seg / 4 + i];
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+        c = __reduce_add_sync(kFull, c);
+        if (lane == 0) s_warp[warp] = c;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = s_warp[lane];
+            const uint32_t incl = warp_incl_scan(v, lane);
+            s_warp[lane] = incl - v;
+            if (lane == 31 && incl) atomicAdd(&ctrl->total, static_cast<unsigned long long>(incl));
+        }
+        __syncthreads();
+        // phase 2: extraction. 128-word steps, lane-major (lane owns 4 words):
+        // an empty step costs ~20 instructions; a step with <= BUCKET_STAGE
+        // keys is extracted in one pass; denser steps fall back to four
+        // 32-word sub-steps (word per lane).
+        uint32_t* o = out + base + s_warp[warp];
+        const uint32_t key_hi = static_cast<uint32_t>(b) << shift;
+        if (seg_words >= 128) {
+            for (uint32_t w0 = 0; w0 < seg_words; w0 += 128) {
+                const uint4 v = s4[(seg + w0) / 4 + lane];
+                const uint32_t cl = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+                const uint32_t incl = warp_incl_scan(cl, lane);
+                const uint32_t ctot = __shfl_sync(kFull, incl, 31);
+                if (ctot == 0) continue;
+                if (ctot <= static_cast<uint32_t>(BUCKET_STAGE)) {
+                    uint32_t p = incl - cl;
+                    const uint32_t kb = key_hi + ((seg + w0 + 4 * lane) << 5);
+                    stage_bits(v.x, kb, p, s_stage);
+                    stage_bits(v.y, kb + 32, p, s_stage);
+                    stage_bits(v.z, kb + 64, p, s_stage);
+                    stage_bits(v.w, kb + 96, p, s_stage);
+                    drain_stage(s_stage, ctot, o, lane);
+                    o += ctot;
+                    continue;
+                }
+#pragma unroll 1
+                for (uint32_t q = 0; q < 128; q += 32)
+                    o += extract_words32(s_bits, seg + w0 + q, key_hi, o, s_stage, lane);
+            }
+        } else {
+            for (uint32_t w0 = 0; w0 < seg_words; w0 += 32)
+                o += extract_words32(s_bits, seg + w0, key_hi, o, s_stage, lane);
+        }
+        __syncthreads();
+    }
+}
+
+// K0: max key (only when no key-range hint is given).
+__global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl* __restrict__ ctrl) {
+    uint32_t mx = 0;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+        mx = max(mx, __ldcs(keys + i));
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(&ctrl->max_key, mx);
+}
+
+}  // namespace
+
+cudaError_t launch_key_max(const uint32_t* keys, size_t n, Ctrl* ctrl, const LaunchGeometry& geo,
+                           cudaStream_t stream) {
+    key_max_kernel<<<geo.fill_blocks, 256, 0, stream>>>(keys, n, ctrl);
+    return cudaGetLastError();
+}
+
+BucketPlan plan_buckets(uint64_t key_range) {
+    BucketPlan p;
+    int log2m = 0;
+    while ((1ull << log2m) < key_range) ++log2m;
+    int shift = log2m - 10;
+    if (shift > MAX_BUCKET_SHIFT) shift = MAX_BUCKET_SHIFT;
+    if (shift < MIN_BUCKET_SHIFT) shift = MIN_BUCKET_SHIFT;
+    p.shift = shift;
+    const uint64_t nb = (key_range + (1ull << shift) - 1) >> shift;
+    p.nb = static_cast<int>(nb < 1 ? 1 : nb);
+    return p;
+}
+
+size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
+    return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H
+           + MAX_BUCKETS * sizeof(uint32_t)                                // tot
+           + (MAX_BUCKETS + 1) * sizeof(unsigned long long);               // base
+}
+
+cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* out,
+                               uint32_t* parted, void* scratch, Ctrl* ctrl, const BucketPlan& plan,
+                               const LaunchGeometry& geo, cudaStream_t stream, int* launches,
+                               KernelTimer* timer) {
+    if (n == 0) return cudaSuccess;
+    const int P = geo.part_blocks;
+    uint32_t* H = static_cast<uint32_t*>(scratch);
+    uint32_t* tot = H + static_cast<size_t>(P) * plan.nb;
+    unsigned long long* base =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(tot + MAX_BUCKETS + 1) & ~uintptr_t(7));
+    const int check = key_range < (1ull << 32);
+    const uint32_t limit = check ? static_cast<uint32_t>(key_range) : 0u;
+    KeySplit ks;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
+    size_t n_head = ((16 - (addr & 15)) & 15) / 4;
+    if (n_head > n) n_head = n;
+    ks.nv = (n - n_head) / 4;
+    ks.body = reinterpret_cast<const uint4*>(keys + n_head);
+    ks.head = keys;
+    ks.n_head = static_cast<int>(n_head);
+    ks.tail = keys + n_head + 4 * ks.nv;
+    ks.n_tail = static_cast<int>(n - n_head - 4 * ks.nv);
+
+    cudaError_t err = cudaMemsetAsync(H, 0, static_cast<size_t>(P) * plan.nb * sizeof(uint32_t), stream);
+    if (err != cudaSuccess) return err;
+    if (timer) timer->before(stream);
+    bucket_hist_kernel<<<P * HIST_SPLIT, BUCKET_HIST_THREADS, 0, stream>>>(ks, plan.shift, plan.nb,
+                                                                           limit, check, H, ctrl);
+    if (timer) timer->after("bucket_hist", stream);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    if (timer) timer->before(stream);
+    bucket_colscan_kernel<<<(plan.nb * 32 + 255) / 256, 256, 0, stream>>>(H, P, plan.nb, tot);
+    if (timer) timer->after("bucket_colscan", stream);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if (timer) timer->before(stream);
+    bucket_partition_kernel<<<P, PART_THREADS, part_smem_bytes(), stream>>>(
+        ks, plan.shift, plan.nb, H, tot, parted, base);
+    if (timer) timer->after("bucket_partition", stream);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    const size_t smem = bucket_sort_smem_bytes(plan.shift);
+    if (timer) timer->before(stream);
+    bucket_sort_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
+        parted, tot, base, plan.shift, plan.nb, out, ctrl);
+    if (timer) timer->after("bucket_sort", stream);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if (launches) *launches = 4;
+    return cudaSuccess;
+}
+
+cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
+    int sms = 0;
+    cudaError_t err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes()));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(bucket_sort_smem_bytes(20)));
+    if (err != cudaSuccess) return err;
+    int per = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_partition_kernel, PART_THREADS,
+                                                        part_smem_bytes());
+    if (err != cudaSuccess) return err;
+    geo->part_blocks = sms * (per > 0 ? per : 1);
+    for (int shift = MIN_BUCKET_SHIFT; shift <= MAX_BUCKET_SHIFT; ++shift) {
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel, BUCKET_THREADS,
+                                                            bucket_sort_smem_bytes(shift));
+        if (err != cudaSuccess) return err;
+        geo->bucket_blocks[shift] = sms * (per > 0 ? per : 1);
+    }
+    return cudaSuccess;
+}
+
+}  // namespace bws_gpu

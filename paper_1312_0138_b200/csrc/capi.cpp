@@ -18,6 +18,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -82,6 +84,19 @@ constexpr size_t kCtrlBytes = sizeof(Ctrl) + kMaxTiles * sizeof(unsigned long lo
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_scatter_mode{bws_gpu::kAuto};
 std::atomic<int> g_device_count{0};  // 0 = not yet resolved
+std::atomic<int> g_path{-1};         // bws_path; -1 = not yet read from BITSORT_PATH
+constexpr size_t kBucketedMinKeys = size_t(1) << 21;
+
+int current_path() {
+    int p = g_path.load();
+    if (p >= 0) return p;
+    const char* env = std::getenv("BITSORT_PATH");
+    p = BWS_PATH_AUTO;
+    if (env && std::strcmp(env, "direct") == 0) p = BWS_PATH_DIRECT;
+    if (env && std::strcmp(env, "bucketed") == 0) p = BWS_PATH_BUCKETED;
+    g_path.store(p);
+    return p;
+}
 
 struct DeviceCtx {
     std::mutex mu;
@@ -94,6 +109,9 @@ struct DeviceCtx {
     unsigned char* ctrl_mem = nullptr;  // Ctrl followed by the K3 tile-status array
     uint32_t* keys = nullptr;           // staging for host arrays
     size_t keys_cap = 0;
+    uint32_t* parted = nullptr;         // bucketed path: keys grouped by bucket
+    size_t parted_cap = 0;
+    void* bucket_scratch = nullptr;     // bucketed path: histograms, totals, bases
     size_t last_count = 0;        // count of the last async device sort (bws_gpu_sort_check)
     uint64_t last_range = 0;      // its key range (0 = derived)
     cudaEvent_t done = nullptr;   // recorded after every queued sort: orders the
@@ -109,10 +127,15 @@ struct DeviceCtx {
         device = dev;
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         cuda_check(bws_gpu::query_geometry(dev, &geo), "occupancy query");
+        cuda_check(bws_gpu::configure_bucket_kernels(dev, &geo), "bucket kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaMalloc(&bits, kMaxWords * sizeof(uint32_t)), "cudaMalloc(bitset 512 MiB)");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes), "cudaMalloc(control block)");
         cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
+        bws_gpu::BucketPlan widest;
+        widest.nb = bws_gpu::MAX_BUCKETS;
+        cuda_check(cudaMalloc(&bucket_scratch, bws_gpu::bucket_scratch_bytes(widest, geo.part_blocks) + 64),
+                   "cudaMalloc(bucket scratch)");
         bits_dirty = true;
         ready = true;
     }
@@ -127,6 +150,16 @@ struct DeviceCtx {
         keys_cap = cap;
     }
 
+    void ensure_parted(size_t n) {
+        if (n <= parted_cap) return;
+        if (parted) cuda_check(cudaFree(parted), "cudaFree(parted)");
+        parted = nullptr;
+        parted_cap = 0;
+        const size_t cap = n + n / 8;
+        cuda_check(cudaMalloc(&parted, cap * sizeof(uint32_t)), "cudaMalloc(bucket keys)");
+        parted_cap = cap;
+    }
+
     void release() {
         if (!ready) return;
         cudaSetDevice(device);
@@ -134,6 +167,11 @@ struct DeviceCtx {
         cudaFree(bits);
         cudaFree(ctrl_mem);
         if (keys) cudaFree(keys);
+        if (parted) cudaFree(parted);
+        if (bucket_scratch) cudaFree(bucket_scratch);
+        parted = nullptr;
+        parted_cap = 0;
+        bucket_scratch = nullptr;
         if (stream) cudaStreamDestroy(stream);
         if (done) cudaEventDestroy(done);
         done = nullptr;
@@ -145,6 +183,75 @@ struct DeviceCtx {
         ready = false;
     }
 };
+
+// Per-kernel CUDA-event timing (bws_gpu_set_kernel_timing): events bracket
+// each launch on its stream; bws_gpu_kernel_timings() resolves and sums them.
+struct EventTimer final : bws_gpu::KernelTimer {
+    std::mutex mu;
+    std::atomic<bool> enabled{false};
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t open = nullptr;
+
+    cudaEvent_t get() {
+        cudaEvent_t e = nullptr;
+        if (!pool.empty()) {
+            e = pool.back();
+            pool.pop_back();
+        } else {
+            cuda_check(cudaEventCreate(&e), "cudaEventCreate(timer)");
+        }
+        return e;
+    }
+    void before(cudaStream_t s) override {
+        std::lock_guard<std::mutex> lock(mu);
+        open = get();
+        cuda_check(cudaEventRecord(open, s), "cudaEventRecord(timer)");
+    }
+    void after(const char* name, cudaStream_t s) override {
+        std::lock_guard<std::mutex> lock(mu);
+        cudaEvent_t b = get();
+        cuda_check(cudaEventRecord(b, s), "cudaEventRecord(timer)");
+        pending.push_back({name, open, b});
+        open = nullptr;
+    }
+    std::string collect() {
+        std::lock_guard<std::mutex> lock(mu);
+        std::map<std::string, std::pair<uint64_t, double>> acc;
+        for (const Rec& r : pending) {
+            cuda_check(cudaEventSynchronize(r.b), "timer event");
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+            auto& slot = acc[r.name];
+            slot.first += 1;
+            slot.second += ms;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+        std::string out;
+        for (const auto& [name, v] : acc)
+            out += name + " " + std::to_string(v.first) + " " + std::to_string(v.second) + "\n";
+        return out;
+    }
+};
+EventTimer g_timer;
+
+bws_gpu::KernelTimer* active_timer() { return g_timer.enabled.load() ? &g_timer : nullptr; }
+
+// Brackets one direct-path launch with the timer when it is enabled.
+template <class F>
+cudaError_t timed_launch(const char* name, cudaStream_t s, F&& launch) {
+    bws_gpu::KernelTimer* t = active_timer();
+    if (t) t->before(s);
+    const cudaError_t err = launch();
+    if (t) t->after(name, s);
+    return err;
+}
 
 constexpr int kMaxDevices = 64;
 DeviceCtx g_ctx[kMaxDevices];
@@ -177,8 +284,8 @@ int current_device() {
 // `stream`: [bitset reset if dirty] -> control/status reset -> K2 -> K3.
 // Caller holds ctx.mu. key_range == 0 derives the range from the keys (K2
 // folds the max key; K3 scans (max >> 5) + 1 words).
-void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
-                  uint64_t key_range, cudaStream_t stream) {
+void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
+                    uint64_t key_range, cudaStream_t stream) {
     const bool derived = key_range == 0;
     const uint64_t words = derived ? 0 : (key_range + 31) / 32;
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
@@ -192,16 +299,62 @@ void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* 
                                stream),
                "control block reset");
     ctx.bits_dirty = true;
-    cuda_check(bws_gpu::launch_scatter(keys, count, ctx.bits, derived ? kMaxKeyRange : key_range,
-                                       ctx.ctrl(), g_scatter_mode.load(), ctx.geo, stream),
+    cuda_check(timed_launch("bitset_scatter", stream,
+                            [&] {
+                                return bws_gpu::launch_scatter(
+                                    keys, count, ctx.bits, derived ? kMaxKeyRange : key_range,
+                                    ctx.ctrl(), g_scatter_mode.load(), ctx.geo, stream);
+                            }),
                "bitset_scatter launch");
     g_launches.fetch_add(1);
-    cuda_check(bws_gpu::launch_scan(ctx.bits, words, 0u, out, count, ctx.ctrl(), ctx.status(),
-                                    nullptr, /*clear=*/1, ctx.geo, stream),
+    cuda_check(timed_launch("bitset_scan", stream,
+                            [&] {
+                                return bws_gpu::launch_scan(ctx.bits, words, 0u, out, count,
+                                                            ctx.ctrl(), ctx.status(), nullptr,
+                                                            /*clear=*/1, ctx.geo, stream);
+                            }),
                "bitset_scan launch");
     g_launches.fetch_add(1);
     ctx.bits_dirty = false;  // K3 zeroes every word it reads; all set bits lie in its range
     cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
+}
+
+// Bucketed pipeline: [K0 max + host readback when no hint] -> KB1..KB4.
+// Leaves the cached bitset untouched.
+void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
+                      uint64_t key_range, cudaStream_t stream) {
+    cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
+    cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
+    if (key_range == 0) {
+        cuda_check(bws_gpu::launch_key_max(keys, count, ctx.ctrl(), ctx.geo, stream), "key_max launch");
+        g_launches.fetch_add(1);
+        unsigned int mx = 0;
+        cuda_check(cudaMemcpyAsync(&mx, &ctx.ctrl()->max_key, sizeof(mx), cudaMemcpyDeviceToHost, stream),
+                   "max key readback");
+        cuda_check(cudaStreamSynchronize(stream), "key_max execution");
+        key_range = static_cast<uint64_t>(mx) + 1;
+    }
+    ctx.ensure_parted(count);
+    const bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range);
+    int launches = 0;
+    cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
+                                           ctx.ctrl(), plan, ctx.geo, stream, &launches,
+                                           active_timer()),
+               "bucketed sort launch");
+    g_launches.fetch_add(static_cast<uint64_t>(launches));
+    cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
+}
+
+void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
+                  uint64_t key_range, cudaStream_t stream) {
+    const int path = current_path();
+    // bucket slots are 32-bit: the bucketed pipeline takes n < 2^32
+    const bool bucketed = count < (size_t(1) << 32) &&
+                          (path == BWS_PATH_BUCKETED || (path == BWS_PATH_AUTO && count >= kBucketedMinKeys));
+    if (bucketed)
+        enqueue_bucketed(ctx, keys, count, out, key_range, stream);
+    else
+        enqueue_direct(ctx, keys, count, out, key_range, stream);
 }
 
 // Synchronises and turns the control block into a status: out-of-range keys
@@ -392,8 +545,12 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
         cuda_check(cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), s), "bitset clear");
         cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
-        cuda_check(bws_gpu::launch_scatter(keys, count, bits, key_range, ctx.ctrl(),
-                                           g_scatter_mode.load(), ctx.geo, s),
+        cuda_check(timed_launch("bitset_scatter", s,
+                                [&] {
+                                    return bws_gpu::launch_scatter(keys, count, bits, key_range,
+                                                                   ctx.ctrl(), g_scatter_mode.load(),
+                                                                   ctx.geo, s);
+                                }),
                    "bitset_scatter launch");
         g_launches.fetch_add(1);
         cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
@@ -422,10 +579,13 @@ bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t 
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0,
                                    sizeof(Ctrl) + tiles * sizeof(unsigned long long), s),
                    "control block reset");
-        cuda_check(bws_gpu::launch_scan(bits, n_words, key_base, out, out_capacity, ctx.ctrl(),
-                                        ctx.status(),
-                                        reinterpret_cast<unsigned long long*>(d_total),
-                                        /*clear=*/0, ctx.geo, s),
+        cuda_check(timed_launch("bitset_scan", s,
+                                [&] {
+                                    return bws_gpu::launch_scan(
+                                        bits, n_words, key_base, out, out_capacity, ctx.ctrl(),
+                                        ctx.status(), reinterpret_cast<unsigned long long*>(d_total),
+                                        /*clear=*/0, ctx.geo, s);
+                                }),
                    "bitset_scan launch");
         g_launches.fetch_add(1);
         cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
@@ -437,6 +597,13 @@ bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode) {
         if (mode < BWS_SCATTER_AUTO || mode > BWS_SCATTER_SMEM)
             throw config_error("unknown scatter mode");
         g_scatter_mode.store(static_cast<int>(mode));
+    });
+}
+
+bws_status bws_gpu_set_path(bws_path path) {
+    return wrap([&] {
+        if (path < BWS_PATH_AUTO || path > BWS_PATH_BUCKETED) throw config_error("unknown path");
+        g_path.store(static_cast<int>(path));
     });
 }
 
@@ -456,6 +623,21 @@ int bws_gpu_device_count(void) {
 }
 
 uint64_t bws_gpu_launch_count(void) { return g_launches.load(); }
+
+bws_status bws_gpu_set_kernel_timing(int enable) {
+    return wrap([&] { g_timer.enabled.store(enable != 0); });
+}
+
+bws_status bws_gpu_kernel_timings(char* buf, size_t buf_size) {
+    return wrap([&] {
+        if (buf == nullptr || buf_size == 0) throw config_error("null output buffer");
+        const std::string text = g_timer.collect();
+        if (text.size() + 1 > buf_size)
+            throw config_error("output buffer too small: need " + std::to_string(text.size() + 1) +
+                               " bytes");
+        std::memcpy(buf, text.c_str(), text.size() + 1);
+    });
+}
 
 void bws_gpu_shutdown(void) {
     for (auto& ctx : g_ctx) {

@@ -39,10 +39,56 @@ inline std::size_t scan_tiles(std::uint64_t n_words) {
     return static_cast<std::size_t>((n_words + SCAN_TILE_WORDS - 1) / SCAN_TILE_WORDS);
 }
 
+// Bucketed pipeline geometry (bucket.cu).
+constexpr int MAX_BUCKETS = 4096;
+constexpr int MIN_BUCKET_SHIFT = 15;  // SMEM bitset of a bucket: 2^shift bits
+constexpr int MAX_BUCKET_SHIFT = 20;  // 128 KB
+constexpr int BUCKET_HIST_THREADS = 512;
+constexpr int HIST_SPLIT = 4;  // histogram CTAs per partition CTA share
+constexpr int PART_THREADS = 1024;
+constexpr int PART_KPT = 16;
+constexpr int PART_TILE = PART_THREADS * PART_KPT;  // 16384 keys per partition tile
+constexpr int BUCKET_THREADS = 1024;
+constexpr int BUCKET_STAGE = 512;  // keys per warp in the extraction stage
+
+constexpr std::size_t part_smem_bytes() {
+    return 2 * PART_TILE * 4 + (MAX_BUCKETS + 1) * (4 + 4 + 4 + 4);  // TMA ring + 4 slot arrays
+}
+constexpr std::size_t bucket_sort_smem_bytes(int shift) {
+    return (std::size_t(1) << (shift - 3)) +
+           (BUCKET_THREADS / 32) * (BUCKET_STAGE + BUCKET_STAGE / 32) * 4;
+}
+
 struct LaunchGeometry {
     int scatter_blocks = 0;
     int scan_blocks = 0;
     int fill_blocks = 0;
+    int part_blocks = 0;                         // KB1/KB3 CTAs (same chunking)
+    int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
+};
+
+// A key array as seen by the bucketed kernels: 16-byte-aligned uint4 body plus
+// up to 3 misaligned head and 3 tail keys.
+struct KeySplit {
+    const uint4* body = nullptr;
+    std::size_t nv = 0;
+    const std::uint32_t* head = nullptr;
+    int n_head = 0;
+    const std::uint32_t* tail = nullptr;
+    int n_tail = 0;
+};
+
+struct BucketPlan {
+    int shift = 20;  // bucket = key >> shift
+    int nb = 1;      // number of buckets, <= MAX_BUCKETS
+};
+
+// Optional per-kernel timing hook (bench.py's live roofline): before() and
+// after() bracket every kernel launch on the launching stream.
+struct KernelTimer {
+    virtual void before(cudaStream_t stream) = 0;
+    virtual void after(const char* kernel, cudaStream_t stream) = 0;
+    virtual ~KernelTimer() = default;
 };
 
 // Computes persistent-grid sizes (SM count x resident blocks) for `device`.
@@ -65,5 +111,21 @@ cudaError_t launch_scan(const std::uint32_t* bits, std::uint64_t n_words, std::u
                         std::uint32_t* out, std::uint64_t out_capacity, Ctrl* ctrl,
                         unsigned long long* status, unsigned long long* d_total, int clear,
                         const LaunchGeometry& geo, cudaStream_t stream);
+
+// Bucketed pipeline (bucket.cu). plan_buckets picks the bucket width for a
+// key range; bucket_scratch_bytes sizes the histogram/offset scratch.
+BucketPlan plan_buckets(std::uint64_t key_range);
+std::size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks);
+cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo);
+// KB1..KB4: sorts n keys (all < key_range) into out via the `parted` buffer
+// (n keys). Adds the number of distinct keys to ctrl->total, counts keys >=
+// key_range in ctrl->bad_keys. `launches` receives the kernel count.
+cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::uint64_t key_range,
+                               std::uint32_t* out, std::uint32_t* parted, void* scratch, Ctrl* ctrl,
+                               const BucketPlan& plan, const LaunchGeometry& geo,
+                               cudaStream_t stream, int* launches, KernelTimer* timer = nullptr);
+// K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
+cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
+                           const LaunchGeometry& geo, cudaStream_t stream);
 
 }  // namespace bws_gpu

@@ -27,6 +27,10 @@ def capi(cuda):
 def _auto_mode(capi):
     yield
     capi.set_scatter_mode(capi.ScatterMode.AUTO)
+    capi.set_path(capi.Path.AUTO)
+
+
+PATHS = ["DIRECT", "BUCKETED"]
 
 
 def gpu_sort_host(capi, keys: np.ndarray) -> np.ndarray:
@@ -46,9 +50,11 @@ def gpu_sort_device(capi, torch, keys: np.ndarray, offset: int = 0) -> np.ndarra
 
 # --- golden vectors from the reference ------------------------------------
 
-def test_acceptance_golden_vectors(capi, acceptance_records):
+@pytest.mark.parametrize("path", PATHS)
+def test_acceptance_golden_vectors(capi, acceptance_records, path):
     """acceptance.cpp:65-95 criterion-2 inputs (uint32 arm) vs the reference's
     bws_sort output; inputs with duplicate draws must be rejected untouched."""
+    capi.set_path(getattr(capi.Path, path))
     checked = rejected = 0
     for rec in acceptance_records:
         a = rec["input"].copy()
@@ -64,7 +70,9 @@ def test_acceptance_golden_vectors(capi, acceptance_records):
     assert checked >= 60
 
 
-def test_edge_golden_vectors(capi, cuda, edge_records):
+@pytest.mark.parametrize("path", PATHS)
+def test_edge_golden_vectors(capi, cuda, edge_records, path):
+    capi.set_path(getattr(capi.Path, path))
     for rec in edge_records:
         assert np.array_equal(gpu_sort_host(capi, rec["input"]), rec["output"])
         assert np.array_equal(gpu_sort_device(capi, cuda, rec["input"]), rec["output"])
@@ -79,7 +87,9 @@ def test_capi_uint8_vector_widened(capi):
 
 # --- the ABI conventions on a GPU ----------------------------------------
 
-def test_status_conventions(capi):
+@pytest.mark.parametrize("path", PATHS)
+def test_status_conventions(capi, path):
+    capi.set_path(getattr(capi.Path, path))
     a = np.array([5, 1, 5], dtype=np.uint32)
     assert capi.sort_raw(a.ctypes.data, 3, 32, 1, 0) == capi.Status.ERROR_DATA
     assert "distinct" in capi.last_error()
@@ -93,7 +103,9 @@ def test_status_conventions(capi):
     assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.PLATFORM) == capi.Status.ERROR_CONFIG
 
 
-def test_range_hint(capi):
+@pytest.mark.parametrize("path", PATHS)
+def test_range_hint(capi, path):
+    capi.set_path(getattr(capi.Path, path))
     keys = np.array([9, 0, 15, 3], dtype=np.uint32)
     a = keys.copy()
     capi.sort_u32_range(a, 16)
@@ -114,9 +126,11 @@ def test_range_hint(capi):
 
 # --- random / ragged / aligned cases vs the oracle -------------------------
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 31, 32, 33, 100, 1000, 4095, 4096, 4097, 65537])
 @pytest.mark.parametrize("key_range", [1 << 12, 1 << 20, 1 << 32])
-def test_random_distinct_vs_oracle(capi, cuda, n, key_range):
+def test_random_distinct_vs_oracle(capi, cuda, n, key_range, path):
+    capi.set_path(getattr(capi.Path, path))
     if n > key_range:
         pytest.skip("n > key_range")
     rng = np.random.default_rng(n * 7919 + key_range % 1000003)
@@ -132,10 +146,16 @@ def test_random_distinct_vs_oracle(capi, cuda, n, key_range):
     assert np.array_equal(a, expected)
 
 
-@pytest.mark.parametrize("mode", ["AUTO", "PLAIN", "WARP_AGG", "SMEM"])
+@pytest.mark.parametrize("mode", ["AUTO", "PLAIN", "WARP_AGG", "SMEM", "BUCKETED"])
 @pytest.mark.parametrize("layout", ["shuffled", "sorted", "reverse", "runs", "clustered"])
 def test_scatter_modes(capi, mode, layout):
-    """Warp aggregation and SMEM staging (K2 paths) give identical bitsets."""
+    """Warp aggregation and SMEM staging (K2 paths) and the bucketed pipeline
+    give identical results on shuffled, sorted and cluster-ordered layouts."""
+    if mode == "BUCKETED":
+        capi.set_path(capi.Path.BUCKETED)
+        mode = "AUTO"
+    else:
+        capi.set_path(capi.Path.DIRECT)
     rng = np.random.default_rng(5)
     n = 300_000
     if layout == "clustered":
@@ -162,8 +182,10 @@ def test_scatter_modes(capi, mode, layout):
     assert np.array_equal(a, expected)
 
 
-def test_dense_identity(capi, cuda):
+@pytest.mark.parametrize("path", PATHS)
+def test_dense_identity(capi, cuda, path):
     """n == M: every word full, output is the identity (dense extraction path)."""
+    capi.set_path(getattr(capi.Path, path))
     n = 1 << 22
     keys = np.random.default_rng(1).permutation(n).astype(np.uint32)
     t = cuda.from_numpy(keys.view(np.int32)).cuda()
@@ -172,14 +194,18 @@ def test_dense_identity(capi, cuda):
     assert cuda.equal(t.cpu(), cuda.arange(n, dtype=cuda.int32))
 
 
-def test_top_of_range(capi):
+@pytest.mark.parametrize("path", PATHS)
+def test_top_of_range(capi, path):
+    capi.set_path(getattr(capi.Path, path))
     keys = (np.uint32(0xFFFFFFFF) - np.arange(5000, dtype=np.uint32) * np.uint32(7)).astype(np.uint32)
     a = keys[::-1].copy()
     capi.sort(a)
     assert np.array_equal(a, np.sort(keys))
 
 
-def test_duplicates_rejected_at_scale(capi):
+@pytest.mark.parametrize("path", PATHS)
+def test_duplicates_rejected_at_scale(capi, path):
+    capi.set_path(getattr(capi.Path, path))
     keys = np.random.default_rng(3).choice(1 << 24, size=1 << 20, replace=False).astype(np.uint32)
     keys[777] = keys[123456]
     a = keys.copy()
@@ -189,7 +215,9 @@ def test_duplicates_rejected_at_scale(capi):
 
 # --- device-resident async API and the multi-rank building blocks ----------
 
-def test_device_async_and_check(capi, cuda):
+@pytest.mark.parametrize("path", PATHS)
+def test_device_async_and_check(capi, cuda, path):
+    capi.set_path(getattr(capi.Path, path))
     keys = np.random.default_rng(11).choice(1 << 28, size=1 << 20, replace=False).astype(np.uint32)
     src = cuda.from_numpy(keys.view(np.int32)).cuda()
     out = cuda.empty_like(src)
@@ -228,9 +256,10 @@ def test_rank_building_blocks_emulated(capi, cuda, world):
 
 # --- full-size BASELINE configs -------------------------------------------
 
-def _config_sort(capi, cuda, name):
+def _config_sort(capi, cuda, name, path="AUTO"):
     from paper_1312_0138_b200.configs import CONFIGS
 
+    capi.set_path(getattr(capi.Path, path))
     cfg = CONFIGS[name]
     keys = cfg.generate()
     t = cuda.from_numpy(keys.view(np.int32)).cuda()
@@ -241,9 +270,11 @@ def _config_sort(capi, cuda, name):
     return cfg, keys, out
 
 
-def test_c1_vs_reference(capi, cuda, anchors):
+@pytest.mark.parametrize("path", PATHS)
+def test_c1_vs_reference(capi, cuda, anchors, path):
     from paper_1312_0138_b200.configs import CONFIGS
 
+    capi.set_path(getattr(capi.Path, path))
     cfg = CONFIGS["C1"]
     keys = cfg.generate()
     assert fnv1a64(keys) == anchors["C1"]["fnv1a64_input"]
@@ -253,25 +284,28 @@ def test_c1_vs_reference(capi, cuda, anchors):
     assert np.array_equal(a, bitwise_sort(keys))
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["C2", "C4"])
-def test_config_vs_reference_hash(capi, cuda, anchors, name):
-    cfg, keys, out = _config_sort(capi, cuda, name)
+def test_config_vs_reference_hash(capi, cuda, anchors, name, path):
+    cfg, keys, out = _config_sort(capi, cuda, name, path)
     assert fnv1a64(keys) == anchors[name]["fnv1a64_input"]
     got = out.cpu().numpy().view(np.uint32)
     assert fnv1a64(got) == anchors[name]["fnv1a64_sorted"]
 
 
-def test_c3_dense_permutation(capi, cuda):
-    cfg, keys, out = _config_sort(capi, cuda, "C3")
+@pytest.mark.parametrize("path", PATHS)
+def test_c3_dense_permutation(capi, cuda, path):
+    cfg, keys, out = _config_sort(capi, cuda, "C3", path)
     del keys
     assert cuda.equal(out, cuda.arange(cfg.n, dtype=cuda.int32, device="cuda"))
 
 
-def test_c5_clustered_properties(capi, cuda):
+@pytest.mark.parametrize("path", PATHS)
+def test_c5_clustered_properties(capi, cuda, path):
     """Size-independent properties: strictly ascending, same count, and the same
     sum and sum-of-squares (mod 2^64) as the input: together a permutation check
     for a strictly ascending output."""
-    cfg, keys, out = _config_sort(capi, cuda, "C5")
+    cfg, keys, out = _config_sort(capi, cuda, "C5", path)
     u = out.to(cuda.int64) & 0xFFFFFFFF
     assert u.numel() == cfg.n
     assert bool((u[1:] > u[:-1]).all())

@@ -38,7 +38,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C4")
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--modes", default="AUTO,PLAIN")
+    ap.add_argument("--modes", default="AUTO")
+    ap.add_argument("--paths", default="DIRECT,BUCKETED")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     flush = torch.empty(1 << 26, dtype=torch.int32, device="cuda")
@@ -51,8 +52,9 @@ def main():
         words = (cfg.key_range + 31) // 32
         bits = torch.empty(words, dtype=torch.int32, device="cuda")
         total = torch.zeros(1, dtype=torch.int64, device="cuda")
-        for mode in args.modes.split(","):
+        for mode, path in [(m, p) for p in args.paths.split(",") for m in args.modes.split(",")]:
             capi.set_scatter_mode(getattr(capi.ScatterMode, mode))
+            capi.set_path(getattr(capi.Path, path))
             build = lambda: capi.bitset_build(keys.data_ptr(), cfg.n, bits.data_ptr(), cfg.key_range, stream)
             scan = lambda: capi.bitset_scan(bits.data_ptr(), words, 0, out.data_ptr(), cfg.n, total.data_ptr(), stream)
             full = lambda: capi.sort_device_async(keys.data_ptr(), cfg.n, out.data_ptr(), cfg.key_range, stream)
@@ -64,7 +66,7 @@ def main():
             tf = timed(full, flush, args.iters)
             ok = capi.sort_check(stream) == cfg.n
             gbs = cfg.alg_bytes / tf[0] / 1e9
-            print(json.dumps({"config": name, "mode": mode, "n": cfg.n, "M": cfg.key_range,
+            print(json.dumps({"config": name, "mode": mode, "path": path, "n": cfg.n, "M": cfg.key_range,
                               "build_us": round(tb[0] * 1e6, 1), "scan_us": round(ts[0] * 1e6, 1),
                               "sort_us": round(tf[0] * 1e6, 1), "sort_min_us": round(tf[1] * 1e6, 1),
                               "gkeys_s": round(cfg.n / tf[0] / 1e9, 2), "alg_GBps": round(gbs, 1),
