@@ -25,6 +25,9 @@
 // M-proportional term. Duplicate keys are detected by sum(popcount) < n.
 #include "kernels.h"
 
+#include <cstdlib>
+#include <string>
+
 namespace bws_gpu {
 namespace {
 
@@ -255,14 +258,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // tile buffer, then thread i stores sorted key i to parted[delta[bucket] + i]:
 // consecutive threads write consecutive addresses within each bucket run.
 // Slot positions are 32-bit (the bucketed path requires n < 2^32).
-__global__ void __launch_bounds__(PART_THREADS, 1)
+template <int THREADS, int KPT, int MAXB>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     bucket_partition_kernel(KeySplit ks, int shift, int nb,
                             const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
                             uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int kSlots = MAX_BUCKETS + 1;
-    uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 x PART_TILE
-    uint32_t* s_cnt = s_buf + 2 * PART_TILE;                   // keys per bucket in the tile
+    constexpr int kSlots = MAXB + 1;
+    constexpr int TILE = THREADS * KPT;
+    constexpr int NWARPS = THREADS / 32;
+    uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 x TILE
+    uint32_t* s_cnt = s_buf + 2 * TILE;                   // keys per bucket in the tile
     uint32_t* s_start = s_cnt + kSlots;                        // tile-local bucket start
     uint32_t* s_cur = s_start + kSlots;                        // next free global slot
     uint32_t* s_delta = s_cur + kSlots;                        // global slot - local index
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
     const unsigned P = gridDim.x, c = blockIdx.x;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t vlo = ks.nv * c / P, vhi = ks.nv * (c + 1) / P;
-    constexpr size_t kTileVec = PART_TILE / 4;
+    constexpr size_t kTileVec = TILE / 4;
     const size_t ntiles = (vhi - vlo + kTileVec - 1) / kTileVec;
     const uint32_t spill = static_cast<uint32_t>(nb);
 
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         for (size_t t = 0; t < 2 && t < ntiles; ++t) {
             const size_t v0 = vlo + t * kTileVec;
             const size_t nvec = min(kTileVec, vhi - v0);
-            tma_load_bytes(s_buf + t * PART_TILE, ks.body + v0, static_cast<unsigned>(nvec * 16),
+            tma_load_bytes(s_buf + t * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16),
                            &s_bar[t]);
         }
     }
@@ -322,24 +328,24 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
     }
     __syncthreads();
 
-    constexpr int VPT = PART_KPT / 4;
+    constexpr int VPT = KPT / 4;
     const int slots = nb + 1;
-    const int per = (slots + PART_THREADS - 1) / PART_THREADS;
+    const int per = (slots + THREADS - 1) / THREADS;
     const int sb = threadIdx.x * per;
     for (size_t t = 0; t < ntiles; ++t) {
         const int p = static_cast<int>(t & 1);
-        uint32_t* buf = s_buf + p * PART_TILE;
+        uint32_t* buf = s_buf + p * TILE;
         const size_t v0 = vlo + t * kTileVec;
         const uint32_t nvec = static_cast<uint32_t>(min(kTileVec, vhi - v0));
         mbar_wait(&s_bar[p], static_cast<unsigned>((t >> 1) & 1));
 
-        uint32_t k[PART_KPT];
-        uint32_t rb[PART_KPT];  // bucket << 16 | rank inside the bucket (rank < PART_TILE)
+        uint32_t k[KPT];
+        uint32_t rb[KPT];  // bucket << 16 | rank inside the bucket (rank < TILE)
         uint32_t kmin = 0xffffffffu, kmax = 0;
         bool all_in = true;
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
-            const uint32_t vi = j * PART_THREADS + threadIdx.x;
+            const uint32_t vi = j * THREADS + threadIdx.x;
             const bool in = vi < nvec;
             all_in &= in;
             const uint4 v = in ? reinterpret_cast<const uint4*>(buf)[vi] : make_uint4(0, 0, 0, 0);
@@ -357,13 +363,13 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         if (blo == bhi && __all_sync(kFull, all_in)) {
             // the whole warp step lies in one bucket: one atomic, ranks by lane
             uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(s_cnt + blo, 32u * PART_KPT);
-            base = __shfl_sync(kFull, base, 0) + lane * PART_KPT;
+            if (lane == 0) base = atomicAdd(s_cnt + blo, 32u * KPT);
+            base = __shfl_sync(kFull, base, 0) + lane * KPT;
 #pragma unroll
-            for (int q = 0; q < PART_KPT; ++q) rb[q] = (blo << 16) | (base + q);
+            for (int q = 0; q < KPT; ++q) rb[q] = (blo << 16) | (base + q);
         } else {
 #pragma unroll
-            for (int q = 0; q < PART_KPT; ++q) rb[q] = (rb[q] << 16) | atomicAdd(s_cnt + rb[q], 1u);
+            for (int q = 0; q < KPT; ++q) rb[q] = (rb[q] << 16) | atomicAdd(s_cnt + rb[q], 1u);
         }
         __syncthreads();  // A: tile counts complete; every thread has read buf
         {
@@ -374,9 +380,9 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             if (lane == 31) s_scratch[warp] = incl;
             __syncthreads();
             if (warp == 0) {
-                const uint32_t w = static_cast<uint32_t>(s_scratch[lane]);  // 32 warps
+                const uint32_t w = lane < NWARPS ? static_cast<uint32_t>(s_scratch[lane]) : 0u;
                 const uint32_t wi = warp_incl_scan(w, lane);
-                s_scratch[lane] = wi - w;
+                if (lane < NWARPS) s_scratch[lane] = wi - w;
             }
             __syncthreads();
             uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
@@ -394,12 +400,15 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             }
         }
         __syncthreads();  // B
+        // all 16 bucket-start lookups first (independent SMEM loads), then the stores
 #pragma unroll
-        for (int q = 0; q < PART_KPT; ++q) buf[s_start[rb[q] >> 16] + (rb[q] & 0xffffu)] = k[q];
+        for (int q = 0; q < KPT; ++q) rb[q] = s_start[rb[q] >> 16] + (rb[q] & 0xffffu);
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) buf[rb[q]] = k[q];
         __syncthreads();  // C
         const uint32_t tile_valid = s_tile_valid;
 #pragma unroll 4
-        for (uint32_t i = threadIdx.x; i < tile_valid; i += PART_THREADS) {
+        for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
             const uint32_t key = buf[i];
             parted[s_delta[key >> shift] + i] = key;
         }
@@ -498,21 +507,44 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         const uint32_t cnt = tot[b];
         const uint32_t* src = parted + base;
         {
-            constexpr int U = 8;
+            // misaligned head (< 4 keys), then 16-byte loads, 4 per thread in flight
+            const uint32_t head = min(cnt, static_cast<uint32_t>(
+                                              ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
+            if (threadIdx.x < head) {
+                const uint32_t x = __ldcs(src + threadIdx.x) & lowmask;
+                atomicOr(s_bits + (x >> 5), 1u << (x & 31));
+            }
+            const uint4* v4 = reinterpret_cast<const uint4*>(src + head);
+            const uint32_t nv = (cnt - head) / 4;
+            constexpr int U = 4;
             constexpr uint32_t kBatch = BUCKET_THREADS * U;
             uint32_t i0 = 0;
-            for (; i0 + kBatch <= cnt; i0 += kBatch) {
-                uint32_t k[U];
+            for (; i0 + kBatch <= nv; i0 += kBatch) {
+                uint4 v[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) k[u] = __ldcs(src + i0 + u * BUCKET_THREADS + threadIdx.x);
+                for (int u = 0; u < U; ++u) v[u] = __ldcs(v4 + i0 + u * BUCKET_THREADS + threadIdx.x);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const uint32_t x = k[u] & lowmask;
+                    const uint32_t kk[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t x = kk[q] & lowmask;
+                        atomicOr(s_bits + (x >> 5), 1u << (x & 31));
+                    }
+                }
+            }
+            for (uint32_t i = i0 + threadIdx.x; i < nv; i += BUCKET_THREADS) {
+                const uint4 v = __ldcs(v4 + i);
+                const uint32_t kk[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t x = kk[q] & lowmask;
                     atomicOr(s_bits + (x >> 5), 1u << (x & 31));
                 }
             }
-            for (uint32_t i = i0 + threadIdx.x; i < cnt; i += BUCKET_THREADS) {
-                const uint32_t x = __ldcs(src + i) & lowmask;
+            const uint32_t done = head + 4 * nv;
+            if (threadIdx.x < cnt - done) {
+                const uint32_t x = __ldcs(src + done + threadIdx.x) & lowmask;
                 atomicOr(s_bits + (x >> 5), 1u << (x & 31));
             }
         }
@@ -582,6 +614,17 @@ __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl
 
 }  // namespace
 
+// The narrow KB3 variant (2 CTAs/SM, 8192-key tiles) measured slower than the
+// wide one on C2 (profiles/r01_*): shorter bucket runs add partial-sector
+// DRAM traffic. It stays selectable for experiments (BITSORT_PART=narrow).
+static bool narrow_partition(const BucketPlan& plan) {
+    static const bool want = [] {
+        const char* e = std::getenv("BITSORT_PART");
+        return e && std::string(e) == "narrow";
+    }();
+    return want && plan.nb <= PART_NARROW_MAXB;
+}
+
 cudaError_t launch_key_max(const uint32_t* keys, size_t n, Ctrl* ctrl, const LaunchGeometry& geo,
                            cudaStream_t stream) {
     key_max_kernel<<<geo.fill_blocks, 256, 0, stream>>>(keys, n, ctrl);
@@ -592,7 +635,12 @@ BucketPlan plan_buckets(uint64_t key_range) {
     BucketPlan p;
     int log2m = 0;
     while ((1ull << log2m) < key_range) ++log2m;
-    int shift = log2m - 10;
+    // Fewest buckets the SMEM bitset allows, but at least 256 of them (KB4
+    // parallelism): KB3 runs faster with fewer buckets (longer runs per tile;
+    // measured C2: 256 buckets 177 us vs 1024 buckets 256 us).
+    int shift = log2m - 8;
+    if (const char* env = std::getenv("BITSORT_BUCKET_SHIFT")) shift = std::atoi(env);  // experiments
+    while (shift < MAX_BUCKET_SHIFT && ((key_range + (1ull << shift) - 1) >> shift) > MAX_BUCKETS) ++shift;
     if (shift > MAX_BUCKET_SHIFT) shift = MAX_BUCKET_SHIFT;
     if (shift < MIN_BUCKET_SHIFT) shift = MIN_BUCKET_SHIFT;
     p.shift = shift;
@@ -612,7 +660,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                                const LaunchGeometry& geo, cudaStream_t stream, int* launches,
                                KernelTimer* timer) {
     if (n == 0) return cudaSuccess;
-    const int P = geo.part_blocks;
+    const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     uint32_t* H = static_cast<uint32_t*>(scratch);
     uint32_t* tot = H + static_cast<size_t>(P) * plan.nb;
     unsigned long long* base =
@@ -643,8 +691,14 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (timer) timer->after("bucket_colscan", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (timer) timer->before(stream);
-    bucket_partition_kernel<<<P, PART_THREADS, part_smem_bytes(), stream>>>(
-        ks, plan.shift, plan.nb, H, tot, parted, base);
+    if (narrow_partition(plan))
+        bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB>
+            <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
+                ks, plan.shift, plan.nb, H, tot, parted, base);
+    else
+        bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS>
+            <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
+                ks, plan.shift, plan.nb, H, tot, parted, base);
     if (timer) timer->after("bucket_partition", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     const size_t smem = bucket_sort_smem_bytes(plan.shift);
@@ -661,17 +715,26 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     int sms = 0;
     cudaError_t err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(part_smem_bytes()));
+    auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS>;
+    auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB>;
+    err = cudaFuncSetAttribute(wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bucket_sort_smem_bytes(20)));
     if (err != cudaSuccess) return err;
     int per = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_partition_kernel, PART_THREADS,
-                                                        part_smem_bytes());
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wide, PART_THREADS,
+                                                        part_smem_bytes(PART_THREADS, MAX_BUCKETS));
     if (err != cudaSuccess) return err;
     geo->part_blocks = sms * (per > 0 ? per : 1);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per, narrow, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB));
+    if (err != cudaSuccess) return err;
+    geo->part_blocks_narrow = sms * (per > 0 ? per : 1);
     for (int shift = MIN_BUCKET_SHIFT; shift <= MAX_BUCKET_SHIFT; ++shift) {
         err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel, BUCKET_THREADS,
                                                             bucket_sort_smem_bytes(shift));

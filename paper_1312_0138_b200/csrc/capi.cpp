@@ -134,7 +134,8 @@ struct DeviceCtx {
         cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
         bws_gpu::BucketPlan widest;
         widest.nb = bws_gpu::MAX_BUCKETS;
-        cuda_check(cudaMalloc(&bucket_scratch, bws_gpu::bucket_scratch_bytes(widest, geo.part_blocks) + 64),
+        const int max_shares = geo.part_blocks > geo.part_blocks_narrow ? geo.part_blocks : geo.part_blocks_narrow;
+        cuda_check(cudaMalloc(&bucket_scratch, bws_gpu::bucket_scratch_bytes(widest, max_shares) + 64),
                    "cudaMalloc(bucket scratch)");
         bits_dirty = true;
         ready = true;

@@ -45,14 +45,18 @@ constexpr int MIN_BUCKET_SHIFT = 15;  // SMEM bitset of a bucket: 2^shift bits
 constexpr int MAX_BUCKET_SHIFT = 20;  // 128 KB
 constexpr int BUCKET_HIST_THREADS = 512;
 constexpr int HIST_SPLIT = 4;  // histogram CTAs per partition CTA share
+// KB3 variants: "wide" (nb <= 4096): 1024 threads, 16384-key tiles, 1 CTA/SM;
+// "narrow" (nb <= 1024): 512 threads, 8192-key tiles, 2 CTAs/SM.
 constexpr int PART_THREADS = 1024;
 constexpr int PART_KPT = 16;
-constexpr int PART_TILE = PART_THREADS * PART_KPT;  // 16384 keys per partition tile
+constexpr int PART_TILE = PART_THREADS * PART_KPT;  // 16384 keys per wide tile
+constexpr int PART_NARROW_THREADS = 512;
+constexpr int PART_NARROW_MAXB = 1024;
 constexpr int BUCKET_THREADS = 1024;
 constexpr int BUCKET_STAGE = 512;  // keys per warp in the extraction stage
 
-constexpr std::size_t part_smem_bytes() {
-    return 2 * PART_TILE * 4 + (MAX_BUCKETS + 1) * (4 + 4 + 4 + 4);  // TMA ring + 4 slot arrays
+constexpr std::size_t part_smem_bytes(int threads, int maxb) {
+    return 2 * std::size_t(threads) * PART_KPT * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
 }
 constexpr std::size_t bucket_sort_smem_bytes(int shift) {
     return (std::size_t(1) << (shift - 3)) +
@@ -63,7 +67,8 @@ struct LaunchGeometry {
     int scatter_blocks = 0;
     int scan_blocks = 0;
     int fill_blocks = 0;
-    int part_blocks = 0;                         // KB1/KB3 CTAs (same chunking)
+    int part_blocks = 0;                         // KB1/KB3 shares, wide KB3 variant
+    int part_blocks_narrow = 0;                  // KB1/KB3 shares, narrow KB3 variant
     int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
 };
 
