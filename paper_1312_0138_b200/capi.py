@@ -16,7 +16,11 @@ import numpy as np
 
 from . import LIB_DIR
 
-LIB_PATH = LIB_DIR / "libbitsort.so.1"
+import os as _os
+from pathlib import Path as _Path
+
+# BITSORT_LIB overrides the library path (A/B experiments on kernel builds)
+LIB_PATH = _Path(_os.environ["BITSORT_LIB"]) if _os.environ.get("BITSORT_LIB") else LIB_DIR / "libbitsort.so.1"
 
 
 class Status(enum.IntEnum):

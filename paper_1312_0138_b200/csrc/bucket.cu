@@ -124,15 +124,26 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
     const size_t vhi = clo + (chi - clo) * (part + 1) / HIST_SPLIT;
     const unsigned lane = threadIdx.x & 31;
     uint32_t mx = 0, bad = 0;
-    constexpr int U = 4;  // uint4 per thread per step: 16 keys, 4 loads in flight
-    for (size_t base = vlo; base < vhi; base += static_cast<size_t>(blockDim.x) * U) {
-        uint4 v[U];
-        bool in[U];
+    constexpr int U = 4;  // uint4 per thread per step: 16 keys
+    const size_t step = static_cast<size_t>(blockDim.x) * U;
+    // software pipelined: the next step's loads are in flight while this
+    // step's buckets are counted
+    uint4 v[U];
+    bool in[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const size_t i = vlo + static_cast<size_t>(u) * blockDim.x + threadIdx.x;
+        in[u] = i < vhi;
+        v[u] = in[u] ? __ldcs(ks.body + i) : make_uint4(0, 0, 0, 0);
+    }
+    for (size_t base = vlo; base < vhi; base += step) {
+        uint4 vn[U];
+        bool inn[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const size_t i = base + static_cast<size_t>(u) * blockDim.x + threadIdx.x;
-            in[u] = i < vhi;
-            v[u] = in[u] ? __ldcs(ks.body + i) : make_uint4(0, 0, 0, 0);
+            const size_t i = base + step + static_cast<size_t>(u) * blockDim.x + threadIdx.x;
+            inn[u] = i < vhi;
+            vn[u] = inn[u] ? __ldcs(ks.body + i) : make_uint4(0, 0, 0, 0);
         }
         uint32_t bk[U * 4];
         uint32_t kmin = 0xffffffffu, kmax = 0;
@@ -159,6 +170,11 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
         } else {
 #pragma unroll
             for (int q = 0; q < U * 4; ++q) atomicAdd(s_h + bk[q], 1u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            v[u] = vn[u];
+            in[u] = inn[u];
         }
     }
     if (threadIdx.x == 0 && part == 0) {  // misaligned head (share 0) / tail (last share)
@@ -471,11 +487,61 @@ __device__ __forceinline__ uint32_t extract_words32(const uint32_t* s_bits, uint
     return ctot;
 }
 
+// KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
+// buckets, the summary of touched words): misaligned head, 16-byte loads
+// with 4 per thread in flight, tail.
+template <bool SPARSE>
+__device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__ src, uint32_t cnt,
+                                                    uint32_t lowmask, uint32_t* s_bits,
+                                                    uint32_t* s_sum) {
+    auto set_key = [&](uint32_t key) {
+        const uint32_t x = key & lowmask;
+        const uint32_t w = x >> 5;
+        atomicOr(s_bits + w, 1u << (x & 31));
+        if (SPARSE) atomicOr(s_sum + (w >> 5), 1u << (w & 31));
+    };
+    const uint32_t head = min(cnt, static_cast<uint32_t>(
+                                       ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
+    if (threadIdx.x < head) set_key(__ldcs(src + threadIdx.x));
+    const uint4* v4 = reinterpret_cast<const uint4*>(src + head);
+    const uint32_t nv = (cnt - head) / 4;
+    constexpr int U = 4;
+    constexpr uint32_t kBatch = BUCKET_THREADS * U;
+    uint32_t i0 = 0;
+    for (; i0 + kBatch <= nv; i0 += kBatch) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(v4 + i0 + u * BUCKET_THREADS + threadIdx.x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            set_key(v[u].x);
+            set_key(v[u].y);
+            set_key(v[u].z);
+            set_key(v[u].w);
+        }
+    }
+    for (uint32_t i = i0 + threadIdx.x; i < nv; i += BUCKET_THREADS) {
+        const uint4 v = __ldcs(v4 + i);
+        set_key(v.x);
+        set_key(v.y);
+        set_key(v.z);
+        set_key(v.w);
+    }
+    const uint32_t done = head + 4 * nv;
+    if (threadIdx.x < cnt - done) set_key(__ldcs(src + done + threadIdx.x));
+}
+
 // KB4: one bucket per CTA iteration (dynamic ticket). SMEM bitset of 2^shift
 // bits; warp w owns words [w*W/32, (w+1)*W/32) and extracts them in order
-// (see phase 2) straight to the output slots of the bucket. Every key of a
-// bucket lands in [base_b, base_b + tot_b) (tot_b counts duplicates too), so
-// no output bounds checks are needed.
+// straight to the output slots of the bucket. Every key of a bucket lands in
+// [base_b, base_b + tot_b) (tot_b counts duplicates too), so no output bounds
+// checks are needed.
+//
+// Dense buckets zero the whole bitset up front and scan every word. Sparse
+// buckets (< 1 key per 4 words: e.g. C4, and the thin tails of C5) also mark
+// each touched word in a summary bitset (one bit per word), visit only
+// touched words, and zero exactly those words again, so a sparse bucket costs
+// O(keys) SMEM work instead of O(2^shift / 32) and leaves the bitset clean.
 __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, int shift, int nb,
@@ -483,7 +549,8 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t W = 1u << (shift - 5);  // words per bucket bitset (>= 1024)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* s_stage_all = s_bits + W;  // BUCKET_THREADS/32 x (BUCKET_STAGE + BUCKET_STAGE/32)
+    uint32_t* s_sum = s_bits + W;             // bit w set <=> word w touched (sparse buckets)
+    uint32_t* s_stage_all = s_sum + W / 32;   // BUCKET_THREADS/32 x stage pitch
     __shared__ uint32_t s_warp[BUCKET_THREADS / 32];
     __shared__ unsigned s_b;
 
@@ -495,66 +562,40 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     const uint32_t lowmask = (1u << shift) - 1;
     const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
 
+    for (uint32_t i = threadIdx.x; i < W / 32; i += BUCKET_THREADS) s_sum[i] = 0u;
+    bool dirty = true;  // block-uniform: bitset needs zeroing before the next bucket
     for (;;) {
         if (threadIdx.x == 0) s_b = atomicAdd(&ctrl->ticket, 1u);
-        // zero the bitset (the previous bucket's readers finished at the loop-end barrier)
-        uint4* b4 = reinterpret_cast<uint4*>(s_bits);
-        for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
+        if (dirty) {  // the previous bucket's readers finished at the loop-end barrier
+            uint4* b4 = reinterpret_cast<uint4*>(s_bits);
+            for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
+        }
         __syncthreads();
         const unsigned b = s_b;
         if (b >= static_cast<unsigned>(nb)) break;
         const unsigned long long base = g_base[b];
         const uint32_t cnt = tot[b];
         const uint32_t* src = parted + base;
-        {
-            // misaligned head (< 4 keys), then 16-byte loads, 4 per thread in flight
-            const uint32_t head = min(cnt, static_cast<uint32_t>(
-                                              ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
-            if (threadIdx.x < head) {
-                const uint32_t x = __ldcs(src + threadIdx.x) & lowmask;
-                atomicOr(s_bits + (x >> 5), 1u << (x & 31));
-            }
-            const uint4* v4 = reinterpret_cast<const uint4*>(src + head);
-            const uint32_t nv = (cnt - head) / 4;
-            constexpr int U = 4;
-            constexpr uint32_t kBatch = BUCKET_THREADS * U;
-            uint32_t i0 = 0;
-            for (; i0 + kBatch <= nv; i0 += kBatch) {
-                uint4 v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) v[u] = __ldcs(v4 + i0 + u * BUCKET_THREADS + threadIdx.x);
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint32_t kk[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t x = kk[q] & lowmask;
-                        atomicOr(s_bits + (x >> 5), 1u << (x & 31));
-                    }
-                }
-            }
-            for (uint32_t i = i0 + threadIdx.x; i < nv; i += BUCKET_THREADS) {
-                const uint4 v = __ldcs(v4 + i);
-                const uint32_t kk[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t x = kk[q] & lowmask;
-                    atomicOr(s_bits + (x >> 5), 1u << (x & 31));
-                }
-            }
-            const uint32_t done = head + 4 * nv;
-            if (threadIdx.x < cnt - done) {
-                const uint32_t x = __ldcs(src + done + threadIdx.x) & lowmask;
-                atomicOr(s_bits + (x >> 5), 1u << (x & 31));
-            }
-        }
+        const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
+        if (sparse)
+            scatter_bucket_keys<true>(src, cnt, lowmask, s_bits, s_sum);
+        else
+            scatter_bucket_keys<false>(src, cnt, lowmask, s_bits, s_sum);
         __syncthreads();
-        // phase 1: per-warp popcount of its segment (128-bit SMEM reads)
+        // phase 1: per-warp popcount of its segment (128-bit SMEM reads; sparse
+        // buckets read only the touched words, found through the summary)
         const uint32_t seg = warp * seg_words;
         uint32_t c = 0;
-        for (uint32_t i = lane; i < seg_words / 4; i += 32) {
-            const uint4 v = s4[seg / 4 + i];
-            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        if (sparse) {
+            for (uint32_t i = lane; i < seg_words / 32; i += 32) {
+                const uint32_t si = seg / 32 + i;
+                for (uint32_t m = s_sum[si]; m; m &= m - 1) c += __popc(s_bits[si * 32 + (__ffs(m) - 1)]);
+            }
+        } else {
+            for (uint32_t i = lane; i < seg_words / 4; i += 32) {
+                const uint4 v = s4[seg / 4 + i];
+                c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            }
         }
         c = __reduce_add_sync(kFull, c);
         if (lane == 0) s_warp[warp] = c;
@@ -566,13 +607,41 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
             if (lane == 31 && incl) atomicAdd(&ctrl->total, static_cast<unsigned long long>(incl));
         }
         __syncthreads();
-        // phase 2: extraction. 128-word steps, lane-major (lane owns 4 words):
-        // an empty step costs ~20 instructions; a step with <= BUCKET_STAGE
-        // keys is extracted in one pass; denser steps fall back to four
-        // 32-word sub-steps (word per lane).
         uint32_t* o = out + base + s_warp[warp];
         const uint32_t key_hi = static_cast<uint32_t>(b) << shift;
-        if (seg_words >= 128) {
+        if (sparse) {
+            // lane-major over summary words: lane owns 32 consecutive bitset
+            // words (one summary word) per round; its keys are contiguous in
+            // the output at its prefix offset. Touched words are zeroed.
+            for (uint32_t i0 = 0; i0 < seg_words / 32; i0 += 32) {
+                const uint32_t si = seg / 32 + i0 + lane;
+                uint32_t m = i0 + lane < seg_words / 32 ? s_sum[si] : 0u;
+                uint32_t cl = 0;
+                for (uint32_t mm = m; mm; mm &= mm - 1) cl += __popc(s_bits[si * 32 + (__ffs(mm) - 1)]);
+                const uint32_t incl = warp_incl_scan(cl, lane);
+                const uint32_t ctot = __shfl_sync(kFull, incl, 31);
+                if (ctot == 0) continue;
+                uint32_t* ol = o + (incl - cl);
+                if (m) s_sum[si] = 0u;
+                while (m) {
+                    const uint32_t t = static_cast<uint32_t>(__ffs(m) - 1);
+                    m &= m - 1;
+                    const uint32_t wi = si * 32 + t;
+                    uint32_t x = s_bits[wi];
+                    s_bits[wi] = 0u;
+                    const uint32_t kb = key_hi + (wi << 5);
+                    while (x) {
+                        const int bt = __ffs(x) - 1;
+                        x &= x - 1;
+                        __stcs(ol++, kb + static_cast<uint32_t>(bt));
+                    }
+                }
+                o += ctot;
+            }
+        } else if (seg_words >= 128) {
+            // 128-word steps, lane-major (lane owns 4 words); a step with
+            // <= BUCKET_STAGE keys is extracted in one pass, denser steps fall
+            // back to four 32-word sub-steps (word per lane)
             for (uint32_t w0 = 0; w0 < seg_words; w0 += 128) {
                 const uint4 v = s4[(seg + w0) / 4 + lane];
                 const uint32_t cl = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
@@ -598,6 +667,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
             for (uint32_t w0 = 0; w0 < seg_words; w0 += 32)
                 o += extract_words32(s_bits, seg + w0, key_hi, o, s_stage, lane);
         }
+        dirty = !sparse;
         __syncthreads();
     }
 }

@@ -59,7 +59,7 @@ constexpr std::size_t part_smem_bytes(int threads, int maxb) {
     return 2 * std::size_t(threads) * PART_KPT * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
 }
 constexpr std::size_t bucket_sort_smem_bytes(int shift) {
-    return (std::size_t(1) << (shift - 3)) +
+    return (std::size_t(1) << (shift - 3)) + (std::size_t(1) << (shift - 8)) +  // bitset + summary
            (BUCKET_THREADS / 32) * (BUCKET_STAGE + BUCKET_STAGE / 32) * 4;
 }
 
