@@ -156,7 +156,7 @@ struct DeviceCtx {
         if (parted) cuda_check(cudaFree(parted), "cudaFree(parted)");
         parted = nullptr;
         parted_cap = 0;
-        const size_t cap = n + n / 8;
+        const size_t cap = n + n / 8 + 64;  // KB4 bulk copies may read up to 12 bytes past n
         cuda_check(cudaMalloc(&parted, cap * sizeof(uint32_t)), "cudaMalloc(bucket keys)");
         parted_cap = cap;
     }

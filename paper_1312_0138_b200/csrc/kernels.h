@@ -54,6 +54,10 @@ constexpr int PART_NARROW_THREADS = 512;
 constexpr int PART_NARROW_MAXB = 1024;
 constexpr int BUCKET_THREADS = 1024;
 constexpr int BUCKET_STAGE = 512;  // keys per warp in the extraction stage
+constexpr int MAX_CLUSTER = 8;          // CTAs per bucket in the cluster KB4 (portable limit)
+constexpr int CLUSTER_SUB_SHIFT = 20;   // each cluster CTA owns a 2^20-key sub-range
+constexpr int CLUSTER_CHUNK = 4096;     // keys per multicast chunk (16 KB), two buffers
+constexpr int CLUSTER_STAGE = 256;      // keys per warp in the cluster kernel's stage
 
 constexpr std::size_t part_smem_bytes(int threads, int maxb) {
     return 2 * std::size_t(threads) * PART_KPT * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
@@ -63,6 +67,11 @@ constexpr std::size_t bucket_sort_smem_bytes(int shift) {
            (BUCKET_THREADS / 32) * (BUCKET_STAGE + BUCKET_STAGE / 32) * 4;
 }
 
+constexpr std::size_t cluster_sort_smem_bytes() {
+    return (std::size_t(1) << (CLUSTER_SUB_SHIFT - 3)) + (std::size_t(1) << (CLUSTER_SUB_SHIFT - 8)) +
+           2 * CLUSTER_CHUNK * 4 + (BUCKET_THREADS / 32) * (CLUSTER_STAGE + CLUSTER_STAGE / 32) * 4;
+}
+
 struct LaunchGeometry {
     int scatter_blocks = 0;
     int scan_blocks = 0;
@@ -70,6 +79,7 @@ struct LaunchGeometry {
     int part_blocks = 0;                         // KB1/KB3 shares, wide KB3 variant
     int part_blocks_narrow = 0;                  // KB1/KB3 shares, narrow KB3 variant
     int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
+    int clusters[4] = {};                          // cluster KB4: max clusters for R = 1,2,4,8
 };
 
 // A key array as seen by the bucketed kernels: 16-byte-aligned uint4 body plus
@@ -84,8 +94,9 @@ struct KeySplit {
 };
 
 struct BucketPlan {
-    int shift = 20;  // bucket = key >> shift
-    int nb = 1;      // number of buckets, <= MAX_BUCKETS
+    int shift = 20;   // bucket = key >> shift
+    int nb = 1;       // number of buckets, <= MAX_BUCKETS
+    int cluster = 1;  // CTAs per bucket in KB4 (bucket range = cluster * 2^20 when > 1)
 };
 
 // Optional per-kernel timing hook (bench.py's live roofline): before() and
