@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--cpu-sample-keys", type=int, default=1 << 25,
                     help="keys in the cpu_baseline sample (about 10 s of reference CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU (NCCL reduce-scatter) path even with one rank")
     return ap.parse_args()
 
 
@@ -242,14 +244,18 @@ def run_ours(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
     capi.set_path(getattr(capi.Path, args.path))
 
     keys_h = cfg.generate()
     n_total, M = cfg.n, cfg.key_range
-    if world > 1:
+    if use_dist:
         from paper_1312_0138_b200.dist import CudaRankOps, distributed_sort, shard_bounds
 
         lo, hi = shard_bounds(n_total, rank, world)
@@ -262,7 +268,7 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
-    if world > 1:
+    if use_dist:
         ops = CudaRankOps(dev)
 
         def step():
@@ -274,7 +280,14 @@ def run_ours(args, cfg):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    if world == 1:
+    if use_dist:
+        res = step()
+        u = res.keys.to(torch.int64) & 0xFFFFFFFF
+        assert res.total == n_total and bool((u[1:] > u[:-1]).all()), "distributed output not ascending"
+        if res.count:
+            assert int(u[0]) >= res.key_lo and int(u[-1]) < res.key_hi
+        del u, res
+    else:
         assert capi.sort_check(sp) == n_total
         u = out_d.to(torch.int64) & 0xFFFFFFFF
         assert bool((u[1:] > u[:-1]).all()), "output not strictly ascending"
@@ -283,7 +296,7 @@ def run_ours(args, cfg):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.05)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     capi.set_kernel_timing(True)
@@ -299,16 +312,16 @@ def run_ours(args, cfg):
         b.record(stream)
     torch.cuda.synchronize(dev)
     t1 = time.perf_counter()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     launches = capi.launch_count() - launches0
     ktimes = capi.kernel_timings()
     capi.set_kernel_timing(False)
     clocks = sampler.summary(t0, t1)
-    if world == 1:
+    if not use_dist:
         assert capi.sort_check(sp) == n_total
     total_ms = sum(a.elapsed_time(b) for a, b in evs)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -349,11 +362,11 @@ def run_ours(args, cfg):
     times = []
     for i in range(e2e_steps + 1):
         np.copyto(host, shard_h)  # restore the unsorted input (outside the timed region)
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t_a = time.perf_counter()
-        if world > 1:
+        if use_dist:
             kd = pinned.to(dev, non_blocking=True)
             res = distributed_sort(kd, M, n_total=n_total, ops=ops)
             res.keys.view(torch.int32).cpu()  # D2H of this rank's sorted slice
@@ -362,10 +375,10 @@ def run_ours(args, cfg):
             capi.sort(host)  # bws_sort(host, n, 32, 1, BWS_ALG_BITWISE): H2D + sort + D2H
         if i > 0:
             times.append(time.perf_counter() - t_a)
-    if world == 1:
+    if not use_dist:
         assert np.all(host[1:] > host[:-1])
     e2e_s = sum(times) / len(times)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
@@ -373,14 +386,14 @@ def run_ours(args, cfg):
            "h2d_bytes_per_step": 4 * int(shard_h.size) * world,
            "d2h_bytes_per_step": 4 * int(shard_h.size) * world,
            "ms_per_step": round(e2e_s * 1e3, 3), "steps": e2e_steps,
-           "api": "bws_sort (C ABI) on a pinned host array" if world == 1
-           else "dist.distributed_sort on pinned host shards"}
+           "api": "dist.distributed_sort on pinned host shards" if use_dist
+           else "bws_sort (C ABI) on a pinned host array"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(keys_h, args.cpu_sample_keys, cfg.name)
 
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     if rank != 0:
         return 0
@@ -391,7 +404,8 @@ def run_ours(args, cfg):
         "data": "synthetic",
         "config": {"workload": cfg.name, "n": n_total, "key_range": M, "recipe": cfg.recipe,
                    "l2": "flushed between steps (256 MiB write, outside the step events)",
-                   "path": args.path, "parallelism": f"key shards x{world}" if world > 1 else "single GPU"},
+                   "path": args.path,
+                   "parallelism": f"key shards x{world} + NCCL reduce-scatter" if use_dist else "single GPU"},
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
         "step_roofline": step_roofline, "kernels": kernels, "cpu_baseline": cpu, "clocks": clocks,
     }

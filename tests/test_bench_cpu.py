@@ -1,0 +1,35 @@
+"""bench.py contract pieces that run without a GPU: the reference arm's JSON
+line and the per-kernel algorithmic-byte formulas."""
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "C1",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                         check=True).stdout.strip().splitlines()
+    assert len(out) == 1
+    d = json.loads(out[0])
+    assert d["impl"] == "reference" and d["unit"] == "Gkeys/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 1
+    assert d["cpu_baseline"]["cores"] == 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["config"]["workload"] == "C1"
+
+
+def test_kernel_alg_bytes():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    n, m = 1 << 26, 1 << 28
+    assert bench.kernel_alg_bytes("bucket_partition", n, m) == 8 * n
+    assert bench.kernel_alg_bytes("bucket_sort", n, m) == 8 * n
+    assert bench.kernel_alg_bytes("bucket_hist", n, m) == 4 * n
+    assert bench.kernel_alg_bytes("bitset_scatter", n, m) == 4 * n + m // 8
+    assert bench.kernel_alg_bytes("bitset_scan", n, m, world=2) == m // 16 + 4 * n

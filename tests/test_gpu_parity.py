@@ -313,3 +313,31 @@ def test_c5_clustered_properties(capi, cuda, path):
     assert int(u.sum()) == int(k.sum())
     assert int((u * u).sum()) == int((k * k).sum())
     assert int(u[0]) == int(keys.min()) and int(u[-1]) == int(keys.max())
+
+
+def test_distributed_sort_nccl_single_rank(capi, cuda):
+    """dist.distributed_sort over a real NCCL process group (world size 1 on
+    the one GPU available): K1+K2 through the C ABI, NCCL reduce-scatter and
+    all-gather, K3 on the slice. Multi-rank host logic is covered on gloo in
+    tests/test_dist_gloo.py."""
+    import torch.distributed as dist
+
+    from paper_1312_0138_b200.dist import distributed_sort
+
+    store = dist.HashStore()
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1,
+                            device_id=cuda.device("cuda", 0))
+    try:
+        keys = np.random.default_rng(77).choice(1 << 24, size=1 << 22, replace=False).astype(np.uint32)
+        t = cuda.from_numpy(keys.view(np.int32)).cuda()
+        res = distributed_sort(t, 1 << 24)
+        assert res.total == keys.size and res.offset == 0 and res.count == keys.size
+        assert np.array_equal(res.keys.cpu().numpy().view(np.uint32), np.sort(keys))
+        bad = keys.copy()
+        bad[5] = bad[6]
+        from paper_1312_0138_b200.capi import BitsortError
+
+        with pytest.raises(BitsortError):
+            distributed_sort(cuda.from_numpy(bad.view(np.int32)).cuda(), 1 << 24)
+    finally:
+        dist.destroy_process_group()

@@ -1,5 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "random_distinct and BUCKETED" > gpurun_out/pytest_quick.log 2>&1; echo quick_exit=$? >> gpurun_out/pytest_quick.log
-if grep -q "quick_exit=0" gpurun_out/pytest_quick.log; then
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --config all --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_all.json 2> gpurun_out/bench_all.err
-fi
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --dist --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_dist1.json 2> gpurun_out/bench_dist1.err; echo exit=$? >> gpurun_out/bench_dist1.err
+timeout 300 python bench.py --steps 100 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
