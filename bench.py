@@ -92,6 +92,7 @@ def kernel_alg_bytes(kernel: str, n: int, key_range: int, world: int = 1) -> int
         "bucket_colscan": 0,
         "bucket_partition": 8 * n,            # read keys, write bucketed keys
         "bucket_sort": 8 * n,                 # read bucketed keys, write sorted keys
+        "bucket_bitset": 4 * n + words_bytes,  # read bucketed keys, write the bitset (multi-GPU)
         "bitset_scatter": 4 * n + words_bytes,          # read keys, write bitset
         "bitset_scan": words_bytes // world + 4 * n,    # read (slice of) bitset, write keys
     }.get(kernel, 0)

@@ -38,9 +38,11 @@ BITSORT_API bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t co
 BITSORT_API bws_status bws_gpu_sort_check(void* stream, uint64_t* distinct_out);
 
 /* Per-rank building blocks for the multi-GPU path (one process per GPU).
- *   bitset_build: K1 clear of key_range/8 bytes at `bits` + K2 scatter of
- *                 `count` keys (device) into it. `bits` must hold
- *                 ceil(key_range/32) uint32 words.
+ *   bitset_build: the full bitset of `count` keys (device) in [0, key_range)
+ *                 at `bits` (ceil(key_range/32) uint32 words, overwritten;
+ *                 no prior clearing needed). Large inputs go through the
+ *                 bucketed SMEM-staged build (no global atomics), small ones
+ *                 through K1 clear + K2 scatter.
  *   bitset_scan:  K3 over n_words words at `bits` (a rank's slice), writing
  *                 key_base + bit_index for every set bit, ascending, to `out`
  *                 (capacity out_capacity keys). The number of keys is written

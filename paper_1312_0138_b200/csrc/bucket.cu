@@ -924,6 +924,44 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
     }
 }
 
+// KB4b (multi-GPU per-rank build): like KB4, but instead of extracting keys
+// each bucket's SMEM bitset is written to the global bitset, coalesced and
+// without atomics; every word below n_words is written, so the caller's
+// bitset needs no clearing.
+__global__ void __launch_bounds__(BUCKET_THREADS, 1)
+    bucket_bitset_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
+                         const unsigned long long* __restrict__ g_base, int shift, int nb,
+                         uint32_t* __restrict__ bits, unsigned long long n_words,
+                         uint32_t last_mask, Ctrl* __restrict__ ctrl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t W = 1u << (shift - 5);
+    uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
+    __shared__ unsigned s_b;
+    const uint32_t lowmask = (1u << shift) - 1;
+    uint4* s4 = reinterpret_cast<uint4*>(s_bits);
+    for (;;) {
+        if (threadIdx.x == 0) s_b = atomicAdd(&ctrl->ticket, 1u);
+        for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) s4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        const unsigned b = s_b;
+        if (b >= static_cast<unsigned>(nb)) break;
+        scatter_bucket_keys<false>(parted + g_base[b], tot[b], lowmask, s_bits, nullptr);
+        __syncthreads();
+        const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
+        // keys in [key_range, 32 * n_words) of a non-multiple-of-32 range never appear
+        if (threadIdx.x == 0 && n_words - 1 >= w0 && n_words - 1 < w0 + W) s_bits[n_words - 1 - w0] &= last_mask;
+        __syncthreads();
+        if (w0 + W <= n_words && (reinterpret_cast<uintptr_t>(bits) & 15) == 0) {
+            uint4* g4 = reinterpret_cast<uint4*>(bits + w0);
+            for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) __stcs(g4 + i, s4[i]);
+        } else {
+            for (uint32_t i = threadIdx.x; i < W; i += BUCKET_THREADS)
+                if (w0 + i < n_words) bits[w0 + i] = s_bits[i];
+        }
+        __syncthreads();
+    }
+}
+
 // K0: max key (only when no key-range hint is given).
 __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl* __restrict__ ctrl) {
     uint32_t mx = 0;
@@ -1050,7 +1088,7 @@ size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
 cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* out,
                                uint32_t* parted, void* scratch, Ctrl* ctrl, const BucketPlan& plan,
                                const LaunchGeometry& geo, cudaStream_t stream, int* launches,
-                               KernelTimer* timer) {
+                               KernelTimer* timer, uint32_t* bits_out, uint64_t n_words) {
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     uint32_t* H = static_cast<uint32_t*>(scratch);
@@ -1093,6 +1131,17 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                 ks, plan.shift, plan.nb, H, tot, parted, base);
     if (timer) timer->after("bucket_partition", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if (bits_out) {  // multi-GPU per-rank build: write the bitset instead of sorted keys
+        if (timer) timer->before(stream);
+        bucket_bitset_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS,
+                               std::size_t(1) << (plan.shift - 3), stream>>>(
+            parted, tot, base, plan.shift, plan.nb, bits_out, n_words,
+            (key_range & 31) ? (1u << (key_range & 31)) - 1u : 0xffffffffu, ctrl);
+        if (timer) timer->after("bucket_bitset", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (launches) *launches = 4;
+        return cudaSuccess;
+    }
     if (timer) timer->before(stream);
     if (plan.cluster > 1) {
         err = launch_cluster_kb4(plan.cluster, geo, parted, tot, base, plan.nb, out, ctrl, stream);
@@ -1119,6 +1168,9 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_bitset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               1 << (MAX_BUCKET_SHIFT - 3));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bucket_sort_smem_bytes(20)));

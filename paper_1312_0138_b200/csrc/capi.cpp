@@ -543,17 +543,37 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
         ctx.init(dev);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const uint64_t words = (key_range + 31) / 32;
-        cuda_check(cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), s), "bitset clear");
         cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
-        cuda_check(timed_launch("bitset_scatter", s,
-                                [&] {
-                                    return bws_gpu::launch_scatter(keys, count, bits, key_range,
-                                                                   ctx.ctrl(), g_scatter_mode.load(),
-                                                                   ctx.geo, s);
-                                }),
-                   "bitset_scatter launch");
-        g_launches.fetch_add(1);
+        const int path = current_path();
+        const bool bucketed = count < (size_t(1) << 32) &&
+                              (path == BWS_PATH_BUCKETED || (path == BWS_PATH_AUTO && count >= kBucketedMinKeys));
+        if (bucketed) {
+            // KB1-KB3 + KB4b: SMEM-staged, coalesced, no atomics to global, no memset
+            ctx.ensure_parted(count);
+            bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range);
+            plan.cluster = 1;
+            if (plan.shift > bws_gpu::MAX_BUCKET_SHIFT) {
+                plan.shift = bws_gpu::MAX_BUCKET_SHIFT;
+                plan.nb = static_cast<int>((key_range + (1ull << plan.shift) - 1) >> plan.shift);
+            }
+            int launches = 0;
+            cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, nullptr, ctx.parted,
+                                                   ctx.bucket_scratch, ctx.ctrl(), plan, ctx.geo, s,
+                                                   &launches, active_timer(), bits, words),
+                       "bucketed bitset build launch");
+            g_launches.fetch_add(static_cast<uint64_t>(launches));
+        } else {
+            cuda_check(cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), s), "bitset clear");
+            cuda_check(timed_launch("bitset_scatter", s,
+                                    [&] {
+                                        return bws_gpu::launch_scatter(keys, count, bits, key_range,
+                                                                       ctx.ctrl(), g_scatter_mode.load(),
+                                                                       ctx.geo, s);
+                                    }),
+                       "bitset_scatter launch");
+            g_launches.fetch_add(1);
+        }
         cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
     });
 }

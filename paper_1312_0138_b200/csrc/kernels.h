@@ -133,13 +133,16 @@ cudaError_t launch_scan(const std::uint32_t* bits, std::uint64_t n_words, std::u
 BucketPlan plan_buckets(std::uint64_t key_range);
 std::size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks);
 cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo);
+// With bits_out set, KB4b writes the bitset (n_words words) instead of sorted
+// keys (multi-GPU per-rank build; no clearing of bits_out needed).
 // KB1..KB4: sorts n keys (all < key_range) into out via the `parted` buffer
 // (n keys). Adds the number of distinct keys to ctrl->total, counts keys >=
 // key_range in ctrl->bad_keys. `launches` receives the kernel count.
 cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::uint64_t key_range,
                                std::uint32_t* out, std::uint32_t* parted, void* scratch, Ctrl* ctrl,
                                const BucketPlan& plan, const LaunchGeometry& geo,
-                               cudaStream_t stream, int* launches, KernelTimer* timer = nullptr);
+                               cudaStream_t stream, int* launches, KernelTimer* timer = nullptr,
+                               std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream);

@@ -232,13 +232,15 @@ def test_device_async_and_check(capi, cuda, path):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_rank_building_blocks_emulated(capi, cuda, world):
+def test_rank_building_blocks_emulated(capi, cuda, world, path):
     """The per-rank K2/K3 calls of dist.py, with the reduce-scatter emulated by
     a sum on one GPU (ranks run one after another; nothing waits on anything)."""
     from paper_1312_0138_b200.dist import CudaRankOps, shard_bounds, slice_words
 
-    n, key_range = 200_000, 1 << 22
+    capi.set_path(getattr(capi.Path, path))
+    n, key_range = 200_000, (1 << 22) - 7  # not a multiple of 32: exercises the last-word mask
     keys = np.random.default_rng(world).choice(key_range, size=n, replace=False).astype(np.uint32)
     words, per = slice_words(key_range, world)
     ops = CudaRankOps()
