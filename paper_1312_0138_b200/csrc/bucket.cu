@@ -24,6 +24,7 @@
 // The global bitset is never materialised: 20n bytes of HBM traffic and no
 // M-proportional term. Duplicate keys are detected by sum(popcount) < n.
 #include "kernels.h"
+#include "device_util.cuh"
 
 #include <cstdlib>
 #include <string>
@@ -31,22 +32,7 @@
 namespace bws_gpu {
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, unsigned lane) {
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t o = __shfl_up_sync(kFull, v, off);
-        if (lane >= static_cast<unsigned>(off)) v += o;
-    }
-    return v;
-}
+using namespace dev;
 
 // Block-wide exclusive scan of `count` (<= MAX_BUCKETS) uint32 values in
 // `vals` (SMEM), written as 64-bit prefixes to `out64` (SMEM or global) and
@@ -230,41 +216,6 @@ __global__ void bucket_colscan_kernel(uint32_t* __restrict__ H, int P, int nb,
     if (lane == 31) tot[b] = incl;
 }
 
-// ---- TMA bulk copy + mbarrier helpers (PTX) ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// One thread: expect `bytes` on `bar` and start a bulk global->shared copy.
-__device__ __forceinline__ void tma_load_bytes(void* dst, const void* src, unsigned bytes,
-                                               unsigned long long* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // KB3: partition, one persistent CTA per SM. CTA c streams its share in
 // 16384-key tiles through a double-buffered SMEM ring filled by TMA bulk copies
 // (the next tile lands while the current one is processed). Per tile: ranks
@@ -438,56 +389,6 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     }
 }
 
-// Writes kb + bit for every set bit of x, ascending, to the padded stage.
-__device__ __forceinline__ void stage_bits(uint32_t x, uint32_t kb, uint32_t& p, uint32_t* stage) {
-    while (x) {
-        const int bt = __ffs(x) - 1;
-        x &= x - 1;
-        stage[p + (p >> 5)] = kb + static_cast<uint32_t>(bt);
-        ++p;
-    }
-}
-
-// Copies `count` staged keys to o[0, count) with coalesced stores.
-__device__ __forceinline__ void drain_stage(const uint32_t* stage, uint32_t count,
-                                            uint32_t* __restrict__ o, unsigned lane) {
-    __syncwarp();
-    for (uint32_t i = lane; i < count; i += 32) __stcs(o + i, stage[i + (i >> 5)]);
-    __syncwarp();
-}
-
-// Extracts the 32 words at s_bits[w .. w+32) (word per lane) to o[0 ..) and
-// returns the number of keys: a chunk with more than BUCKET_STAGE keys goes
-// word by word with a ballot (lane = bit, coalesced 128-byte stores), others
-// through the warp's stage.
-template <int STAGE = BUCKET_STAGE>
-__device__ __forceinline__ uint32_t extract_words32(const uint32_t* s_bits, uint32_t w,
-                                                    uint32_t key_hi, uint32_t* __restrict__ o,
-                                                    uint32_t* s_stage, unsigned lane) {
-    const uint32_t x = s_bits[w + lane];
-    const uint32_t cx = __popc(x);
-    const uint32_t incl = warp_incl_scan(cx, lane);
-    const uint32_t ctot = __shfl_sync(kFull, incl, 31);
-    if (ctot == 0) return 0;
-    if (ctot > static_cast<uint32_t>(STAGE)) {
-        const unsigned lt = lanemask_lt();
-        uint32_t q = 0;
-        const uint32_t kb = key_hi + (w << 5) + lane;
-        for (int j = 0; j < 32; ++j) {
-            const uint32_t xj = __shfl_sync(kFull, x, j);
-            const bool bit = (xj >> lane) & 1u;
-            const unsigned m = __ballot_sync(kFull, bit);
-            if (bit) __stcs(o + q + __popc(m & lt), kb + (static_cast<uint32_t>(j) << 5));
-            q += __popc(m);
-        }
-        return ctot;
-    }
-    uint32_t p = incl - cx;
-    stage_bits(x, key_hi + ((w + lane) << 5), p, s_stage);
-    drain_stage(s_stage, ctot, o, lane);
-    return ctot;
-}
-
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
 // with 4 per thread in flight, tail.
@@ -639,6 +540,8 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
                 }
                 o += ctot;
             }
+        } else if (seg_words % 512 == 0) {
+            extract_span512<BUCKET_STAGE>(s_bits, seg, seg_words, key_hi, o, s_stage, lane, false, nullptr);
         } else if (seg_words >= 128) {
             // 128-word steps, lane-major (lane owns 4 words); a step with
             // <= BUCKET_STAGE keys is extracted in one pass, denser steps fall

@@ -79,7 +79,9 @@ void cuda_check(cudaError_t err, const char* what) {
 constexpr uint64_t kMaxKeyRange = 1ull << 32;
 constexpr uint64_t kMaxWords = kMaxKeyRange / 32;               // 2^27 words = 512 MiB
 constexpr size_t kMaxTiles = (kMaxWords + bws_gpu::SCAN_TILE_WORDS - 1) / bws_gpu::SCAN_TILE_WORDS;
-constexpr size_t kCtrlBytes = sizeof(Ctrl) + kMaxTiles * sizeof(unsigned long long);
+// Ctrl + tile status (v1: 8 B per 2048-word tile; the two-pass v2 scan keeps
+// offsets, tile counts and 16 segment counts per 8192-word tile there)
+constexpr size_t kCtrlBytes = sizeof(Ctrl) + 4 * kMaxTiles * sizeof(unsigned long long);
 
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_scatter_mode{bws_gpu::kAuto};
@@ -128,6 +130,7 @@ struct DeviceCtx {
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         cuda_check(bws_gpu::query_geometry(dev, &geo), "occupancy query");
         cuda_check(bws_gpu::configure_bucket_kernels(dev, &geo), "bucket kernel configuration");
+        cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaMalloc(&bits, kMaxWords * sizeof(uint32_t)), "cudaMalloc(bitset 512 MiB)");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes), "cudaMalloc(control block)");
@@ -244,6 +247,37 @@ EventTimer g_timer;
 
 bws_gpu::KernelTimer* active_timer() { return g_timer.enabled.load() ? &g_timer : nullptr; }
 
+// K3: v2 (TMA tiles, 128-wide lookback) unless the bitset is not 16-byte
+// aligned or BITSORT_SCAN=v1 asks for the first version (A/B runs).
+// Two-pass (tile counts first, then extraction without lookback) when the
+// bitset is large relative to the output: the single-pass lookback chain
+// stalls on sparse bitsets (measured C4 512 MiB: 584 us single pass).
+// BITSORT_SCAN=v1|lookback|twopass forces a variant (A/B runs).
+cudaError_t launch_scan_any(const uint32_t* bits, uint64_t n_words, uint32_t key_base, uint32_t* out,
+                            uint64_t cap, Ctrl* ctrl, unsigned long long* status,
+                            unsigned long long* d_total, int clear, const bws_gpu::LaunchGeometry& geo,
+                            cudaStream_t s) {
+    static const int mode = [] {
+        const char* e = std::getenv("BITSORT_SCAN");
+        if (!e) return 0;
+        if (std::strcmp(e, "v1") == 0) return 1;
+        if (std::strcmp(e, "lookback") == 0) return 2;
+        if (std::strcmp(e, "twopass") == 0) return 3;
+        return 0;
+    }();
+    int launches = 1;
+    cudaError_t err;
+    if (mode != 1 && bws_gpu::scan2_supported(bits)) {
+        const bool two = n_words != 0 && (mode == 3 || (mode == 0 && n_words * 4 >= cap));
+        err = bws_gpu::launch_scan2(const_cast<uint32_t*>(bits), n_words, key_base, out, cap, ctrl,
+                                    status, d_total, clear, geo, s, two ? 1 : 0, &launches);
+    } else {
+        err = bws_gpu::launch_scan(bits, n_words, key_base, out, cap, ctrl, status, d_total, clear, geo, s);
+    }
+    g_launches.fetch_add(static_cast<uint64_t>(launches - 1));  // callers count one
+    return err;
+}
+
 // Brackets one direct-path launch with the timer when it is enabled.
 template <class F>
 cudaError_t timed_launch(const char* name, cudaStream_t s, F&& launch) {
@@ -310,9 +344,9 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
     g_launches.fetch_add(1);
     cuda_check(timed_launch("bitset_scan", stream,
                             [&] {
-                                return bws_gpu::launch_scan(ctx.bits, words, 0u, out, count,
-                                                            ctx.ctrl(), ctx.status(), nullptr,
-                                                            /*clear=*/1, ctx.geo, stream);
+                                return launch_scan_any(ctx.bits, words, 0u, out, count, ctx.ctrl(),
+                                                       ctx.status(), nullptr, /*clear=*/1, ctx.geo,
+                                                       stream);
                             }),
                "bitset_scan launch");
     g_launches.fetch_add(1);
@@ -602,7 +636,7 @@ bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t 
                    "control block reset");
         cuda_check(timed_launch("bitset_scan", s,
                                 [&] {
-                                    return bws_gpu::launch_scan(
+                                    return launch_scan_any(
                                         bits, n_words, key_base, out, out_capacity, ctx.ctrl(),
                                         ctx.status(), reinterpret_cast<unsigned long long*>(d_total),
                                         /*clear=*/0, ctx.geo, s);

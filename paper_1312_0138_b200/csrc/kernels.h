@@ -27,6 +27,14 @@ constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ROUNDS = 8;
 constexpr int SCAN_TILE_WORDS = SCAN_THREADS * SCAN_ROUNDS;  // 2048 words = 65536 keys
 
+// K3 v2 geometry (scan.cu): 8192-word tiles via TMA, 16 warps, 2 CTAs/SM.
+constexpr int SCAN2_THREADS = 512;
+constexpr int SCAN2_TILE_WORDS = 8192;
+constexpr int SCAN2_STAGE = 512;  // keys per warp stage
+constexpr std::size_t scan2_smem_bytes() {
+    return 2 * SCAN2_TILE_WORDS * 4 + (SCAN2_THREADS / 32) * (SCAN2_STAGE + SCAN2_STAGE / 32) * 4;  // 2nd buffer spare
+}
+
 // K2 geometry: a tile is SCATTER_VEC uint4 loads per thread.
 constexpr int SCATTER_THREADS = 256;
 constexpr int SCATTER_VEC = 4;
@@ -80,6 +88,7 @@ struct LaunchGeometry {
     int part_blocks_narrow = 0;                  // KB1/KB3 shares, narrow KB3 variant
     int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
     int clusters[4] = {};                          // cluster KB4: max clusters for R = 1,2,4,8
+    int scan2_blocks = 0;                          // K3 v2 CTAs
 };
 
 // A key array as seen by the bucketed kernels: 16-byte-aligned uint4 body plus
@@ -127,6 +136,18 @@ cudaError_t launch_scan(const std::uint32_t* bits, std::uint64_t n_words, std::u
                         std::uint32_t* out, std::uint64_t out_capacity, Ctrl* ctrl,
                         unsigned long long* status, unsigned long long* d_total, int clear,
                         const LaunchGeometry& geo, cudaStream_t stream);
+
+// K3 v2 (scan.cu): same contract as launch_scan; needs a 16-byte-aligned
+// bitset (scan2_supported). status needs ceil(n_words / 8192) zeroed words.
+bool scan2_supported(const std::uint32_t* bits);
+cudaError_t configure_scan2(int device, LaunchGeometry* geo);
+// two_pass: tile popcounts + their prefix first (no lookback; needs
+// n_words > 0 known on the host), then the same extraction.
+cudaError_t launch_scan2(std::uint32_t* bits, std::uint64_t n_words, std::uint32_t key_base,
+                         std::uint32_t* out, std::uint64_t out_capacity, Ctrl* ctrl,
+                         unsigned long long* status, unsigned long long* d_total, int clear,
+                         const LaunchGeometry& geo, cudaStream_t stream, int two_pass,
+                         int* launches);
 
 // Bucketed pipeline (bucket.cu). plan_buckets picks the bucket width for a
 // key range; bucket_scratch_bytes sizes the histogram/offset scratch.
