@@ -389,6 +389,163 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     }
 }
 
+
+// KB3 "xwide" for more than 1024 buckets: one 24576-key tile per iteration
+// (96 KB of the SMEM tile space, filled by two TMA bulk copies), so each
+// bucket's run per tile is 1.5x as long as with 16384-key tiles (at
+// 4096 buckets, 4-key runs measured +55% partial-sector DRAM traffic). The 24
+// keys of a thread stay in registers; ranks come from a counting pass
+// (SMEM atomics without return) and a fill pass (atomics with return).
+__global__ void __launch_bounds__(PART_THREADS, 1)
+    bucket_partition_xwide_kernel(KeySplit ks, int shift, int nb,
+                                  const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
+                                  uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int KPT = 24;
+    constexpr int TILE = PART_THREADS * KPT;  // 24576
+    constexpr int kSlots = MAX_BUCKETS + 1;
+    constexpr int NWARPS = PART_THREADS / 32;
+    uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // TILE keys
+    uint32_t* s_cnt = s_buf + TILE;        // keys per bucket in the tile, then fill pointers
+    uint32_t* s_start = s_cnt + kSlots;    // (unused slot kept for the shared layout)
+    uint32_t* s_cur = s_start + kSlots;    // next free global slot
+    uint32_t* s_delta = s_cur + kSlots;    // global slot - local index
+    __shared__ unsigned long long s_scratch[33];
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    __shared__ uint32_t s_tile_valid;
+
+    const unsigned P = gridDim.x, c = blockIdx.x;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t vlo = ks.nv * c / P, vhi = ks.nv * (c + 1) / P;
+    constexpr size_t kTileVec = TILE / 4;
+    constexpr size_t kHalfVec = kTileVec / 2;
+    const size_t ntiles = (vhi - vlo + kTileVec - 1) / kTileVec;
+    const uint32_t spill = static_cast<uint32_t>(nb);
+    auto load_tile = [&](size_t t, unsigned parity_unused) {  // thread 0
+        const size_t v0 = vlo + t * kTileVec;
+        const size_t nvec = min(kTileVec, vhi - v0);
+        const size_t n0 = min(kHalfVec, nvec), n1 = nvec - n0;
+        fence_proxy_async_smem();
+        tma_load_bytes(s_buf, ks.body + v0, static_cast<unsigned>(n0 * 16), &s_bar[0]);
+        if (n1) tma_load_bytes(s_buf + TILE / 2, ks.body + v0 + n0, static_cast<unsigned>(n1 * 16), &s_bar[1]);
+        (void)parity_unused;
+    };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && ntiles > 0) load_tile(0, 0);
+
+    unsigned long long* s_base64 = reinterpret_cast<unsigned long long*>(s_cnt);  // spans cnt+start
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cur[b] = tot[b];
+    __syncthreads();
+    const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        if (c == 0) g_base[b] = s_base64[b];
+        s_delta[b] = static_cast<uint32_t>(s_base64[b] + H[static_cast<size_t>(b) * P + c]);
+    }
+    if (c == 0 && threadIdx.x == 0) g_base[nb] = total;
+    __syncthreads();
+    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+        s_cur[b] = b < nb ? s_delta[b] : 0u;
+        s_cnt[b] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // misaligned head (CTA 0) / tail (CTA P-1) keys
+        const uint32_t* extra = c == 0 ? ks.head : nullptr;
+        int ne = c == 0 ? ks.n_head : 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = 0; i < ne; ++i) {
+                const uint32_t b = bucket_or_spill(extra[i], true, shift, nb);
+                if (b != spill) parted[s_cur[b]++] = extra[i];
+            }
+            extra = c == P - 1 ? ks.tail : nullptr;
+            ne = c == P - 1 ? ks.n_tail : 0;
+        }
+    }
+    __syncthreads();
+
+    const int slots = nb + 1;
+    const int per = (slots + PART_THREADS - 1) / PART_THREADS;
+    const int sb = threadIdx.x * per;
+    for (size_t t = 0; t < ntiles; ++t) {
+        const size_t v0 = vlo + t * kTileVec;
+        const uint32_t nvec = static_cast<uint32_t>(min(kTileVec, vhi - v0));
+        mbar_wait(&s_bar[0], static_cast<unsigned>(t & 1));
+        if (nvec > kHalfVec) mbar_wait(&s_bar[1], static_cast<unsigned>(t & 1));  // only the last tile can be short
+        uint32_t k[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT / 4; ++j) {
+            const uint32_t vi = j * PART_THREADS + threadIdx.x;
+            const uint4 v = vi < nvec ? reinterpret_cast<const uint4*>(s_buf)[vi] : make_uint4(0, 0, 0, 0);
+            k[4 * j] = vi < nvec ? v.x : 0xffffffffu;
+            k[4 * j + 1] = v.y;
+            k[4 * j + 2] = v.z;
+            k[4 * j + 3] = v.w;
+            if (vi >= nvec) k[4 * j] = k[4 * j + 1] = k[4 * j + 2] = k[4 * j + 3] = 0u;
+        }
+        // counting pass (padding lanes count into the spill slot)
+#pragma unroll
+        for (int j = 0; j < KPT / 4; ++j) {
+            const bool in = j * PART_THREADS + threadIdx.x < nvec;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) atomicAdd(s_cnt + bucket_or_spill(k[4 * j + q], in, shift, nb), 1u);
+        }
+        __syncthreads();  // counts complete; every thread holds its keys
+        {
+            uint32_t local = 0;
+            for (int q = 0; q < per; ++q)
+                if (sb + q < slots) local += s_cnt[sb + q];
+            const uint32_t incl = warp_incl_scan(local, lane);
+            if (lane == 31) s_scratch[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = lane < NWARPS ? static_cast<uint32_t>(s_scratch[lane]) : 0u;
+                const uint32_t wi = warp_incl_scan(w, lane);
+                if (lane < NWARPS) s_scratch[lane] = wi - w;
+            }
+            __syncthreads();
+            uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
+            for (int q = 0; q < per; ++q) {
+                const int b = sb + q;
+                if (b < slots) {
+                    const uint32_t cb = s_cnt[b];
+                    s_delta[b] = s_cur[b] - run;
+                    s_cur[b] += cb;
+                    s_cnt[b] = run;  // fill pointer for the scatter
+                    if (b == nb) s_tile_valid = run;
+                    run += cb;
+                }
+            }
+        }
+        __syncthreads();
+        // fill pass: in-place counting-sort scatter
+#pragma unroll
+        for (int j = 0; j < KPT / 4; ++j) {
+            const bool in = j * PART_THREADS + threadIdx.x < nvec;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t b = bucket_or_spill(k[4 * j + q], in, shift, nb);
+                s_buf[atomicAdd(s_cnt + b, 1u)] = k[4 * j + q];
+            }
+        }
+        __syncthreads();
+        const uint32_t tile_valid = s_tile_valid;
+#pragma unroll 4
+        for (uint32_t i = threadIdx.x; i < tile_valid; i += PART_THREADS) {
+            const uint32_t key = s_buf[i];
+            parted[s_delta[key >> shift] + i] = key;
+        }
+        for (int q = 0; q < per; ++q)
+            if (sb + q < slots) s_cnt[sb + q] = 0;
+        __syncthreads();  // tile buffer free
+        if (threadIdx.x == 0 && t + 1 < ntiles) load_tile(t + 1, 0);
+    }
+}
+
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
 // with 4 per thread in flight, tail.
@@ -1024,7 +1181,12 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (timer) timer->after("bucket_colscan", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (timer) timer->before(stream);
-    if (narrow_partition(plan))
+    // xwide measured slightly slower (C4 KB3 121 vs 112 us, C5 1576 vs 1535 us):
+    // opt-in only (BITSORT_XWIDE=1)
+    if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE"))
+        bucket_partition_xwide_kernel<<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
+            ks, plan.shift, plan.nb, H, tot, parted, base);
+    else if (narrow_partition(plan))
         bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB>
             <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                 ks, plan.shift, plan.nb, H, tot, parted, base);
@@ -1067,6 +1229,9 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS>;
     auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB>;
     err = cudaFuncSetAttribute(wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_xwide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,

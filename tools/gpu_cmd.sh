@@ -1,5 +1,6 @@
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_plain.json 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_bench.log 2>&1
-python tools/run_one.py --config C2 --iters 1 > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"bucket_" -c 4 -o gpurun_out/prof_c2_final python tools/run_one.py --config C2 --iters 1 > gpurun_out/ncu_full.log 2>&1
-for c in C3 C4 C5; do python tools/run_one.py --config $c --iters 1 > gpurun_out/plain_$c.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/traffic_$c.csv python tools/run_one.py --config $c --iters 1 > /dev/null 2>&1; done
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "BUCKETED" > gpurun_out/pytest_quick.log 2>&1; echo quick_exit=$? >> gpurun_out/pytest_quick.log
+if grep -q "quick_exit=0" gpurun_out/pytest_quick.log; then
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --config all --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_all.json 2> gpurun_out/bench_all.err
+for c in C4 C5; do BITSORT_NO_XWIDE=1 timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_noxw_$c.json 2>&1; done
+fi
