@@ -390,6 +390,20 @@ def run_ours(args, cfg):
            "api": "dist.distributed_sort on pinned host shards" if use_dist
            else "bws_sort (C ABI) on a pinned host array"}
 
+    if not use_dist:  # the same drop-in call on ordinary (pageable) host memory
+        pg = shard_h.copy()
+        ptimes = []
+        for i in range(min(e2e_steps, 3) + 1):
+            np.copyto(pg, shard_h)
+            t_a = time.perf_counter()
+            capi.sort(pg)
+            if i > 0:
+                ptimes.append(time.perf_counter() - t_a)
+        assert np.all(pg[1:] > pg[:-1])
+        e2e["pageable"] = {"value": round(n_total / (sum(ptimes) / len(ptimes)) / 1e9, 4),
+                           "ms_per_step": round(1e3 * sum(ptimes) / len(ptimes), 3)}
+        del pg
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(keys_h, args.cpu_sample_keys, cfg.name)

@@ -268,7 +268,10 @@ cudaError_t launch_scan_any(const uint32_t* bits, uint64_t n_words, uint32_t key
     int launches = 1;
     cudaError_t err;
     if (mode != 1 && bws_gpu::scan2_supported(bits)) {
-        const bool two = n_words != 0 && (mode == 3 || (mode == 0 && n_words * 4 >= cap));
+        // two-pass only for large sparse bitsets (>= 16 MiB, at least 1 word per key);
+        // small ones (C1) are latency-bound and one kernel is cheaper than three
+        const bool two = n_words != 0 && (mode == 3 || (mode == 0 && n_words * 4 >= cap &&
+                                                         n_words >= (uint64_t(1) << 22)));
         err = bws_gpu::launch_scan2(const_cast<uint32_t*>(bits), n_words, key_base, out, cap, ctrl,
                                     status, d_total, clear, geo, s, two ? 1 : 0, &launches);
     } else {

@@ -343,3 +343,41 @@ def test_distributed_sort_nccl_single_rank(capi, cuda):
             distributed_sort(cuda.from_numpy(bad.view(np.int32)).cuda(), 1 << 24)
     finally:
         dist.destroy_process_group()
+
+
+def test_concurrent_host_threads(capi):
+    """The reference is reentrant: concurrent bws_sort calls from
+    several host threads on distinct arrays must all succeed."""
+    import threading
+
+    rng = np.random.default_rng(123)
+    arrays = [rng.choice(1 << 26, size=200_000 + 1000 * i, replace=False).astype(np.uint32) for i in range(6)]
+    expected = [np.sort(a) for a in arrays]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                a = arrays[i].copy()
+                capi.sort(a)
+                assert np.array_equal(a, expected[i])
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(arrays))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+
+
+def test_pageable_and_pinned_host_paths(capi, cuda):
+    keys = np.random.default_rng(9).choice(1 << 28, size=1 << 21, replace=False).astype(np.uint32)
+    pageable = keys.copy()
+    capi.sort(pageable)
+    pinned_t = cuda.empty(keys.size, dtype=cuda.int32, pin_memory=True)
+    pinned = pinned_t.numpy().view(np.uint32)
+    np.copyto(pinned, keys)
+    capi.sort(pinned)
+    assert np.array_equal(pageable, np.sort(keys)) and np.array_equal(pinned, pageable)
