@@ -225,15 +225,24 @@ __global__ void bucket_colscan_kernel(uint32_t* __restrict__ H, int P, int nb,
 // tile buffer, then thread i stores sorted key i to parted[delta[bucket] + i]:
 // consecutive threads write consecutive addresses within each bucket run.
 // Slot positions are 32-bit (the bucketed path requires n < 2^32).
-template <int THREADS, int KPT, int MAXB>
+//
+// Packed layout (SLAB false): a CTA's slots in every bucket come from KB1/KB2.
+// Slab layout (SLAB true, see SlabArgs): each tile claims its run in every
+// bucket with one global atomicAdd per non-empty bucket; the claims are
+// issued before the tile's SMEM scatter and consumed after it, so their
+// latency overlaps that work. The last CTA to finish turns the fill counters
+// into bucket totals and output offsets for KB4.
+template <int THREADS, int KPT, int MAXB, bool SLAB>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     bucket_partition_kernel(KeySplit ks, int shift, int nb,
                             const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
-                            uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base) {
+                            uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base,
+                            SlabArgs sa) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int kSlots = MAXB + 1;
     constexpr int TILE = THREADS * KPT;
     constexpr int NWARPS = THREADS / 32;
+    constexpr int PER_MAX = (kSlots + THREADS - 1) / THREADS;
     uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 x TILE
     uint32_t* s_cnt = s_buf + 2 * TILE;                   // keys per bucket in the tile
     uint32_t* s_start = s_cnt + kSlots;                        // tile-local bucket start
@@ -242,6 +251,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     __shared__ unsigned long long s_scratch[33];
     __shared__ __align__(8) unsigned long long s_bar[2];
     __shared__ uint32_t s_tile_valid;
+    __shared__ uint32_t s_last;
 
     const unsigned P = gridDim.x, c = blockIdx.x;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -265,19 +275,22 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         }
     }
 
-    // bucket bases (exclusive prefix of totals) + this CTA's first slot per bucket
     unsigned long long* s_base64 = reinterpret_cast<unsigned long long*>(s_cnt);  // spans cnt+start
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cur[b] = tot[b];
-    __syncthreads();
-    const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        if (c == 0) g_base[b] = s_base64[b];
-        s_delta[b] = static_cast<uint32_t>(s_base64[b] + H[static_cast<size_t>(b) * P + c]);
+    uint32_t bad = 0;  // slab: keys >= sa.limit (KB1 counts them in the packed layout)
+    if constexpr (!SLAB) {
+        // bucket bases (exclusive prefix of totals) + this CTA's first slot per bucket
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cur[b] = tot[b];
+        __syncthreads();
+        const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            if (c == 0) g_base[b] = s_base64[b];
+            s_delta[b] = static_cast<uint32_t>(s_base64[b] + H[static_cast<size_t>(b) * P + c]);
+        }
+        if (c == 0 && threadIdx.x == 0) g_base[nb] = total;
+        __syncthreads();
     }
-    if (c == 0 && threadIdx.x == 0) g_base[nb] = total;
-    __syncthreads();
     for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
-        s_cur[b] = b < nb ? s_delta[b] : 0u;
+        if constexpr (!SLAB) s_cur[b] = b < nb ? s_delta[b] : 0u;
         s_cnt[b] = 0;
     }
     __syncthreads();
@@ -287,7 +300,15 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
                 const uint32_t b = bucket_or_spill(extra[i], true, shift, nb);
-                if (b != spill) parted[s_cur[b]++] = extra[i];
+                if constexpr (SLAB) {
+                    bad += (sa.check && extra[i] >= sa.limit) ? 1u : 0u;
+                    if (b != spill) {
+                        const uint32_t pos = atomicAdd(sa.gcnt + b, 1u);
+                        if (pos < sa.cap) parted[b * sa.cap + pos] = extra[i];
+                    }
+                } else {
+                    if (b != spill) parted[s_cur[b]++] = extra[i];
+                }
             }
             extra = c == P - 1 ? ks.tail : nullptr;
             ne = c == P - 1 ? ks.n_tail : 0;
@@ -323,6 +344,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 rb[4 * j + q] = bucket_or_spill(kk[q], in, shift, nb);
                 kmin = min(kmin, kk[q]);
                 kmax = max(kmax, kk[q]);
+                if constexpr (SLAB) bad += (sa.check && in && kk[q] >= sa.limit) ? 1u : 0u;
             }
         }
         const uint32_t blo = bucket_or_spill(__reduce_min_sync(kFull, kmin), true, shift, nb);
@@ -339,6 +361,8 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             for (int q = 0; q < KPT; ++q) rb[q] = (rb[q] << 16) | atomicAdd(s_cnt + rb[q], 1u);
         }
         __syncthreads();  // A: tile counts complete; every thread has read buf
+        uint32_t claim[SLAB ? PER_MAX : 1];  // slab: first claimed slot per bucket (in flight)
+        uint32_t ccnt[SLAB ? PER_MAX : 1];
         {
             uint32_t local = 0;
             for (int q = 0; q < per; ++q)
@@ -353,16 +377,33 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             }
             __syncthreads();
             uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
-            for (int q = 0; q < per; ++q) {
-                const int b = sb + q;
-                if (b < slots) {
-                    const uint32_t cb = s_cnt[b];
-                    s_start[b] = run;
-                    s_delta[b] = s_cur[b] - run;
-                    s_cur[b] += cb;
-                    s_cnt[b] = 0;
-                    if (b == nb) s_tile_valid = run;  // spill keys sort after every bucket
-                    run += cb;
+            if constexpr (SLAB) {
+#pragma unroll
+                for (int q = 0; q < PER_MAX; ++q) {
+                    const int b = sb + q;
+                    ccnt[q] = 0;
+                    if (q < per && b < slots) {
+                        const uint32_t cb = s_cnt[b];
+                        s_start[b] = run;
+                        s_cnt[b] = 0;
+                        if (b == nb) s_tile_valid = run;  // spill keys sort after every bucket
+                        else if (cb) claim[q] = atomicAdd(sa.gcnt + b, cb);
+                        ccnt[q] = b < nb ? cb : 0u;
+                        run += cb;
+                    }
+                }
+            } else {
+                for (int q = 0; q < per; ++q) {
+                    const int b = sb + q;
+                    if (b < slots) {
+                        const uint32_t cb = s_cnt[b];
+                        s_start[b] = run;
+                        s_delta[b] = s_cur[b] - run;
+                        s_cur[b] += cb;
+                        s_cnt[b] = 0;
+                        if (b == nb) s_tile_valid = run;  // spill keys sort after every bucket
+                        run += cb;
+                    }
                 }
             }
         }
@@ -372,6 +413,18 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         for (int q = 0; q < KPT; ++q) rb[q] = s_start[rb[q] >> 16] + (rb[q] & 0xffffu);
 #pragma unroll
         for (int q = 0; q < KPT; ++q) buf[rb[q]] = k[q];
+        if constexpr (SLAB) {
+#pragma unroll
+            for (int q = 0; q < PER_MAX; ++q) {
+                if (ccnt[q]) {
+                    const uint32_t b = sb + q;
+                    // a claim past the bucket's capacity (only duplicates can cause
+                    // one) lands in the dump tile instead
+                    const uint32_t dst = claim[q] + ccnt[q] <= sa.cap ? b * sa.cap + claim[q] : sa.dump;
+                    s_delta[b] = dst - s_start[b];
+                }
+            }
+        }
         __syncthreads();  // C
         const uint32_t tile_valid = s_tile_valid;
 #pragma unroll 4
@@ -385,6 +438,32 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             const size_t nv2 = min(kTileVec, vhi - v2);
             fence_proxy_async_smem();
             tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
+        }
+    }
+    if constexpr (SLAB) {
+        const uint32_t wb = __reduce_add_sync(kFull, bad);
+        if (lane == 0 && wb) atomicAdd(&sa.ctrl->bad_keys, wb);
+        // last CTA out: bucket totals (0 for an overflowed bucket: its keys are
+        // lost, so the sort sees fewer set bits than keys) and output offsets
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&sa.ctrl->done_ctas, 1u) == P - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+                const uint32_t v = __ldcg(sa.gcnt + b);
+                s_cur[b] = v <= sa.cap ? v : 0u;
+            }
+            __syncthreads();
+            const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
+            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+                sa.g_base[b] = s_base64[b];
+                sa.tot[b] = s_cur[b];
+            }
+            if (threadIdx.x == 0) sa.g_base[nb] = total;
         }
     }
 }
@@ -601,10 +680,11 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
 // each touched word in a summary bitset (one bit per word), visit only
 // touched words, and zero exactly those words again, so a sparse bucket costs
 // O(keys) SMEM work instead of O(2^shift / 32) and leaves the bitset clean.
+template <int STAGE>
 __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, int shift, int nb,
-                       uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
+                       uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t W = 1u << (shift - 5);  // words per bucket bitset (>= 1024)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
@@ -615,7 +695,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
 
     const unsigned lane = threadIdx.x & 31;
     const unsigned warp = threadIdx.x >> 5;
-    constexpr int kStagePitch = BUCKET_STAGE + BUCKET_STAGE / 32;
+    constexpr int kStagePitch = STAGE + STAGE / 32;
     uint32_t* s_stage = s_stage_all + warp * kStagePitch;
     const uint32_t seg_words = W / (BUCKET_THREADS / 32);
     const uint32_t lowmask = (1u << shift) - 1;
@@ -634,7 +714,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         if (b >= static_cast<unsigned>(nb)) break;
         const unsigned long long base = g_base[b];
         const uint32_t cnt = tot[b];
-        const uint32_t* src = parted + base;
+        const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         if (sparse)
             scatter_bucket_keys<true>(src, cnt, lowmask, s_bits, s_sum);
@@ -698,7 +778,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
                 o += ctot;
             }
         } else if (seg_words % 512 == 0) {
-            extract_span512<BUCKET_STAGE>(s_bits, seg, seg_words, key_hi, o, s_stage, lane, false, nullptr);
+            extract_span512<STAGE>(s_bits, seg, seg_words, key_hi, o, s_stage, lane, false, nullptr);
         } else if (seg_words >= 128) {
             // 128-word steps, lane-major (lane owns 4 words); a step with
             // <= BUCKET_STAGE keys is extracted in one pass, denser steps fall
@@ -709,7 +789,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
                 const uint32_t incl = warp_incl_scan(cl, lane);
                 const uint32_t ctot = __shfl_sync(kFull, incl, 31);
                 if (ctot == 0) continue;
-                if (ctot <= static_cast<uint32_t>(BUCKET_STAGE)) {
+                if (ctot <= static_cast<uint32_t>(STAGE)) {
                     uint32_t p = incl - cl;
                     const uint32_t kb = key_hi + ((seg + w0 + 4 * lane) << 5);
                     stage_bits(v.x, kb, p, s_stage);
@@ -722,11 +802,11 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
                 }
 #pragma unroll 1
                 for (uint32_t q = 0; q < 128; q += 32)
-                    o += extract_words32(s_bits, seg + w0 + q, key_hi, o, s_stage, lane);
+                    o += extract_words32<STAGE>(s_bits, seg + w0 + q, key_hi, o, s_stage, lane);
             }
         } else {
             for (uint32_t w0 = 0; w0 < seg_words; w0 += 32)
-                o += extract_words32(s_bits, seg + w0, key_hi, o, s_stage, lane);
+                o += extract_words32<STAGE>(s_bits, seg + w0, key_hi, o, s_stage, lane);
         }
         dirty = !sparse;
         __syncthreads();
@@ -991,7 +1071,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
 __global__ void __launch_bounds__(BUCKET_THREADS, 1)
     bucket_bitset_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                          const unsigned long long* __restrict__ g_base, int shift, int nb,
-                         uint32_t* __restrict__ bits, unsigned long long n_words,
+                         uint32_t src_cap, uint32_t* __restrict__ bits, unsigned long long n_words,
                          uint32_t last_mask, Ctrl* __restrict__ ctrl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t W = 1u << (shift - 5);
@@ -1005,7 +1085,8 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
         __syncthreads();
         const unsigned b = s_b;
         if (b >= static_cast<unsigned>(nb)) break;
-        scatter_bucket_keys<false>(parted + g_base[b], tot[b], lowmask, s_bits, nullptr);
+        scatter_bucket_keys<false>(parted + (src_cap ? static_cast<size_t>(b) * src_cap : g_base[b]), tot[b],
+                                   lowmask, s_bits, nullptr);
         __syncthreads();
         const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
         // keys in [key_range, 32 * n_words) of a non-multiple-of-32 range never appear
@@ -1139,8 +1220,24 @@ BucketPlan plan_buckets(uint64_t key_range) {
     return p;
 }
 
+uint64_t slab_slots(const BucketPlan& plan, size_t n) {
+    static const bool off = [] {
+        const char* e = std::getenv("BITSORT_SLAB");
+        return e && std::string(e) == "0";
+    }();
+    if (off || plan.cluster > 1 || narrow_partition(plan) ||
+        (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE")))
+        return 0;
+    uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
+    if (cap > (1ull << plan.shift)) cap = 1ull << plan.shift;
+    const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_TILE;  // + dump tile
+    // the slab trades memory (up to 4 slots per key) for the histogram pass
+    if (slots > 4 * static_cast<uint64_t>(n) + PART_TILE || slots >= (1ull << 32)) return 0;
+    return slots;
+}
+
 size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
-    return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H
+    return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H (slab: fill counters)
            + MAX_BUCKETS * sizeof(uint32_t)                                // tot
            + (MAX_BUCKETS + 1) * sizeof(unsigned long long);               // base
 }
@@ -1148,7 +1245,8 @@ size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
 cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* out,
                                uint32_t* parted, void* scratch, Ctrl* ctrl, const BucketPlan& plan,
                                const LaunchGeometry& geo, cudaStream_t stream, int* launches,
-                               KernelTimer* timer, uint32_t* bits_out, uint64_t n_words) {
+                               KernelTimer* timer, uint32_t* bits_out, uint64_t n_words,
+                               uint64_t parted_cap) {
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     uint32_t* H = static_cast<uint32_t*>(scratch);
@@ -1168,43 +1266,71 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     ks.tail = keys + n_head + 4 * ks.nv;
     ks.n_tail = static_cast<int>(n - n_head - 4 * ks.nv);
 
-    cudaError_t err = cudaMemsetAsync(H, 0, static_cast<size_t>(P) * plan.nb * sizeof(uint32_t), stream);
-    if (err != cudaSuccess) return err;
-    if (timer) timer->before(stream);
-    bucket_hist_kernel<<<P * HIST_SPLIT, BUCKET_HIST_THREADS, 0, stream>>>(ks, plan.shift, plan.nb,
-                                                                           limit, check, H, ctrl);
-    if (timer) timer->after("bucket_hist", stream);
-    err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
-    if (timer) timer->before(stream);
-    bucket_colscan_kernel<<<(plan.nb * 32 + 255) / 256, 256, 0, stream>>>(H, P, plan.nb, tot);
-    if (timer) timer->after("bucket_colscan", stream);
-    if ((err = cudaGetLastError()) != cudaSuccess) return err;
-    if (timer) timer->before(stream);
-    // xwide measured slightly slower (C4 KB3 121 vs 112 us, C5 1576 vs 1535 us):
-    // opt-in only (BITSORT_XWIDE=1)
-    if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE"))
-        bucket_partition_xwide_kernel<<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
-            ks, plan.shift, plan.nb, H, tot, parted, base);
-    else if (narrow_partition(plan))
-        bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB>
-            <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
-                ks, plan.shift, plan.nb, H, tot, parted, base);
-    else
-        bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS>
+    const uint64_t slab = slab_slots(plan, n);
+    const bool use_slab = slab != 0 && slab <= parted_cap;
+    SlabArgs sa;
+    int nlaunch = 0;
+    cudaError_t err;
+    if (use_slab) {
+        // KB3 (slab) claims slots with fill counters: no KB1/KB2
+        sa.gcnt = H;
+        sa.cap = static_cast<uint32_t>((slab - PART_TILE) / plan.nb);
+        sa.dump = static_cast<uint32_t>(slab - PART_TILE);
+        sa.limit = limit;
+        sa.check = check;
+        sa.ctrl = ctrl;
+        sa.tot = tot;
+        sa.g_base = base;
+        err = cudaMemsetAsync(H, 0, static_cast<size_t>(plan.nb) * sizeof(uint32_t), stream);
+        if (err != cudaSuccess) return err;
+        if (timer) timer->before(stream);
+        bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
             <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
+                ks, plan.shift, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+        if (timer) timer->after("bucket_partition", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        nlaunch = 1;
+    } else {
+        err = cudaMemsetAsync(H, 0, static_cast<size_t>(P) * plan.nb * sizeof(uint32_t), stream);
+        if (err != cudaSuccess) return err;
+        if (timer) timer->before(stream);
+        bucket_hist_kernel<<<P * HIST_SPLIT, BUCKET_HIST_THREADS, 0, stream>>>(ks, plan.shift, plan.nb,
+                                                                               limit, check, H, ctrl);
+        if (timer) timer->after("bucket_hist", stream);
+        err = cudaGetLastError();
+        if (err != cudaSuccess) return err;
+        if (timer) timer->before(stream);
+        bucket_colscan_kernel<<<(plan.nb * 32 + 255) / 256, 256, 0, stream>>>(H, P, plan.nb, tot);
+        if (timer) timer->after("bucket_colscan", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (timer) timer->before(stream);
+        // xwide measured slightly slower (C4 KB3 121 vs 112 us, C5 1576 vs 1535 us):
+        // opt-in only (BITSORT_XWIDE=1)
+        if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE"))
+            bucket_partition_xwide_kernel<<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
                 ks, plan.shift, plan.nb, H, tot, parted, base);
-    if (timer) timer->after("bucket_partition", stream);
-    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        else if (narrow_partition(plan))
+            bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>
+                <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
+                    ks, plan.shift, plan.nb, H, tot, parted, base, sa);
+        else
+            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
+                    ks, plan.shift, plan.nb, H, tot, parted, base, sa);
+        if (timer) timer->after("bucket_partition", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        nlaunch = 3;
+    }
+    const uint32_t src_cap = use_slab ? sa.cap : 0u;
     if (bits_out) {  // multi-GPU per-rank build: write the bitset instead of sorted keys
         if (timer) timer->before(stream);
         bucket_bitset_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS,
                                std::size_t(1) << (plan.shift - 3), stream>>>(
-            parted, tot, base, plan.shift, plan.nb, bits_out, n_words,
+            parted, tot, base, plan.shift, plan.nb, src_cap, bits_out, n_words,
             (key_range & 31) ? (1u << (key_range & 31)) - 1u : 0xffffffffu, ctrl);
         if (timer) timer->after("bucket_bitset", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
-        if (launches) *launches = 4;
+        if (launches) *launches = nlaunch + 1;
         return cudaSuccess;
     }
     if (timer) timer->before(stream);
@@ -1213,12 +1339,16 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (err != cudaSuccess) return err;
     } else {
         const size_t smem = bucket_sort_smem_bytes(plan.shift);
-        bucket_sort_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-            parted, tot, base, plan.shift, plan.nb, out, ctrl);
+        if (plan.shift >= MAX_BUCKET_SHIFT)
+            bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
+                parted, tot, base, plan.shift, plan.nb, src_cap, out, ctrl);
+        else  // narrower buckets: a smaller stage lets two CTAs share an SM
+            bucket_sort_kernel<BUCKET_STAGE_SMALL><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
+                parted, tot, base, plan.shift, plan.nb, src_cap, out, ctrl);
     }
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
-    if (launches) *launches = 4;
+    if (launches) *launches = nlaunch + 1;
     return cudaSuccess;
 }
 
@@ -1226,9 +1356,13 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     int sms = 0;
     cudaError_t err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (err != cudaSuccess) return err;
-    auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS>;
-    auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB>;
+    auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>;
+    auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>;
     err = cudaFuncSetAttribute(wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_xwide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1240,8 +1374,11 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_bitset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                1 << (MAX_BUCKET_SHIFT - 3));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bucket_sort_smem_bytes(20)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(bucket_sort_smem_bytes(19)));
     if (err != cudaSuccess) return err;
     int per = 0;
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wide, PART_THREADS,
@@ -1253,8 +1390,11 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     if (err != cudaSuccess) return err;
     geo->part_blocks_narrow = sms * (per > 0 ? per : 1);
     for (int shift = MIN_BUCKET_SHIFT; shift <= MAX_BUCKET_SHIFT; ++shift) {
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel, BUCKET_THREADS,
-                                                            bucket_sort_smem_bytes(shift));
+        err = shift >= MAX_BUCKET_SHIFT
+                  ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel<BUCKET_STAGE>,
+                                                                  BUCKET_THREADS, bucket_sort_smem_bytes(shift))
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel<BUCKET_STAGE_SMALL>,
+                                                                  BUCKET_THREADS, bucket_sort_smem_bytes(shift));
         if (err != cudaSuccess) return err;
         geo->bucket_blocks[shift] = sms * (per > 0 ? per : 1);
     }

@@ -233,14 +233,27 @@ struct DeviceCtx {
         keys_cap = cap;
     }
 
-    void ensure_parted(size_t n) {
-        if (n <= parted_cap) return;
+    // Bucket buffer for n keys under `plan`: the slab layout's slots when it
+    // applies (bws_gpu::slab_slots), else n. Returns the usable capacity.
+    size_t ensure_parted(size_t n, const bws_gpu::BucketPlan& plan) {
+        const size_t need = static_cast<size_t>(bws_gpu::slab_slots(plan, n)) > n
+                                ? static_cast<size_t>(bws_gpu::slab_slots(plan, n))
+                                : n;
+        if (need <= parted_cap) return parted_cap;
         if (parted) cuda_check(cudaFree(parted), "cudaFree(parted)");
         parted = nullptr;
         parted_cap = 0;
-        const size_t cap = n + n / 8 + 64;  // KB4 bulk copies may read up to 12 bytes past n
-        cuda_check(cudaMalloc(&parted, cap * sizeof(uint32_t)), "cudaMalloc(bucket keys)");
-        parted_cap = cap;
+        const size_t cap = need + n / 8 + 64;  // KB4 bulk copies may read up to 12 bytes past a bucket
+        if (cudaMalloc(&parted, cap * sizeof(uint32_t)) != cudaSuccess) {
+            // the slab is an optimisation: fall back to the packed layout's n slots
+            cudaGetLastError();
+            const size_t packed = n + n / 8 + 64;
+            cuda_check(cudaMalloc(&parted, packed * sizeof(uint32_t)), "cudaMalloc(bucket keys)");
+            parted_cap = packed - 64;
+            return parted_cap;
+        }
+        parted_cap = cap - 64;
+        return parted_cap;
     }
 
     void ensure_bounce() {
@@ -465,12 +478,12 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
         cuda_check(cudaStreamSynchronize(stream), "key_max execution");
         key_range = static_cast<uint64_t>(mx) + 1;
     }
-    ctx.ensure_parted(count);
     const bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range);
+    const size_t parted_cap = ctx.ensure_parted(count, plan);
     int launches = 0;
     cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
                                            ctx.ctrl(), plan, ctx.geo, stream, &launches,
-                                           active_timer()),
+                                           active_timer(), nullptr, 0, parted_cap),
                "bucketed sort launch");
     g_launches.fetch_add(static_cast<uint64_t>(launches));
     cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
@@ -730,17 +743,17 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
                               (path == BWS_PATH_BUCKETED || (path == BWS_PATH_AUTO && count >= kBucketedMinKeys));
         if (bucketed) {
             // KB1-KB3 + KB4b: SMEM-staged, coalesced, no atomics to global, no memset
-            ctx.ensure_parted(count);
             bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range);
             plan.cluster = 1;
             if (plan.shift > bws_gpu::MAX_BUCKET_SHIFT) {
                 plan.shift = bws_gpu::MAX_BUCKET_SHIFT;
                 plan.nb = static_cast<int>((key_range + (1ull << plan.shift) - 1) >> plan.shift);
             }
+            const size_t parted_cap = ctx.ensure_parted(count, plan);
             int launches = 0;
             cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, nullptr, ctx.parted,
                                                    ctx.bucket_scratch, ctx.ctrl(), plan, ctx.geo, s,
-                                                   &launches, active_timer(), bits, words),
+                                                   &launches, active_timer(), bits, words, parted_cap),
                        "bucketed bitset build launch");
             g_launches.fetch_add(static_cast<uint64_t>(launches));
         } else {

@@ -15,8 +15,8 @@ namespace bws_gpu {
 struct alignas(64) Ctrl {
     unsigned int max_key;          // atomicMax over every in-range key (K2)
     unsigned int bad_keys;         // keys >= key_range (K2); never scattered
-    unsigned int ticket;           // K3 dynamic tile ticket
-    unsigned int pad0;
+    unsigned int ticket;           // K3 dynamic tile ticket / KB4 bucket ticket
+    unsigned int done_ctas;        // slab KB3: CTAs finished (the last one scans the counts)
     unsigned long long total;      // set bits over the whole scan (K3, last tile)
     unsigned long long pad1[5];
 };
@@ -61,7 +61,8 @@ constexpr int PART_TILE = PART_THREADS * PART_KPT;  // 16384 keys per wide tile
 constexpr int PART_NARROW_THREADS = 512;
 constexpr int PART_NARROW_MAXB = 1024;
 constexpr int BUCKET_THREADS = 1024;
-constexpr int BUCKET_STAGE = 512;  // keys per warp in the extraction stage
+constexpr int BUCKET_STAGE = 512;        // keys per warp in the extraction stage (2^20 buckets)
+constexpr int BUCKET_STAGE_SMALL = 256;  // narrower buckets: fits two CTAs per SM
 constexpr int MAX_CLUSTER = 8;          // CTAs per bucket in the cluster KB4 (portable limit)
 constexpr int CLUSTER_SUB_SHIFT = 20;   // each cluster CTA owns a 2^20-key sub-range
 constexpr int CLUSTER_CHUNK = 4096;     // keys per multicast chunk (16 KB), two buffers
@@ -71,8 +72,9 @@ constexpr std::size_t part_smem_bytes(int threads, int maxb) {
     return 2 * std::size_t(threads) * PART_KPT * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
 }
 constexpr std::size_t bucket_sort_smem_bytes(int shift) {
+    const int stage = shift >= MAX_BUCKET_SHIFT ? BUCKET_STAGE : BUCKET_STAGE_SMALL;
     return (std::size_t(1) << (shift - 3)) + (std::size_t(1) << (shift - 8)) +  // bitset + summary
-           (BUCKET_THREADS / 32) * (BUCKET_STAGE + BUCKET_STAGE / 32) * 4;
+           (BUCKET_THREADS / 32) * (stage + stage / 32) * 4;
 }
 
 constexpr std::size_t cluster_sort_smem_bytes() {
@@ -106,6 +108,23 @@ struct BucketPlan {
     int shift = 20;   // bucket = key >> shift
     int nb = 1;       // number of buckets, <= MAX_BUCKETS
     int cluster = 1;  // CTAs per bucket in KB4 (bucket range = cluster * 2^20 when > 1)
+};
+
+// Slab layout of the bucket buffer (KB3 without KB1/KB2): bucket b owns the
+// fixed slots [b * cap, (b + 1) * cap), cap = min(2^shift, n) rounded up to 4,
+// which no set of DISTINCT keys can overflow; per-bucket fill counters replace
+// the histogram pass. A spare tile of slots after the last bucket absorbs the
+// runs of a bucket that duplicates overflowed (that bucket then sorts nothing,
+// so the sort reports the duplicates).
+struct SlabArgs {
+    std::uint32_t* gcnt = nullptr;         // nb zeroed fill counters
+    std::uint32_t cap = 0;                 // slots per bucket
+    std::uint32_t dump = 0;                // first slot of the overflow tile
+    std::uint32_t limit = 0;               // keys >= limit are counted as bad (check != 0)
+    int check = 0;
+    Ctrl* ctrl = nullptr;
+    std::uint32_t* tot = nullptr;          // out: keys per bucket
+    unsigned long long* g_base = nullptr;  // out: output offset per bucket (+ total at [nb])
 };
 
 // Optional per-kernel timing hook (bench.py's live roofline): before() and
@@ -152,18 +171,24 @@ cudaError_t launch_scan2(std::uint32_t* bits, std::uint64_t n_words, std::uint32
 // Bucketed pipeline (bucket.cu). plan_buckets picks the bucket width for a
 // key range; bucket_scratch_bytes sizes the histogram/offset scratch.
 BucketPlan plan_buckets(std::uint64_t key_range);
+// Bucket-buffer slots the slab layout needs for n keys (0: use the packed
+// histogram layout: the slab would exceed 4n slots or 2^32).
+std::uint64_t slab_slots(const BucketPlan& plan, std::size_t n);
 std::size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks);
 cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo);
-// With bits_out set, KB4b writes the bitset (n_words words) instead of sorted
-// keys (multi-GPU per-rank build; no clearing of bits_out needed).
 // KB1..KB4: sorts n keys (all < key_range) into out via the `parted` buffer
-// (n keys). Adds the number of distinct keys to ctrl->total, counts keys >=
-// key_range in ctrl->bad_keys. `launches` receives the kernel count.
+// of parted_cap slots (>= n; the slab layout is used when parted_cap >=
+// slab_slots(plan, n) > 0, and then KB1/KB2 are skipped). Adds the number of
+// distinct keys to ctrl->total, counts keys >= key_range in ctrl->bad_keys.
+// `launches` receives the kernel count. With bits_out set, KB4b writes the
+// bitset (n_words words) instead of sorted keys (multi-GPU per-rank build; no
+// clearing of bits_out needed).
 cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::uint64_t key_range,
                                std::uint32_t* out, std::uint32_t* parted, void* scratch, Ctrl* ctrl,
                                const BucketPlan& plan, const LaunchGeometry& geo,
                                cudaStream_t stream, int* launches, KernelTimer* timer = nullptr,
-                               std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0);
+                               std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0,
+                               std::uint64_t parted_cap = 0);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream);

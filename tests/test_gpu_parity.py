@@ -213,6 +213,93 @@ def test_duplicates_rejected_at_scale(capi, path):
     assert np.array_equal(a, keys)
 
 
+# --- slab layout of the bucket buffer (KB3 fill counters, no KB1/KB2) -------
+# Used when n >= key_range / 4 (kernels.h SlabArgs): n = 2^22 keys below 2^24
+# gives 256 buckets of 2^16 slots.
+
+SLAB_N = 1 << 22
+SLAB_RANGE = 1 << 24
+
+
+@pytest.mark.parametrize("extra", [0, 3])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_slab_layout_vs_oracle(capi, cuda, extra, offset):
+    capi.set_path(capi.Path.BUCKETED)
+    n = SLAB_N + extra
+    keys = np.random.default_rng(21 + extra).choice(SLAB_RANGE, size=n, replace=False).astype(np.uint32)
+    expected = np.sort(keys)
+    assert np.array_equal(gpu_sort_device(capi, cuda, keys, offset), expected)
+    a = keys.copy()
+    capi.sort_u32_range(a, SLAB_RANGE)
+    assert np.array_equal(a, expected)
+    # a non-power-of-two range: the last bucket is partial; a key at the limit is bad
+    b = keys.copy()
+    capi.sort_u32_range(b, int(keys.max()) + 1)
+    assert np.array_equal(b, expected)
+    c = keys.copy()
+    with pytest.raises(capi.BitsortError) as e:
+        capi.sort_u32_range(c, int(keys.max()))
+    assert e.value.status == capi.Status.ERROR_DATA
+    assert np.array_equal(c, keys)
+
+
+def test_slab_layout_full_bucket(capi):
+    """A bucket that holds every key of its range (2^16 slots exactly full)."""
+    capi.set_path(capi.Path.BUCKETED)
+    rng = np.random.default_rng(8)
+    full = np.arange(5 << 16, 6 << 16, dtype=np.uint32)
+    rest = rng.choice(np.setdiff1d(np.arange(SLAB_RANGE, dtype=np.uint32), full),
+                      size=SLAB_N - full.size, replace=False).astype(np.uint32)
+    keys = np.concatenate([full, rest])
+    rng.shuffle(keys)
+    a = keys.copy()
+    capi.sort_u32_range(a, SLAB_RANGE)
+    assert np.array_equal(a, np.sort(keys))
+
+
+@pytest.mark.parametrize("kind", ["pair", "overflow"])
+def test_slab_layout_duplicates(capi, kind):
+    """Duplicates are rejected in the slab layout too, including ones that
+    overflow a bucket's fixed slots (then that bucket sorts nothing)."""
+    capi.set_path(capi.Path.BUCKETED)
+    keys = np.random.default_rng(4).choice(SLAB_RANGE, size=SLAB_N, replace=False).astype(np.uint32)
+    if kind == "pair":
+        keys[5] = keys[SLAB_N - 9]
+    else:  # 2^17 copies of 40 keys of bucket 7: far past its 2^16 slots
+        keys[: 1 << 17] = (7 << 16) + (np.arange(1 << 17, dtype=np.uint32) % 40)
+    for _ in range(2):  # and the next sort is unaffected
+        a = keys.copy()
+        assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.ERROR_DATA
+        assert "distinct" in capi.last_error()
+        assert np.array_equal(a, keys)
+    good = np.random.default_rng(5).choice(SLAB_RANGE, size=SLAB_N, replace=False).astype(np.uint32)
+    a = good.copy()
+    capi.sort_u32_range(a, SLAB_RANGE)
+    assert np.array_equal(a, np.sort(good))
+
+
+@pytest.mark.parametrize("kind", ["distinct", "overflow"])
+def test_slab_layout_bitset_build(capi, cuda, kind):
+    """The per-rank bitset build (KB4b) over the slab layout: exact bitset for
+    distinct keys; fewer set bits than keys when duplicates overflow a bucket
+    (how dist.py detects them)."""
+    capi.set_path(capi.Path.BUCKETED)
+    keys = np.random.default_rng(6).choice(SLAB_RANGE, size=SLAB_N, replace=False).astype(np.uint32)
+    if kind == "overflow":
+        keys[: 1 << 17] = (3 << 16) + (np.arange(1 << 17, dtype=np.uint32) % 5)
+    src = cuda.from_numpy(keys.view(np.int32)).cuda()
+    bits = cuda.full((SLAB_RANGE // 32,), -1, dtype=cuda.int32, device="cuda")
+    capi.bitset_build(src.data_ptr(), SLAB_N, bits.data_ptr(), SLAB_RANGE)
+    cuda.cuda.synchronize()
+    got = np.unpackbits(bits.cpu().numpy().view(np.uint8), bitorder="little")
+    if kind == "distinct":
+        want = np.zeros(SLAB_RANGE, dtype=np.uint8)
+        want[keys] = 1
+        assert np.array_equal(got, want)
+    else:
+        assert int(got.sum()) < SLAB_N
+
+
 # --- device-resident async API and the multi-rank building blocks ----------
 
 @pytest.mark.parametrize("path", PATHS)

@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 20 --no-cpu-baseline > gpurun_out/bench_c2_e2e.json 2> gpurun_out/bench_c2_e2e.err
+timeout 600 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+for c in C2 C3; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_slab_$c.json 2>&1; done
+BITSORT_SLAB=0 timeout 300 python bench.py --config C2 --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_noslab_C2.json 2>&1
