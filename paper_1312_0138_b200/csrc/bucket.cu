@@ -216,6 +216,38 @@ __global__ void bucket_colscan_kernel(uint32_t* __restrict__ H, int P, int nb,
     if (lane == 31) tot[b] = incl;
 }
 
+// Slab epilogue shared by the slab KB3 variants: folds the CTA's bad-key
+// count into ctrl, and the last CTA to finish turns the fill counters into
+// bucket totals (0 for an overflowed bucket: its keys are lost, so the sort
+// sees fewer set bits than keys) and output offsets for KB4. `s_vals` holds
+// nb uint32, `s_out64` nb uint64 (both SMEM).
+__device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t bad, uint32_t* s_vals,
+                                            unsigned long long* s_out64, unsigned long long* s_scratch,
+                                            uint32_t* s_last) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t wb = __reduce_add_sync(kFull, bad);
+    if (lane == 0 && wb) atomicAdd(&sa.ctrl->bad_keys, wb);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *s_last = atomicAdd(&sa.ctrl->done_ctas, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const uint32_t v = __ldcg(sa.gcnt + b);
+        s_vals[b] = v <= sa.cap ? v : 0u;
+    }
+    __syncthreads();
+    const unsigned long long total = block_exclusive_scan_u64(s_vals, nb, s_out64, s_scratch);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        sa.g_base[b] = s_out64[b];
+        sa.tot[b] = s_vals[b];
+    }
+    if (threadIdx.x == 0) sa.g_base[nb] = total;
+}
+
 // KB3: partition, one persistent CTA per SM. CTA c streams its share in
 // 16384-key tiles through a double-buffered SMEM ring filled by TMA bulk copies
 // (the next tile lands while the current one is processed). Per tile: ranks
@@ -440,32 +472,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
         }
     }
-    if constexpr (SLAB) {
-        const uint32_t wb = __reduce_add_sync(kFull, bad);
-        if (lane == 0 && wb) atomicAdd(&sa.ctrl->bad_keys, wb);
-        // last CTA out: bucket totals (0 for an overflowed bucket: its keys are
-        // lost, so the sort sees fewer set bits than keys) and output offsets
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            s_last = atomicAdd(&sa.ctrl->done_ctas, 1u) == P - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-                const uint32_t v = __ldcg(sa.gcnt + b);
-                s_cur[b] = v <= sa.cap ? v : 0u;
-            }
-            __syncthreads();
-            const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
-            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-                sa.g_base[b] = s_base64[b];
-                sa.tot[b] = s_cur[b];
-            }
-            if (threadIdx.x == 0) sa.g_base[nb] = total;
-        }
-    }
+    if constexpr (SLAB) slab_finish(sa, nb, bad, s_cur, s_base64, s_scratch, &s_last);
 }
 
 
@@ -1225,7 +1232,7 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
         const char* e = std::getenv("BITSORT_SLAB");
         return e && std::string(e) == "0";
     }();
-    if (off || plan.cluster > 1 || narrow_partition(plan) ||
+    if (off || plan.cluster > 1 ||
         (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE")))
         return 0;
     uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
@@ -1284,9 +1291,14 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         err = cudaMemsetAsync(H, 0, static_cast<size_t>(plan.nb) * sizeof(uint32_t), stream);
         if (err != cudaSuccess) return err;
         if (timer) timer->before(stream);
-        bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
-            <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
-                ks, plan.shift, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+        if (narrow_partition(plan))
+            bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>
+                <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
+                    ks, plan.shift, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+        else
+            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
+                    ks, plan.shift, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         if (timer) timer->after("bucket_partition", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         nlaunch = 1;
@@ -1364,6 +1376,10 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_xwide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
