@@ -238,6 +238,7 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         const uint32_t v = __ldcg(sa.gcnt + b);
         s_vals[b] = v <= sa.cap ? v : 0u;
+        sa.gcnt[b] = 0u;  // the counters start the next sort at zero
     }
     __syncthreads();
     const unsigned long long total = block_exclusive_scan_u64(s_vals, nb, s_out64, s_scratch);
@@ -1244,9 +1245,10 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
 }
 
 size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
-    return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H (slab: fill counters)
-           + MAX_BUCKETS * sizeof(uint32_t)                                // tot
-           + (MAX_BUCKETS + 1) * sizeof(unsigned long long);               // base
+    return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H
+           + (MAX_BUCKETS + 1) * sizeof(uint32_t)                          // tot
+           + (MAX_BUCKETS + 2) * sizeof(unsigned long long)                // base (8-aligned)
+           + MAX_BUCKETS * sizeof(uint32_t);                               // slab fill counters
 }
 
 cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* out,
@@ -1256,7 +1258,9 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                                uint64_t parted_cap) {
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
-    uint32_t* H = static_cast<uint32_t*>(scratch);
+    // scratch: slab fill counters (fixed place: they persist across sorts), then H, tot, base
+    uint32_t* gcnt = static_cast<uint32_t*>(scratch);
+    uint32_t* H = gcnt + MAX_BUCKETS;
     uint32_t* tot = H + static_cast<size_t>(P) * plan.nb;
     unsigned long long* base =
         reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(tot + MAX_BUCKETS + 1) & ~uintptr_t(7));
@@ -1279,8 +1283,9 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     int nlaunch = 0;
     cudaError_t err;
     if (use_slab) {
-        // KB3 (slab) claims slots with fill counters: no KB1/KB2
-        sa.gcnt = H;
+        // KB3 (slab) claims slots with fill counters: no KB1/KB2. The counters
+        // are zeroed once at allocation and re-zeroed by the last KB3 CTA.
+        sa.gcnt = gcnt;
         sa.cap = static_cast<uint32_t>((slab - PART_TILE) / plan.nb);
         sa.dump = static_cast<uint32_t>(slab - PART_TILE);
         sa.limit = limit;
@@ -1288,8 +1293,6 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.ctrl = ctrl;
         sa.tot = tot;
         sa.g_base = base;
-        err = cudaMemsetAsync(H, 0, static_cast<size_t>(plan.nb) * sizeof(uint32_t), stream);
-        if (err != cudaSuccess) return err;
         if (timer) timer->before(stream);
         if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>

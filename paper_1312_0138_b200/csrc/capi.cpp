@@ -217,8 +217,10 @@ struct DeviceCtx {
         bws_gpu::BucketPlan widest;
         widest.nb = bws_gpu::MAX_BUCKETS;
         const int max_shares = geo.part_blocks > geo.part_blocks_narrow ? geo.part_blocks : geo.part_blocks_narrow;
-        cuda_check(cudaMalloc(&bucket_scratch, bws_gpu::bucket_scratch_bytes(widest, max_shares) + 64),
-                   "cudaMalloc(bucket scratch)");
+        const size_t scratch_bytes = bws_gpu::bucket_scratch_bytes(widest, max_shares) + 64;
+        cuda_check(cudaMalloc(&bucket_scratch, scratch_bytes), "cudaMalloc(bucket scratch)");
+        // the slab fill counters must start at zero (KB3 re-zeroes them after each sort)
+        cuda_check(cudaMemset(bucket_scratch, 0, scratch_bytes), "bucket scratch clear");
         bits_dirty = true;
         ready = true;
     }

@@ -1,2 +1,2 @@
-for v in "" "BITSORT_KB4_BALLOT=64" "BITSORT_KB4_BALLOT=160"; do for c in C2 C5; do env $v timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${c}_$v.json 2>&1; done; done
-BITSORT_KB4_BALLOT=64 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "BUCKETED or slab" > gpurun_out/pytest_ballot.log 2>&1; echo exit=$? >> gpurun_out/pytest_ballot.log
+timeout 600 python -m pytest tests -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+for c in C2 C3; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${c}.json 2>&1; done
