@@ -88,17 +88,20 @@ __device__ unsigned long long block_exclusive_scan_u64(const uint32_t* vals, int
 // Slot of a key in KB1/KB3: its bucket, clamped to the spill slot `nb` for
 // keys beyond the last bucket; padding lanes (`in` false) also spill. KB1 and
 // KB3 apply the same rule, so slot counts always match. A key in
-// [key_range, nb << shift) (non-power-of-two ranges) lands in the last bucket;
+// [key_range, nb * width) (ranges that are not a multiple of the width) lands in the last bucket;
 // KB1 counts it in ctrl->bad_keys exactly, and the host then rejects the sort.
-__device__ __forceinline__ uint32_t bucket_or_spill(uint32_t k, bool in, int shift, int nb) {
-    return in ? min(k >> shift, static_cast<uint32_t>(nb)) : static_cast<uint32_t>(nb);
+__device__ __forceinline__ uint32_t bucket_id(uint32_t k, const BucketMap& m) {
+    return __umulhi((k >> m.ms) << 12, m.mq);
+}
+__device__ __forceinline__ uint32_t bucket_or_spill(uint32_t k, bool in, const BucketMap& m, int nb) {
+    return in ? min(bucket_id(k, m), static_cast<uint32_t>(nb)) : static_cast<uint32_t>(nb);
 }
 
 // KB1: histogram of bucket ids over partition CTA c's share, computed by
 // HIST_SPLIT CTAs per share (more loads in flight) that add into the zeroed,
 // bucket-major H[b * P + c] (KB2 scans contiguous rows).
 __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
-    bucket_hist_kernel(KeySplit ks, int shift, int nb, uint32_t limit, int check,
+    bucket_hist_kernel(KeySplit ks, BucketMap bm, int nb, uint32_t limit, int check,
                        uint32_t* __restrict__ H, Ctrl* __restrict__ ctrl) {
     __shared__ uint32_t s_h[MAX_BUCKETS + 1];
     for (int b = threadIdx.x; b <= nb; b += blockDim.x) s_h[b] = 0;
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
             all_in &= in[u];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                bk[u * 4 + q] = bucket_or_spill(kk[q], in[u], shift, nb);
+                bk[u * 4 + q] = bucket_or_spill(kk[q], in[u], bm, nb);
                 kmin = min(kmin, in[u] ? kk[q] : 0xffffffffu);
                 kmax = max(kmax, in[u] ? kk[q] : 0u);
                 bad += (check && in[u] && kk[q] >= limit) ? 1u : 0u;
@@ -149,8 +152,8 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
         mx = max(mx, kmax);
         const uint32_t wlo = __reduce_min_sync(kFull, kmin);
         const uint32_t whi = __reduce_max_sync(kFull, kmax);
-        const uint32_t blo = bucket_or_spill(wlo, true, shift, nb);
-        if (blo == bucket_or_spill(whi, true, shift, nb) && __all_sync(kFull, all_in)) {
+        const uint32_t blo = bucket_or_spill(wlo, true, bm, nb);
+        if (blo == bucket_or_spill(whi, true, bm, nb) && __all_sync(kFull, all_in)) {
             // sorted / clustered input: one bucket for the whole warp step
             if (lane == 0) atomicAdd(s_h + blo, 32u * U * 4);
         } else {
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
         int ne = c == 0 ? ks.n_head : 0;
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
-                atomicAdd(s_h + bucket_or_spill(extra[i], true, shift, nb), 1u);
+                atomicAdd(s_h + bucket_or_spill(extra[i], true, bm, nb), 1u);
                 mx = max(mx, extra[i]);
                 bad += (check && extra[i] >= limit) ? 1u : 0u;
             }
@@ -267,7 +270,7 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
 // into bucket totals and output offsets for KB4.
 template <int THREADS, int KPT, int MAXB, bool SLAB>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
-    bucket_partition_kernel(KeySplit ks, int shift, int nb,
+    bucket_partition_kernel(KeySplit ks, BucketMap bm, int nb,
                             const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
                             uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base,
                             SlabArgs sa) {
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         int ne = c == 0 ? ks.n_head : 0;
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
-                const uint32_t b = bucket_or_spill(extra[i], true, shift, nb);
+                const uint32_t b = bucket_or_spill(extra[i], true, bm, nb);
                 if constexpr (SLAB) {
                     bad += (sa.check && extra[i] >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
@@ -374,14 +377,14 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 k[4 * j + q] = kk[q];
-                rb[4 * j + q] = bucket_or_spill(kk[q], in, shift, nb);
+                rb[4 * j + q] = bucket_or_spill(kk[q], in, bm, nb);
                 kmin = min(kmin, kk[q]);
                 kmax = max(kmax, kk[q]);
                 if constexpr (SLAB) bad += (sa.check && in && kk[q] >= sa.limit) ? 1u : 0u;
             }
         }
-        const uint32_t blo = bucket_or_spill(__reduce_min_sync(kFull, kmin), true, shift, nb);
-        const uint32_t bhi = bucket_or_spill(__reduce_max_sync(kFull, kmax), true, shift, nb);
+        const uint32_t blo = bucket_or_spill(__reduce_min_sync(kFull, kmin), true, bm, nb);
+        const uint32_t bhi = bucket_or_spill(__reduce_max_sync(kFull, kmax), true, bm, nb);
         if (blo == bhi && __all_sync(kFull, all_in)) {
             // the whole warp step lies in one bucket: one atomic, ranks by lane
             uint32_t base = 0;
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 #pragma unroll 4
         for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
             const uint32_t key = buf[i];
-            parted[s_delta[key >> shift] + i] = key;
+            parted[s_delta[bucket_id(key, bm)] + i] = key;
         }
         __syncthreads();  // D: buf free again
         if (threadIdx.x == 0 && t + 2 < ntiles) {
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 // keys of a thread stay in registers; ranks come from a counting pass
 // (SMEM atomics without return) and a fill pass (atomics with return).
 __global__ void __launch_bounds__(PART_THREADS, 1)
-    bucket_partition_xwide_kernel(KeySplit ks, int shift, int nb,
+    bucket_partition_xwide_kernel(KeySplit ks, BucketMap bm, int nb,
                                   const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
                                   uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         int ne = c == 0 ? ks.n_head : 0;
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
-                const uint32_t b = bucket_or_spill(extra[i], true, shift, nb);
+                const uint32_t b = bucket_or_spill(extra[i], true, bm, nb);
                 if (b != spill) parted[s_cur[b]++] = extra[i];
             }
             extra = c == P - 1 ? ks.tail : nullptr;
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         for (int j = 0; j < KPT / 4; ++j) {
             const bool in = j * PART_THREADS + threadIdx.x < nvec;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) atomicAdd(s_cnt + bucket_or_spill(k[4 * j + q], in, shift, nb), 1u);
+            for (int q = 0; q < 4; ++q) atomicAdd(s_cnt + bucket_or_spill(k[4 * j + q], in, bm, nb), 1u);
         }
         __syncthreads();  // counts complete; every thread holds its keys
         {
@@ -615,7 +618,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             const bool in = j * PART_THREADS + threadIdx.x < nvec;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const uint32_t b = bucket_or_spill(k[4 * j + q], in, shift, nb);
+                const uint32_t b = bucket_or_spill(k[4 * j + q], in, bm, nb);
                 s_buf[atomicAdd(s_cnt + b, 1u)] = k[4 * j + q];
             }
         }
@@ -624,7 +627,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
 #pragma unroll 4
         for (uint32_t i = threadIdx.x; i < tile_valid; i += PART_THREADS) {
             const uint32_t key = s_buf[i];
-            parted[s_delta[key >> shift] + i] = key;
+            parted[s_delta[bucket_id(key, bm)] + i] = key;
         }
         for (int q = 0; q < per; ++q)
             if (sb + q < slots) s_cnt[sb + q] = 0;
@@ -638,10 +641,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
 // with 4 per thread in flight, tail.
 template <bool SPARSE>
 __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__ src, uint32_t cnt,
-                                                    uint32_t lowmask, uint32_t* s_bits,
+                                                    uint32_t key_lo, uint32_t* s_bits,
                                                     uint32_t* s_sum) {
     auto set_key = [&](uint32_t key) {
-        const uint32_t x = key & lowmask;
+        const uint32_t x = key - key_lo;  // < width: the key's bucket is this one
         const uint32_t w = x >> 5;
         atomicOr(s_bits + w, 1u << (x & 31));
         if (SPARSE) atomicOr(s_sum + (w >> 5), 1u << (w & 31));
@@ -691,10 +694,10 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
 template <int STAGE>
 __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
-                       const unsigned long long* __restrict__ g_base, int shift, int nb,
+                       const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const uint32_t W = 1u << (shift - 5);  // words per bucket bitset (>= 1024)
+    const uint32_t W = bm.width >> 5;  // words per bucket bitset (>= 1024; 2^k or a multiple of 4096)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* s_sum = s_bits + W;             // bit w set <=> word w touched (sparse buckets)
     uint32_t* s_stage_all = s_sum + W / 32;   // BUCKET_THREADS/32 x stage pitch
@@ -706,7 +709,6 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     constexpr int kStagePitch = STAGE + STAGE / 32;
     uint32_t* s_stage = s_stage_all + warp * kStagePitch;
     const uint32_t seg_words = W / (BUCKET_THREADS / 32);
-    const uint32_t lowmask = (1u << shift) - 1;
     const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
 
     for (uint32_t i = threadIdx.x; i < W / 32; i += BUCKET_THREADS) s_sum[i] = 0u;
@@ -725,9 +727,9 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         if (sparse)
-            scatter_bucket_keys<true>(src, cnt, lowmask, s_bits, s_sum);
+            scatter_bucket_keys<true>(src, cnt, static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
         else
-            scatter_bucket_keys<false>(src, cnt, lowmask, s_bits, s_sum);
+            scatter_bucket_keys<false>(src, cnt, static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
         __syncthreads();
         // phase 1: per-warp popcount of its segment (128-bit SMEM reads; sparse
         // buckets read only the touched words, found through the summary)
@@ -755,7 +757,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         }
         __syncthreads();
         uint32_t* o = out + base + s_warp[warp];
-        const uint32_t key_hi = static_cast<uint32_t>(b) << shift;
+        const uint32_t key_hi = static_cast<uint32_t>(b) * bm.width;
         if (sparse) {
             // lane-major over summary words: lane owns 32 consecutive bitset
             // words (one summary word) per round; its keys are contiguous in
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
             }
         } else if (seg_words % 512 == 0) {
             extract_span512<STAGE>(s_bits, seg, seg_words, key_hi, o, s_stage, lane, false, nullptr);
-        } else if (seg_words >= 128) {
+        } else if (seg_words % 128 == 0) {
             // 128-word steps, lane-major (lane owns 4 words); a step with
             // <= BUCKET_STAGE keys is extracted in one pass, denser steps fall
             // back to four 32-word sub-steps (word per lane)
@@ -1078,14 +1080,13 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
 // bitset needs no clearing.
 __global__ void __launch_bounds__(BUCKET_THREADS, 1)
     bucket_bitset_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
-                         const unsigned long long* __restrict__ g_base, int shift, int nb,
+                         const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                          uint32_t src_cap, uint32_t* __restrict__ bits, unsigned long long n_words,
                          uint32_t last_mask, Ctrl* __restrict__ ctrl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const uint32_t W = 1u << (shift - 5);
+    const uint32_t W = bm.width >> 5;
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
     __shared__ unsigned s_b;
-    const uint32_t lowmask = (1u << shift) - 1;
     uint4* s4 = reinterpret_cast<uint4*>(s_bits);
     for (;;) {
         if (threadIdx.x == 0) s_b = atomicAdd(&ctrl->ticket, 1u);
@@ -1094,7 +1095,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
         const unsigned b = s_b;
         if (b >= static_cast<unsigned>(nb)) break;
         scatter_bucket_keys<false>(parted + (src_cap ? static_cast<size_t>(b) * src_cap : g_base[b]), tot[b],
-                                   lowmask, s_bits, nullptr);
+                                   static_cast<uint32_t>(b) * bm.width, s_bits, nullptr);
         __syncthreads();
         const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
         // keys in [key_range, 32 * n_words) of a non-multiple-of-32 range never appear
@@ -1194,7 +1195,15 @@ cudaError_t launch_key_max(const uint32_t* keys, size_t n, Ctrl* ctrl, const Lau
     return cudaGetLastError();
 }
 
-BucketPlan plan_buckets(uint64_t key_range) {
+static BucketMap pow2_map(int shift) {
+    BucketMap m;
+    m.ms = shift;
+    m.mq = 1u << 20;
+    m.width = 1u << shift;
+    return m;
+}
+
+BucketPlan plan_buckets(uint64_t key_range, int kb4_ctas, bool allow_cluster) {
     BucketPlan p;
     int log2m = 0;
     while ((1ull << log2m) < key_range) ++log2m;
@@ -1208,23 +1217,48 @@ BucketPlan plan_buckets(uint64_t key_range) {
     // of a cluster must hold every in-flight multicast chunk, so a cluster streams
     // at one SM's share of HBM bandwidth while occupying R SMs. BITSORT_CLUSTER=1
     // enables it for experiments.
-    if (shift > MAX_BUCKET_SHIFT && std::getenv("BITSORT_CLUSTER")) {
+    if (allow_cluster && shift > MAX_BUCKET_SHIFT && std::getenv("BITSORT_CLUSTER")) {
         int r = shift - MAX_BUCKET_SHIFT;
         if ((1 << r) > MAX_CLUSTER) r = 0;
         while ((1 << (r + 1)) <= MAX_CLUSTER && r < shift - MAX_BUCKET_SHIFT) ++r;
         p.cluster = 1 << r;
         const uint64_t nbc = (key_range + (1ull << (MAX_BUCKET_SHIFT + r)) - 1) >> (MAX_BUCKET_SHIFT + r);
         p.shift = MAX_BUCKET_SHIFT + r;
+        p.map = pow2_map(p.shift);
         p.nb = static_cast<int>(nbc);
         return p;
     }
-    if (const char* env = std::getenv("BITSORT_BUCKET_SHIFT")) shift = std::atoi(env);  // experiments
+    const char* env = std::getenv("BITSORT_BUCKET_SHIFT");  // experiments
+    if (env) shift = std::atoi(env);
     while (shift < MAX_BUCKET_SHIFT && ((key_range + (1ull << shift) - 1) >> shift) > MAX_BUCKETS) ++shift;
     if (shift > MAX_BUCKET_SHIFT) shift = MAX_BUCKET_SHIFT;
     if (shift < MIN_BUCKET_SHIFT) shift = MIN_BUCKET_SHIFT;
     p.shift = shift;
+    p.map = pow2_map(shift);
     const uint64_t nb = (key_range + (1ull << shift) - 1) >> shift;
     p.nb = static_cast<int>(nb < 1 ? 1 : nb);
+    // Widest buckets: KB4 runs ceil(nb / CTAs) rounds of one bucket per CTA,
+    // so 256 buckets on 148 SMs leave 40 SMs idle in the second round. Widths
+    // q * 2^17 (q = 5..7; KB4's warp segments need multiples of 2^17 keys)
+    // can fill the rounds better: C2 (2^28 keys) -> 293 buckets of 7 * 2^17,
+    // two full rounds at 7/8 of the work each. Ties keep the wider buckets
+    // (fewer KB3 runs).
+    if (shift == MAX_BUCKET_SHIFT && kb4_ctas > 0 && !env && !std::getenv("BITSORT_POW2_BUCKETS")) {
+        auto rounds = [&](uint64_t n) { return (n + kb4_ctas - 1) / kb4_ctas; };
+        uint64_t best = rounds(nb) * 8;
+        for (uint32_t q = 7; q >= 5; --q) {
+            const uint64_t w = static_cast<uint64_t>(q) << 17;
+            const uint64_t nq = (key_range + w - 1) / w;
+            if (nq > static_cast<uint64_t>(MAX_BUCKETS)) break;
+            if (rounds(nq) * q < best) {
+                best = rounds(nq) * q;
+                p.map.ms = 17;
+                p.map.mq = ((1u << 20) + q - 1) / q;
+                p.map.width = static_cast<uint32_t>(w);
+                p.nb = static_cast<int>(nq);
+            }
+        }
+    }
     return p;
 }
 
@@ -1237,10 +1271,10 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
         (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE")))
         return 0;
     uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
-    if (cap > (1ull << plan.shift)) cap = 1ull << plan.shift;
+    if (cap > plan.map.width) cap = plan.map.width;
     const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_TILE;  // + dump tile
-    // the slab trades memory (up to 4 slots per key) for the histogram pass
-    if (slots > 4 * static_cast<uint64_t>(n) + PART_TILE || slots >= (1ull << 32)) return 0;
+    // the slab trades memory (up to 4.5 slots per key) for the histogram pass
+    if (slots > 4 * static_cast<uint64_t>(n) + n / 2 + PART_TILE || slots >= (1ull << 32)) return 0;
     return slots;
 }
 
@@ -1297,11 +1331,11 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
-                    ks, plan.shift, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+                    ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         else
             bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
-                    ks, plan.shift, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+                    ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         if (timer) timer->after("bucket_partition", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         nlaunch = 1;
@@ -1309,7 +1343,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         err = cudaMemsetAsync(H, 0, static_cast<size_t>(P) * plan.nb * sizeof(uint32_t), stream);
         if (err != cudaSuccess) return err;
         if (timer) timer->before(stream);
-        bucket_hist_kernel<<<P * HIST_SPLIT, BUCKET_HIST_THREADS, 0, stream>>>(ks, plan.shift, plan.nb,
+        bucket_hist_kernel<<<P * HIST_SPLIT, BUCKET_HIST_THREADS, 0, stream>>>(ks, plan.map, plan.nb,
                                                                                limit, check, H, ctrl);
         if (timer) timer->after("bucket_hist", stream);
         err = cudaGetLastError();
@@ -1323,15 +1357,15 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         // opt-in only (BITSORT_XWIDE=1)
         if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE"))
             bucket_partition_xwide_kernel<<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
-                ks, plan.shift, plan.nb, H, tot, parted, base);
+                ks, plan.map, plan.nb, H, tot, parted, base);
         else if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
-                    ks, plan.shift, plan.nb, H, tot, parted, base, sa);
+                    ks, plan.map, plan.nb, H, tot, parted, base, sa);
         else
             bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
-                    ks, plan.shift, plan.nb, H, tot, parted, base, sa);
+                    ks, plan.map, plan.nb, H, tot, parted, base, sa);
         if (timer) timer->after("bucket_partition", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         nlaunch = 3;
@@ -1341,7 +1375,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (timer) timer->before(stream);
         bucket_bitset_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS,
                                std::size_t(1) << (plan.shift - 3), stream>>>(
-            parted, tot, base, plan.shift, plan.nb, src_cap, bits_out, n_words,
+            parted, tot, base, plan.map, plan.nb, src_cap, bits_out, n_words,
             (key_range & 31) ? (1u << (key_range & 31)) - 1u : 0xffffffffu, ctrl);
         if (timer) timer->after("bucket_bitset", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
@@ -1356,10 +1390,10 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         const size_t smem = bucket_sort_smem_bytes(plan.shift);
         if (plan.shift >= MAX_BUCKET_SHIFT)
             bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-                parted, tot, base, plan.shift, plan.nb, src_cap, out, ctrl);
+                parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
         else  // narrower buckets: a smaller stage lets two CTAs share an SM
             bucket_sort_kernel<BUCKET_STAGE_SMALL><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-                parted, tot, base, plan.shift, plan.nb, src_cap, out, ctrl);
+                parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
     }
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;

@@ -480,7 +480,8 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
         cuda_check(cudaStreamSynchronize(stream), "key_max execution");
         key_range = static_cast<uint64_t>(mx) + 1;
     }
-    const bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range);
+    const bws_gpu::BucketPlan plan =
+        bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
     const size_t parted_cap = ctx.ensure_parted(count, plan);
     int launches = 0;
     cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
@@ -745,12 +746,8 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
                               (path == BWS_PATH_BUCKETED || (path == BWS_PATH_AUTO && count >= kBucketedMinKeys));
         if (bucketed) {
             // KB1-KB3 + KB4b: SMEM-staged, coalesced, no atomics to global, no memset
-            bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range);
-            plan.cluster = 1;
-            if (plan.shift > bws_gpu::MAX_BUCKET_SHIFT) {
-                plan.shift = bws_gpu::MAX_BUCKET_SHIFT;
-                plan.nb = static_cast<int>((key_range + (1ull << plan.shift) - 1) >> plan.shift);
-            }
+            const bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(
+                key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT], /*allow_cluster=*/false);
             const size_t parted_cap = ctx.ensure_parted(count, plan);
             int launches = 0;
             cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, nullptr, ctx.parted,

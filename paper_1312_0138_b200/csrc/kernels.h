@@ -104,10 +104,21 @@ struct KeySplit {
     int n_tail = 0;
 };
 
+// Bucket of a key: floor(key / width), width = q * 2^ms with q <= 8, computed
+// as __umulhi((key >> ms) << 12, mq), mq = ceil(2^20 / q). Exact for every
+// uint32 key: the pre-shifted key is < 2^17 (ms >= 15), so the rounding error
+// of mq stays below one bucket step.
+struct BucketMap {
+    int ms = 20;
+    std::uint32_t mq = 1u << 20;
+    std::uint32_t width = 1u << 20;  // keys per bucket
+};
+
 struct BucketPlan {
-    int shift = 20;   // bucket = key >> shift
+    int shift = 20;   // SMEM bitset class of a bucket: 2^shift bits >= map.width
     int nb = 1;       // number of buckets, <= MAX_BUCKETS
     int cluster = 1;  // CTAs per bucket in KB4 (bucket range = cluster * 2^20 when > 1)
+    BucketMap map;
 };
 
 // Slab layout of the bucket buffer (KB3 without KB1/KB2): bucket b owns the
@@ -170,7 +181,9 @@ cudaError_t launch_scan2(std::uint32_t* bits, std::uint64_t n_words, std::uint32
 
 // Bucketed pipeline (bucket.cu). plan_buckets picks the bucket width for a
 // key range; bucket_scratch_bytes sizes the histogram/offset scratch.
-BucketPlan plan_buckets(std::uint64_t key_range);
+// kb4_ctas: resident KB4 CTAs (0: power-of-two widths only). With
+// allow_cluster, ranges above 2^28 may use the opt-in cluster KB4.
+BucketPlan plan_buckets(std::uint64_t key_range, int kb4_ctas, bool allow_cluster = true);
 // Bucket-buffer slots the slab layout needs for n keys (0: use the packed
 // histogram layout: the slab would exceed 4n slots or 2^32).
 std::uint64_t slab_slots(const BucketPlan& plan, std::size_t n);

@@ -278,6 +278,45 @@ def test_slab_layout_duplicates(capi, kind):
     assert np.array_equal(a, np.sort(good))
 
 
+@pytest.mark.parametrize("n_log2,range_log2", [(26, 28), (20, 29), (22, 28)])
+def test_non_power_of_two_bucket_width(capi, cuda, n_log2, range_log2):
+    """Ranges >= 2^28 may use buckets of 7 * 2^17 keys (bucket = umulhi
+    mapping; plan_buckets): slab layout (n = 2^26 below 2^28) and packed
+    layout (fewer keys), sort and per-rank bitset build, plus duplicates."""
+    capi.set_path(capi.Path.BUCKETED)
+    n, m = 1 << n_log2, 1 << range_log2
+    rng = np.random.default_rng(n_log2 * 31 + range_log2)
+    step = m // n  # one key per stride of the range, jittered: distinct by construction
+    keys = (np.arange(n, dtype=np.uint64) * step + rng.integers(0, step, size=n)).astype(np.uint32)
+    # keys on both sides of the 7 * 2^17 boundaries near the top of the range
+    w = 7 << 17
+    edges = np.array([b * w + d for b in range(m // w - 2, m // w + 1) for d in (-1, 0, 1)
+                      if 0 <= b * w + d < m], dtype=np.uint32)
+    keys = np.concatenate([keys[~np.isin(keys, edges)], edges])
+    expected = np.sort(keys)
+    rng.shuffle(keys)
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    out = cuda.empty_like(t)
+    stream = cuda.cuda.current_stream().cuda_stream
+    capi.sort_device_async(t.data_ptr(), t.numel(), out.data_ptr(), m, stream)
+    assert capi.sort_check(stream) == keys.size
+    got = out.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, expected)
+    # per-rank bitset build: bucketed (KB4b) == direct (K2 scatter)
+    bits = {}
+    for path in ("BUCKETED", "DIRECT"):
+        capi.set_path(getattr(capi.Path, path))
+        b = cuda.full((m // 32,), -1, dtype=cuda.int32, device="cuda")
+        capi.bitset_build(t.data_ptr(), t.numel(), b.data_ptr(), m)
+        cuda.cuda.synchronize()
+        bits[path] = b
+    assert cuda.equal(bits["BUCKETED"], bits["DIRECT"])
+    capi.set_path(capi.Path.BUCKETED)
+    dup = keys.copy()
+    dup[1] = dup[keys.size - 2]
+    assert capi.sort_raw(dup.ctypes.data, dup.size, 32, 1, 0) == capi.Status.ERROR_DATA
+
+
 @pytest.mark.parametrize("kind", ["distinct", "overflow"])
 def test_slab_layout_bitset_build(capi, cuda, kind):
     """The per-rank bitset build (KB4b) over the slab layout: exact bitset for
