@@ -295,6 +295,14 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     constexpr size_t kTileVec = TILE / 4;
     const size_t ntiles = (vhi - vlo + kTileVec - 1) / kTileVec;
     const uint32_t spill = static_cast<uint32_t>(nb);
+    // Slot of a key: its bucket, or the spill slot for padding lanes and (slab
+    // layout, which has no KB1 to count them) keys beyond the range, so the
+    // spill count of a tile gives the out-of-range keys for free.
+    const uint32_t last = SLAB && sa.check ? sa.limit - 1u : 0xffffffffu;
+    auto slot_of = [&](uint32_t key, bool in) -> uint32_t {
+        if constexpr (SLAB) return in && key <= last ? bucket_id(key, bm) : spill;
+        else return bucket_or_spill(key, in, bm, nb);
+    };
 
     if (threadIdx.x == 0) {
         mbar_init(&s_bar[0], 1);
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         int ne = c == 0 ? ks.n_head : 0;
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
-                const uint32_t b = bucket_or_spill(extra[i], true, bm, nb);
+                const uint32_t b = slot_of(extra[i], true);
                 if constexpr (SLAB) {
                     bad += (sa.check && extra[i] >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
@@ -377,14 +385,13 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 k[4 * j + q] = kk[q];
-                rb[4 * j + q] = bucket_or_spill(kk[q], in, bm, nb);
+                rb[4 * j + q] = slot_of(kk[q], in);
                 kmin = min(kmin, kk[q]);
                 kmax = max(kmax, kk[q]);
-                if constexpr (SLAB) bad += (sa.check && in && kk[q] >= sa.limit) ? 1u : 0u;
             }
         }
-        const uint32_t blo = bucket_or_spill(__reduce_min_sync(kFull, kmin), true, bm, nb);
-        const uint32_t bhi = bucket_or_spill(__reduce_max_sync(kFull, kmax), true, bm, nb);
+        const uint32_t blo = slot_of(__reduce_min_sync(kFull, kmin), true);
+        const uint32_t bhi = slot_of(__reduce_max_sync(kFull, kmax), true);
         if (blo == bhi && __all_sync(kFull, all_in)) {
             // the whole warp step lies in one bucket: one atomic, ranks by lane
             uint32_t base = 0;
@@ -422,8 +429,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                         const uint32_t cb = s_cnt[b];
                         s_start[b] = run;
                         s_cnt[b] = 0;
-                        if (b == nb) s_tile_valid = run;  // spill keys sort after every bucket
-                        else if (cb) claim[q] = atomicAdd(sa.gcnt + b, cb);
+                        if (b == nb) {
+                            s_tile_valid = run;  // spill keys sort after every bucket
+                            bad += cb - (TILE - 4 * nvec);  // out-of-range keys (padding lanes spill too)
+                        } else if (cb) {
+                            claim[q] = atomicAdd(sa.gcnt + b, cb);
+                        }
                         ccnt[q] = b < nb ? cb : 0u;
                         run += cb;
                     }
