@@ -1343,6 +1343,10 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+        else if (plan.nb <= PART_NARROW_MAXB)  // fewer slot-scan iterations per thread
+            bucket_partition_kernel<PART_THREADS, PART_KPT, PART_NARROW_MAXB, true>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, PART_NARROW_MAXB), stream>>>(
+                    ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         else
             bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
@@ -1424,6 +1428,10 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_THREADS, PART_NARROW_MAXB)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
