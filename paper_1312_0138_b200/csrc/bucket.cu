@@ -1283,9 +1283,9 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
         return 0;
     uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
     if (cap > plan.map.width) cap = plan.map.width;
-    const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_TILE;  // + dump tile
+    const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_DUMP;  // + dump tile
     // the slab trades memory (up to 4.5 slots per key) for the histogram pass
-    if (slots > 4 * static_cast<uint64_t>(n) + n / 2 + PART_TILE || slots >= (1ull << 32)) return 0;
+    if (slots > 4 * static_cast<uint64_t>(n) + n / 2 + PART_DUMP || slots >= (1ull << 32)) return 0;
     return slots;
 }
 
@@ -1331,8 +1331,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         // KB3 (slab) claims slots with fill counters: no KB1/KB2. The counters
         // are zeroed once at allocation and re-zeroed by the last KB3 CTA.
         sa.gcnt = gcnt;
-        sa.cap = static_cast<uint32_t>((slab - PART_TILE) / plan.nb);
-        sa.dump = static_cast<uint32_t>(slab - PART_TILE);
+        sa.cap = static_cast<uint32_t>((slab - PART_DUMP) / plan.nb);
+        sa.dump = static_cast<uint32_t>(slab - PART_DUMP);
         sa.limit = limit;
         sa.check = check;
         sa.ctrl = ctrl;
@@ -1344,8 +1344,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         else if (plan.nb <= PART_NARROW_MAXB)  // fewer slot-scan iterations per thread
-            bucket_partition_kernel<PART_THREADS, PART_KPT, PART_NARROW_MAXB, true>
-                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, PART_NARROW_MAXB), stream>>>(
+            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, true>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, PART_NARROW_MAXB, PART_KPT_SLAB), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         else
             bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
@@ -1429,9 +1429,9 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(part_smem_bytes(PART_THREADS, PART_NARROW_MAXB)));
+                               static_cast<int>(part_smem_bytes(PART_THREADS, PART_NARROW_MAXB, PART_KPT_SLAB)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -68,8 +68,10 @@ constexpr int CLUSTER_SUB_SHIFT = 20;   // each cluster CTA owns a 2^20-key sub-
 constexpr int CLUSTER_CHUNK = 4096;     // keys per multicast chunk (16 KB), two buffers
 constexpr int CLUSTER_STAGE = 256;      // keys per warp in the cluster kernel's stage
 
-constexpr std::size_t part_smem_bytes(int threads, int maxb) {
-    return 2 * std::size_t(threads) * PART_KPT * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
+constexpr int PART_KPT_SLAB = 20;   // slab KB3 with <= 1024 buckets: 20480-key tiles
+constexpr int PART_DUMP = 32768;    // slab overflow tile (>= any KB3 tile)
+constexpr std::size_t part_smem_bytes(int threads, int maxb, int kpt = PART_KPT) {
+    return 2 * std::size_t(threads) * kpt * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
 }
 constexpr std::size_t bucket_sort_smem_bytes(int shift) {
     const int stage = shift >= MAX_BUCKET_SHIFT ? BUCKET_STAGE : BUCKET_STAGE_SMALL;
