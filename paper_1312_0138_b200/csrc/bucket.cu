@@ -802,8 +802,8 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
             extract_span512<STAGE>(s_bits, seg, seg_words, key_hi, o, s_stage, lane, false, nullptr);
         } else if (seg_words % 128 == 0) {
             // 128-word steps, lane-major (lane owns 4 words); a step with
-            // <= BUCKET_STAGE keys is extracted in one pass, denser steps fall
-            // back to four 32-word sub-steps (word per lane)
+            // <= STAGE keys is extracted in one pass, denser steps as two
+            // 64-word sub-steps (two words per lane)
             for (uint32_t w0 = 0; w0 < seg_words; w0 += 128) {
                 const uint4 v = s4[(seg + w0) / 4 + lane];
                 const uint32_t cl = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
@@ -821,9 +821,14 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
                     o += ctot;
                     continue;
                 }
+                if (ctot > 2u * STAGE) {  // dense: word-by-word ballots
 #pragma unroll 1
-                for (uint32_t q = 0; q < 128; q += 32)
-                    o += extract_words32<STAGE>(s_bits, seg + w0 + q, key_hi, o, s_stage, lane);
+                    for (uint32_t q = 0; q < 128; q += 32)
+                        o += extract_words32<STAGE>(s_bits, seg + w0 + q, key_hi, o, s_stage, lane);
+                    continue;
+                }
+                const uint32_t n0 = extract_words64<STAGE>(s_bits, seg + w0, key_hi, o, s_stage, lane);
+                o += n0 + extract_words64<STAGE>(s_bits, seg + w0 + 64, key_hi, o + n0, s_stage, lane);
             }
         } else {
             for (uint32_t w0 = 0; w0 < seg_words; w0 += 32)

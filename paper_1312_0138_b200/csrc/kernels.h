@@ -61,7 +61,7 @@ constexpr int PART_TILE = PART_THREADS * PART_KPT;  // 16384 keys per wide tile
 constexpr int PART_NARROW_THREADS = 512;
 constexpr int PART_NARROW_MAXB = 1024;
 constexpr int BUCKET_THREADS = 1024;
-constexpr int BUCKET_STAGE = 512;        // keys per warp in the extraction stage (2^20 buckets)
+constexpr int BUCKET_STAGE = 640;        // keys per warp in the extraction stage (2^20 buckets)
 constexpr int BUCKET_STAGE_SMALL = 256;  // narrower buckets: fits two CTAs per SM
 constexpr int MAX_CLUSTER = 8;          // CTAs per bucket in the cluster KB4 (portable limit)
 constexpr int CLUSTER_SUB_SHIFT = 20;   // each cluster CTA owns a 2^20-key sub-range
