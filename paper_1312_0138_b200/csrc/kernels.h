@@ -30,7 +30,7 @@ constexpr int SCAN_TILE_WORDS = SCAN_THREADS * SCAN_ROUNDS;  // 2048 words = 655
 // K3 v2 geometry (scan.cu): 8192-word tiles via TMA, 16 warps, 2 CTAs/SM.
 constexpr int SCAN2_THREADS = 512;
 constexpr int SCAN2_TILE_WORDS = 8192;
-constexpr int SCAN2_STAGE = 512;  // keys per warp stage
+constexpr int SCAN2_STAGE = 640;  // keys per warp stage
 constexpr std::size_t scan2_smem_bytes() {
     return 2 * SCAN2_TILE_WORDS * 4 + (SCAN2_THREADS / 32) * (SCAN2_STAGE + SCAN2_STAGE / 32) * 4;  // 2nd buffer spare
 }
