@@ -713,7 +713,11 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     uint32_t* s_sum = s_bits + W;             // bit w set <=> word w touched (sparse buckets)
     uint32_t* s_stage_all = s_sum + W / 32;   // BUCKET_THREADS/32 x stage pitch
     __shared__ uint32_t s_warp[BUCKET_THREADS / 32];
-    __shared__ unsigned s_b;
+    // next bucket (ticket, offset, count), fetched by thread 0 one bucket ahead
+    // so its latency hides behind the current bucket (sparse buckets are short)
+    __shared__ unsigned s_b[2];
+    __shared__ unsigned long long s_bbase[2];
+    __shared__ uint32_t s_bcnt[2];
 
     const unsigned lane = threadIdx.x & 31;
     const unsigned warp = threadIdx.x >> 5;
@@ -722,19 +726,29 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     const uint32_t seg_words = W / (BUCKET_THREADS / 32);
     const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
 
+    auto fetch = [&](int slot) {  // thread 0
+        const unsigned nbk = atomicAdd(&ctrl->ticket, 1u);
+        s_b[slot] = nbk;
+        if (nbk < static_cast<unsigned>(nb)) {
+            s_bbase[slot] = g_base[nbk];
+            s_bcnt[slot] = tot[nbk];
+        }
+    };
     for (uint32_t i = threadIdx.x; i < W / 32; i += BUCKET_THREADS) s_sum[i] = 0u;
+    if (threadIdx.x == 0) fetch(0);
     bool dirty = true;  // block-uniform: bitset needs zeroing before the next bucket
-    for (;;) {
-        if (threadIdx.x == 0) s_b = atomicAdd(&ctrl->ticket, 1u);
+    for (unsigned it = 0;; ++it) {
+        const int slot = static_cast<int>(it & 1u);
         if (dirty) {  // the previous bucket's readers finished at the loop-end barrier
             uint4* b4 = reinterpret_cast<uint4*>(s_bits);
             for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
         }
         __syncthreads();
-        const unsigned b = s_b;
+        const unsigned b = s_b[slot];
         if (b >= static_cast<unsigned>(nb)) break;
-        const unsigned long long base = g_base[b];
-        const uint32_t cnt = tot[b];
+        const unsigned long long base = s_bbase[slot];
+        const uint32_t cnt = s_bcnt[slot];
+        if (threadIdx.x == 0) fetch(slot ^ 1);  // read again only after two more barriers
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         if (sparse)
