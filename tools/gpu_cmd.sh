@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
-for c in C2 C4 C5; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${c}.json 2>&1; done
+timeout 300 python bench.py --config C2 --steps 50 --warmup 5 > gpurun_out/bench_C2_full.json 2>&1
+BENCH_NO_KERNEL_TIMING=1 timeout 300 python bench.py --config C2 --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_C2_nokt.json 2>&1
