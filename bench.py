@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU (NCCL reduce-scatter) path even with one rank")
+    ap.add_argument("--a2a", action="store_true",
+                    help="multi-GPU key all-to-all variant (range split + NCCL all-to-all + range sort)")
     return ap.parse_args()
 
 
@@ -257,7 +259,7 @@ def run_ours(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    use_dist = world > 1 or args.dist
+    use_dist = world > 1 or args.dist or args.a2a
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
@@ -269,7 +271,11 @@ def run_ours(args, cfg):
     keys_h = cfg.generate()
     n_total, M = cfg.n, cfg.key_range
     if use_dist:
-        from paper_1312_0138_b200.dist import CudaRankOps, distributed_sort, shard_bounds
+        from paper_1312_0138_b200.dist import CudaRankOps, shard_bounds
+        from paper_1312_0138_b200.dist import distributed_sort as dist_rs
+        from paper_1312_0138_b200.dist import distributed_sort_a2a as dist_a2a
+
+        distributed_sort = dist_a2a if args.a2a else dist_rs
 
         lo, hi = shard_bounds(n_total, rank, world)
         shard_h = keys_h[lo:hi]
@@ -450,7 +456,9 @@ def run_ours(args, cfg):
         "config": {"workload": cfg.name, "n": n_total, "key_range": M, "recipe": cfg.recipe,
                    "l2": "flushed between steps (256 MiB write, outside the step events)",
                    "path": args.path,
-                   "parallelism": f"key shards x{world} + NCCL reduce-scatter" if use_dist else "single GPU"},
+                   "parallelism": (f"key shards x{world} + " + ("NCCL all-to-all of range-split keys"
+                                                                  if args.a2a else "NCCL reduce-scatter"))
+                   if use_dist else "single GPU"},
         "step_ms": {"median": round(statistics.median(step_ms), 4), "best": round(min(step_ms), 4),
                     "worst": round(max(step_ms), 4)},
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,

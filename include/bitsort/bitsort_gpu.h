@@ -32,6 +32,25 @@ BITSORT_API bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t co
                                                  uint32_t* out, uint64_t key_range,
                                                  void* stream);
 
+/* bws_gpu_sort_device_async for keys in [key_lo, key_lo + key_range)
+ * (key_lo + key_range <= 2^32): the bucketed pipeline works on key - key_lo,
+ * so a rank's slice of a larger range (multi-GPU key all-to-all) costs no
+ * more than a sort starting at 0. Checked by bws_gpu_sort_check. */
+BITSORT_API bws_status bws_gpu_sort_range_device_async(const uint32_t* keys, size_t count,
+                                                       uint32_t* out, uint32_t key_lo,
+                                                       uint64_t key_range, void* stream);
+
+/* Range split for the multi-GPU key all-to-all: writes
+ * the `count` device keys (all < key_range) to `out` grouped by part, part p
+ * holding keys in [p * W, (p + 1) * W) ∩ [0, key_range), in part order (order
+ * inside a part is unspecified), and the number of keys of each part to the
+ * device array d_counts[parts] (uint32). *part_width receives W (the smallest
+ * q * 2^s >= ceil(key_range / parts), q <= 8). Synchronises `stream`; keys >=
+ * key_range -> BWS_ERROR_DATA. */
+BITSORT_API bws_status bws_gpu_range_split(const uint32_t* keys, size_t count, uint64_t key_range,
+                                           int parts, uint32_t* out, uint32_t* d_counts,
+                                           uint64_t* part_width, void* stream);
+
 /* Synchronises `stream` and validates the last bws_gpu_sort_device_async on
  * the current device: BWS_ERROR_DATA on duplicates / out-of-range keys.
  * *distinct_out (optional) receives the number of keys written. */

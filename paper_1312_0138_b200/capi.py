@@ -87,6 +87,8 @@ def _load() -> ctypes.CDLL:
         "bws_sort_u32_range": (i32, [vp, sz, u64]),
         "bws_gpu_sort_device_async": (i32, [vp, sz, vp, u64, vp]),
         "bws_gpu_sort_check": (i32, [vp, ctypes.POINTER(u64)]),
+        "bws_gpu_sort_range_device_async": (i32, [vp, sz, vp, u32, u64, vp]),
+        "bws_gpu_range_split": (i32, [vp, sz, u64, i32, vp, vp, ctypes.POINTER(u64), vp]),
         "bws_gpu_bitset_build": (i32, [vp, sz, vp, u64, vp]),
         "bws_gpu_bitset_scan": (i32, [vp, u64, u32, vp, u64, vp, vp]),
         "bws_gpu_set_scatter_mode": (i32, [i32]),
@@ -111,6 +113,7 @@ lib = _load()
 EXPORTED = (
     "bws_version", "bws_last_error", "bws_algorithm_name", "bws_algorithm_from_name",
     "bws_sort", "bws_sort_u32_range", "bws_gpu_sort_device_async", "bws_gpu_sort_check",
+    "bws_gpu_sort_range_device_async", "bws_gpu_range_split",
     "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode", "bws_gpu_set_path",
     "bws_gpu_set_device_count", "bws_gpu_device_count", "bws_gpu_launch_count",
     "bws_gpu_set_kernel_timing", "bws_gpu_kernel_timings",
@@ -174,6 +177,22 @@ def sort_u32_range(data, key_range: int) -> None:
 
 def sort_device_async(keys_ptr: int, count: int, out_ptr: int, key_range: int, stream: int = 0) -> None:
     _check(lib.bws_gpu_sort_device_async(keys_ptr, count, out_ptr, key_range, stream or None))
+
+
+def sort_range_device_async(keys_ptr: int, count: int, out_ptr: int, key_lo: int, key_range: int,
+                            stream: int = 0) -> None:
+    """Device sort of keys in [key_lo, key_lo + key_range); check with sort_check."""
+    _check(lib.bws_gpu_sort_range_device_async(keys_ptr, count, out_ptr, key_lo, key_range, stream or None))
+
+
+def range_split(keys_ptr: int, count: int, key_range: int, parts: int, out_ptr: int, counts_ptr: int,
+                stream: int = 0) -> int:
+    """Groups device keys by part (part p = keys in [p*W, (p+1)*W)); writes uint32
+    counts per part to the device array at counts_ptr; returns W."""
+    w = ctypes.c_uint64(0)
+    _check(lib.bws_gpu_range_split(keys_ptr, count, key_range, parts, out_ptr, counts_ptr,
+                                   ctypes.byref(w), stream or None))
+    return int(w.value)
 
 
 def sort_check(stream: int = 0) -> int:

@@ -91,7 +91,7 @@ __device__ unsigned long long block_exclusive_scan_u64(const uint32_t* vals, int
 // [key_range, nb * width) (ranges that are not a multiple of the width) lands in the last bucket;
 // KB1 counts it in ctrl->bad_keys exactly, and the host then rejects the sort.
 __device__ __forceinline__ uint32_t bucket_id(uint32_t k, const BucketMap& m) {
-    return __umulhi((k >> m.ms) << 12, m.mq);
+    return __umulhi(((k - m.lo) >> m.ms) << 12, m.mq);
 }
 __device__ __forceinline__ uint32_t bucket_or_spill(uint32_t k, bool in, const BucketMap& m, int nb) {
     return in ? min(bucket_id(k, m), static_cast<uint32_t>(nb)) : static_cast<uint32_t>(nb);
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
                 bk[u * 4 + q] = bucket_or_spill(kk[q], in[u], bm, nb);
                 kmin = min(kmin, in[u] ? kk[q] : 0xffffffffu);
                 kmax = max(kmax, in[u] ? kk[q] : 0u);
-                bad += (check && in[u] && kk[q] >= limit) ? 1u : 0u;
+                bad += (check && in[u] && kk[q] - bm.lo >= limit) ? 1u : 0u;
             }
         }
         mx = max(mx, kmax);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
             for (int i = 0; i < ne; ++i) {
                 atomicAdd(s_h + bucket_or_spill(extra[i], true, bm, nb), 1u);
                 mx = max(mx, extra[i]);
-                bad += (check && extra[i] >= limit) ? 1u : 0u;
+                bad += (check && extra[i] - bm.lo >= limit) ? 1u : 0u;
             }
             extra = c == P - 1 ? ks.tail : nullptr;
             ne = c == P - 1 ? ks.n_tail : 0;
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     // spill count of a tile gives the out-of-range keys for free.
     const uint32_t last = SLAB && sa.check ? sa.limit - 1u : 0xffffffffu;
     auto slot_of = [&](uint32_t key, bool in) -> uint32_t {
-        if constexpr (SLAB) return in && key <= last ? bucket_id(key, bm) : spill;
+        if constexpr (SLAB) return in && key - bm.lo <= last ? bucket_id(key, bm) : spill;
         else return bucket_or_spill(key, in, bm, nb);
     };
 
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             for (int i = 0; i < ne; ++i) {
                 const uint32_t b = slot_of(extra[i], true);
                 if constexpr (SLAB) {
-                    bad += (sa.check && extra[i] >= sa.limit) ? 1u : 0u;
+                    bad += (sa.check && extra[i] - bm.lo >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
                         const uint32_t pos = atomicAdd(sa.gcnt + b, 1u);
                         if (pos < sa.cap) parted[b * sa.cap + pos] = extra[i];
@@ -752,9 +752,9 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         if (sparse)
-            scatter_bucket_keys<true>(src, cnt, static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
+            scatter_bucket_keys<true>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
         else
-            scatter_bucket_keys<false>(src, cnt, static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
+            scatter_bucket_keys<false>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
         __syncthreads();
         // phase 1: per-warp popcount of its segment (128-bit SMEM reads; sparse
         // buckets read only the touched words, found through the summary)
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         }
         __syncthreads();
         uint32_t* o = out + base + s_warp[warp];
-        const uint32_t key_hi = static_cast<uint32_t>(b) * bm.width;
+        const uint32_t key_hi = bm.lo + static_cast<uint32_t>(b) * bm.width;
         if (sparse) {
             // lane-major over summary words: lane owns 32 consecutive bitset
             // words (one summary word) per round; its keys are contiguous in
@@ -1125,7 +1125,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
         const unsigned b = s_b;
         if (b >= static_cast<unsigned>(nb)) break;
         scatter_bucket_keys<false>(parted + (src_cap ? static_cast<size_t>(b) * src_cap : g_base[b]), tot[b],
-                                   static_cast<uint32_t>(b) * bm.width, s_bits, nullptr);
+                                   bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, nullptr);
         __syncthreads();
         const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
         // keys in [key_range, 32 * n_words) of a non-multiple-of-32 range never appear
@@ -1292,12 +1292,43 @@ BucketPlan plan_buckets(uint64_t key_range, int kb4_ctas, bool allow_cluster) {
     return p;
 }
 
+BucketPlan plan_range_split(uint64_t key_range, int parts) {
+    BucketPlan p;
+    const uint64_t want = (key_range + parts - 1) / parts;
+    uint64_t best = 0;
+    int best_s = 12;
+    uint32_t best_q = 1;
+    for (int s = 12; s <= 31; ++s) {  // (key >> 32 would be undefined)
+        for (uint32_t q = 1; q <= 8; ++q) {
+            const uint64_t w = static_cast<uint64_t>(q) << s;
+            if (w < want || (q > 1 && s < 15)) continue;  // q > 1 needs s >= 15 for an exact map
+            if (best == 0 || w < best) {
+                best = w;
+                best_s = s;
+                best_q = q;
+            }
+        }
+    }
+    p.map.ms = best_s;
+    p.map.mq = ((1u << 20) + best_q - 1) / best_q;
+    p.map.width = best >= (1ull << 32) ? 0xffffffffu : static_cast<uint32_t>(best);
+    p.shift = MAX_BUCKET_SHIFT;
+    p.nb = parts;
+    p.partition_only = true;
+    return p;
+}
+
+const uint32_t* bucket_totals(const void* scratch, const BucketPlan& plan, const LaunchGeometry& geo) {
+    const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
+    return static_cast<const uint32_t*>(scratch) + MAX_BUCKETS + static_cast<size_t>(P) * plan.nb;
+}
+
 uint64_t slab_slots(const BucketPlan& plan, size_t n) {
     static const bool off = [] {
         const char* e = std::getenv("BITSORT_SLAB");
         return e && std::string(e) == "0";
     }();
-    if (off || plan.cluster > 1 ||
+    if (off || plan.cluster > 1 || plan.partition_only ||
         (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE")))
         return 0;
     uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
@@ -1403,6 +1434,10 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (timer) timer->after("bucket_partition", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         nlaunch = 3;
+    }
+    if (plan.partition_only) {  // range split: the packed groups are the result
+        if (launches) *launches = nlaunch;
+        return cudaSuccess;
     }
     const uint32_t src_cap = use_slab ? sa.cap : 0u;
     if (bits_out) {  // multi-GPU per-rank build: write the bitset instead of sorted keys

@@ -468,7 +468,7 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
 // Bucketed pipeline: [K0 max + host readback when no hint] -> KB1..KB4.
 // Leaves the cached bitset untouched.
 void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
-                      uint64_t key_range, cudaStream_t stream) {
+                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0) {
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
     cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
     if (key_range == 0) {
@@ -480,8 +480,8 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
         cuda_check(cudaStreamSynchronize(stream), "key_max execution");
         key_range = static_cast<uint64_t>(mx) + 1;
     }
-    const bws_gpu::BucketPlan plan =
-        bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
+    bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
+    plan.map.lo = key_lo;
     const size_t parted_cap = ctx.ensure_parted(count, plan);
     int launches = 0;
     cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
@@ -708,6 +708,73 @@ bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t count, uint32_
         ctx.last_range = key_range;
         if (count == 0) return;
         enqueue_sort(ctx, keys, count, out, key_range, static_cast<cudaStream_t>(stream));
+    });
+}
+
+bws_status bws_gpu_sort_range_device_async(const uint32_t* keys, size_t count, uint32_t* out,
+                                           uint32_t key_lo, uint64_t key_range, void* stream) {
+    return wrap([&] {
+        if (count > 0 && (keys == nullptr || out == nullptr))
+            throw data_error("null device pointer with nonzero count");
+        if (key_range == 0 || static_cast<uint64_t>(key_lo) + key_range > kMaxKeyRange)
+            throw std::out_of_range("key range [" + std::to_string(key_lo) + ", " +
+                                    std::to_string(static_cast<uint64_t>(key_lo) + key_range) +
+                                    ") is empty or exceeds 2^32");
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        ctx.last_count = count;
+        ctx.last_range = key_range;
+        if (count == 0) return;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (key_lo == 0) {
+            enqueue_sort(ctx, keys, count, out, key_range, s);
+        } else {
+            if (count >= (size_t(1) << 32)) throw std::out_of_range("range sorts take fewer than 2^32 keys");
+            enqueue_bucketed(ctx, keys, count, out, key_range, s, key_lo);
+        }
+    });
+}
+
+bws_status bws_gpu_range_split(const uint32_t* keys, size_t count, uint64_t key_range, int parts,
+                               uint32_t* out, uint32_t* d_counts, uint64_t* part_width, void* stream) {
+    return wrap([&] {
+        if (parts < 1 || parts > bws_gpu::MAX_BUCKETS) throw std::out_of_range("parts must be in [1, 4096]");
+        if (key_range == 0 || key_range > kMaxKeyRange) throw std::out_of_range("key range must be in [1, 2^32]");
+        if (d_counts == nullptr || part_width == nullptr || (count > 0 && (keys == nullptr || out == nullptr)))
+            throw data_error("null pointer");
+        if (count >= (size_t(1) << 32)) throw std::out_of_range("range split takes fewer than 2^32 keys");
+        const bws_gpu::BucketPlan plan = bws_gpu::plan_range_split(key_range, parts);
+        *part_width = plan.map.width == 0xffffffffu ? kMaxKeyRange : plan.map.width;
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        if (count == 0) {
+            cuda_check(cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * parts, s), "count reset");
+        } else {
+            cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
+            int launches = 0;
+            cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, nullptr, out, ctx.bucket_scratch,
+                                                   ctx.ctrl(), plan, ctx.geo, s, &launches, active_timer()),
+                       "range split launch");
+            g_launches.fetch_add(static_cast<uint64_t>(launches));
+            cuda_check(cudaMemcpyAsync(d_counts, bws_gpu::bucket_totals(ctx.bucket_scratch, plan, ctx.geo),
+                                       sizeof(uint32_t) * parts, cudaMemcpyDeviceToDevice, s),
+                       "part counts");
+            // keys >= key_range are counted by KB1: report them like a sort would
+            unsigned int bad = 0;
+            cuda_check(cudaMemcpyAsync(&bad, &ctx.ctrl()->bad_keys, sizeof(bad), cudaMemcpyDeviceToHost, s),
+                       "bad key count");
+            cuda_check(cudaStreamSynchronize(s), "range split execution");
+            if (bad != 0)
+                throw data_error(std::to_string(bad) + " key(s) not below the key range " +
+                                 std::to_string(key_range));
+        }
+        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
     });
 }
 

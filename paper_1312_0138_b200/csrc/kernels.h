@@ -114,6 +114,7 @@ struct BucketMap {
     int ms = 20;
     std::uint32_t mq = 1u << 20;
     std::uint32_t width = 1u << 20;  // keys per bucket
+    std::uint32_t lo = 0;            // first key of bucket 0 (range sorts); key - lo is bucketed
 };
 
 struct BucketPlan {
@@ -121,6 +122,7 @@ struct BucketPlan {
     int nb = 1;       // number of buckets, <= MAX_BUCKETS
     int cluster = 1;  // CTAs per bucket in KB4 (bucket range = cluster * 2^20 when > 1)
     BucketMap map;
+    bool partition_only = false;  // stop after KB3 (range split: packed groups, totals in scratch)
 };
 
 // Slab layout of the bucket buffer (KB3 without KB1/KB2): bucket b owns the
@@ -183,6 +185,12 @@ cudaError_t launch_scan2(std::uint32_t* bits, std::uint64_t n_words, std::uint32
 
 // Bucketed pipeline (bucket.cu). plan_buckets picks the bucket width for a
 // key range; bucket_scratch_bytes sizes the histogram/offset scratch.
+// Range split into `parts` groups of consecutive key ranges (multi-GPU key
+// all-to-all): group width = the smallest q * 2^s >= ceil(key_range / parts)
+// (q <= 8, s >= 12), so the bucket map stays exact; the last group is shorter.
+BucketPlan plan_range_split(std::uint64_t key_range, int parts);
+// Bucket totals (uint32 per bucket) in the scratch of the last launch_bucket_sort.
+const std::uint32_t* bucket_totals(const void* scratch, const BucketPlan& plan, const LaunchGeometry& geo);
 // kb4_ctas: resident KB4 CTAs (0: power-of-two widths only). With
 // allow_cluster, ranges above 2^28 may use the opt-in cluster KB4.
 BucketPlan plan_buckets(std::uint64_t key_range, int kb4_ctas, bool allow_cluster = true);

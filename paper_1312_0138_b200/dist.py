@@ -11,6 +11,13 @@ Rank r of G holds an input-position shard of the keys. Each rank
      so the total only drops) -> BWS_ERROR_DATA.
 The global sorted array is the rank-order concatenation of the local outputs.
 
+Key all-to-all variant (``distributed_sort_a2a``): rank r
+splits its shard by destination key range (range split, C ABI), the ranks
+exchange the groups with one all-to-all (4n/G bytes per rank instead of the
+reduce-scatter's (G-1)/G * M/8), and each rank sorts the keys of its range
+[r*W, (r+1)*W) with the bucketed pipeline offset by r*W. Cheaper than the
+bitset reduce-scatter whenever n/M < G/32 (sparse ranges: C4, C5).
+
 The collectives go through torch.distributed (NCCL on GPUs; gloo in the CPU
 tests). The per-rank compute is an injectable ``RankOps``: ``CudaRankOps``
 (the product, sm_100a kernels through libbitsort.so) or, in tests only, an
@@ -32,6 +39,14 @@ class RankOps(Protocol):
     def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int) -> tuple[torch.Tensor, torch.Tensor]:
         """(out[capacity] keys, count as a 1-element int64 tensor) of a slice."""
 
+    def range_split(self, keys: torch.Tensor, key_range: int, parts: int):
+        """(keys grouped by part, int64 counts[parts] tensor, part width W, ok):
+        part p holds keys in [p*W, (p+1)*W); ok is False if a key >= key_range."""
+
+    def sort_range(self, keys: torch.Tensor, key_lo: int, key_range: int):
+        """(sorted keys, ok) for keys in [key_lo, key_lo + key_range); ok is
+        False on duplicates or keys outside the range."""
+
 
 @dataclass
 class SliceResult:
@@ -49,6 +64,22 @@ def slice_words(key_range: int, world: int) -> tuple[int, int]:
     words = (key_range + 31) // 32
     per = (words + world - 1) // world
     return per * world, per
+
+
+def part_width(key_range: int, parts: int) -> int:
+    """Range-split part width: the smallest q * 2^s >= ceil(key_range / parts)
+    with q <= 8, s in [12, 31] and s >= 15 when q > 1 (the bucket map of the C
+    library's range split, bucket.cu plan_range_split, which this mirrors)."""
+    want = -(-key_range // parts)
+    best = None
+    for s_ in range(12, 32):
+        for q in range(1, 9):
+            w = q << s_
+            if w < want or (q > 1 and s_ < 15):
+                continue
+            if best is None or w < best:
+                best = w
+    return best
 
 
 def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -80,6 +111,28 @@ class CudaRankOps:
         self._capi.bitset_build(keys.data_ptr(), keys.numel(), bits.data_ptr(), key_range,
                                 self._stream())
         return bits
+
+    def range_split(self, keys: torch.Tensor, key_range: int, parts: int):
+        grouped = torch.empty(max(keys.numel(), 1), dtype=torch.int32, device=self.device)
+        counts = torch.zeros(parts, dtype=torch.int32, device=self.device)
+        try:
+            width = self._capi.range_split(keys.data_ptr(), keys.numel(), key_range, parts,
+                                           grouped.data_ptr(), counts.data_ptr(), self._stream())
+        except self._capi.BitsortError:
+            return grouped, counts.to(torch.int64), 0, False
+        return grouped, counts.to(torch.int64), width, True
+
+    def sort_range(self, keys: torch.Tensor, key_lo: int, key_range: int):
+        out = torch.empty_like(keys)
+        if keys.numel() == 0:
+            return out, True
+        s = self._stream()
+        self._capi.sort_range_device_async(keys.data_ptr(), keys.numel(), out.data_ptr(), key_lo, key_range, s)
+        try:
+            self._capi.sort_check(s)
+        except self._capi.BitsortError:
+            return out, False
+        return out, True
 
     def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int):
         if self._out is None or self._out.numel() < capacity:
@@ -122,6 +175,63 @@ def distributed_sort(keys: torch.Tensor, key_range: int, n_total: Optional[int] 
 
         raise BitsortError(Status.ERROR_DATA,
                            f"keys are not distinct or out of range: {n_total} keys, {total} distinct")
+    count = counts_h[rank]
+    return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
+                       key_lo=key_lo, key_hi=key_hi)
+
+
+def _data_error(msg: str):
+    from .capi import BitsortError, Status
+
+    return BitsortError(Status.ERROR_DATA, msg)
+
+
+def distributed_sort_a2a(keys: torch.Tensor, key_range: int, n_total: Optional[int] = None,
+                         ops: Optional[RankOps] = None, group=None) -> SliceResult:
+    """Key all-to-all variant of :func:`distributed_sort`: same inputs, same
+    global result; rank r's slice is the sorted keys of [r*W, (r+1)*W) where W
+    is the range-split part width."""
+    if not 0 < key_range <= 1 << 32:
+        raise ValueError("key_range must be in [1, 2^32]")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ops = ops or CudaRankOps(keys.device)
+    dev = keys.device
+    if n_total is None:
+        t = torch.tensor([keys.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, group=group)
+        n_total = int(t.item())
+
+    if world == 1:  # one part: the split is the identity
+        grouped, width, ok = keys, part_width(key_range, 1), True
+        counts = torch.tensor([keys.numel()], dtype=torch.int64, device=dev)
+    else:
+        grouped, counts, width, ok = ops.range_split(keys, key_range, world)
+    bad = torch.tensor([0 if ok else 1], dtype=torch.int64, device=dev)
+    dist.all_reduce(bad, group=group)  # every rank raises together, before the exchange
+    if int(bad.item()):
+        raise _data_error(f"keys not below the key range {key_range} on {int(bad.item())} rank(s)")
+    counts = counts.to(dev)
+    recv_counts = torch.empty_like(counts)
+    dist.all_to_all_single(recv_counts, counts, group=group)
+    sc = [int(c) for c in counts.tolist()]
+    rc = [int(c) for c in recv_counts.tolist()]
+    recv = torch.empty(sum(rc), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(recv, grouped[:sum(sc)], output_split_sizes=rc, input_split_sizes=sc,
+                           group=group)
+
+    key_lo = min(rank * width, key_range)
+    key_hi = min((rank + 1) * width, key_range)
+    out, ok = ops.sort_range(recv, key_lo, max(key_hi - key_lo, 1)) if recv.numel() else (recv, True)
+    stat = torch.tensor([recv.numel(), 0 if ok else 1], dtype=torch.int64, device=dev)
+    stats = [torch.empty_like(stat) for _ in range(world)]
+    dist.all_gather(stats, stat, group=group)
+    counts_h = [int(x[0].item()) for x in stats]
+    errors = sum(int(x[1].item()) for x in stats)
+    total = sum(counts_h)
+    if errors or total != n_total:
+        raise _data_error(f"keys are not distinct: {n_total} keys, duplicates within "
+                          f"{errors} rank range(s)")
     count = counts_h[rank]
     return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
                        key_lo=key_lo, key_hi=key_hi)

@@ -17,7 +17,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1312_0138_b200.dist import distributed_sort, shard_bounds, slice_words
+from paper_1312_0138_b200.dist import (distributed_sort, distributed_sort_a2a, part_width,
+                                       shard_bounds, slice_words)
 
 
 class OracleRankOps:
@@ -33,6 +34,24 @@ class OracleRankOps:
         cnt = oracle.ORACLE.oracle_bitset_scan(b.ctypes.data, b.size, key_base, out.ctypes.data, capacity)
         return torch.from_numpy(out.view(np.int32)), torch.tensor([cnt], dtype=torch.int64)
 
+    def range_split(self, keys, key_range, parts):
+        k = keys.numpy().view(np.uint32).astype(np.uint64)
+        if k.size and int(k.max()) >= key_range:
+            return keys, torch.zeros(parts, dtype=torch.int64), 0, False
+        w = part_width(key_range, parts)
+        dest = k // w
+        order = np.argsort(dest, kind="stable")
+        counts = np.bincount(dest.astype(np.int64), minlength=parts)[:parts]
+        grouped = k[order].astype(np.uint32)
+        return torch.from_numpy(grouped.view(np.int32)), torch.from_numpy(counts.astype(np.int64)), w, True
+
+    def sort_range(self, keys, key_lo, key_range):
+        k = keys.numpy().view(np.uint32)
+        ok = bool(((k.astype(np.uint64) >= key_lo) & (k.astype(np.uint64) < key_lo + key_range)).all())
+        out = oracle.bitwise_sort(k)
+        ok = ok and bool((out[1:] > out[:-1]).all())
+        return torch.from_numpy(out.view(np.int32)), ok
+
 
 def _free_port():
     s = socket.socket()
@@ -42,7 +61,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, keys, key_range, q):
+def _worker(rank, world, port, keys, key_range, q, variant="rs"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -50,7 +69,8 @@ def _worker(rank, world, port, keys, key_range, q):
         lo, hi = shard_bounds(keys.size, rank, world)
         shard = torch.from_numpy(keys[lo:hi].view(np.int32).copy())
         try:
-            r = distributed_sort(shard, key_range, ops=OracleRankOps())
+            sorter = distributed_sort_a2a if variant == "a2a" else distributed_sort
+            r = sorter(shard, key_range, ops=OracleRankOps())
             q.put((rank, "ok", r.keys.numpy().view(np.uint32).copy(), r.offset, r.total, r.key_lo, r.key_hi))
         except Exception as e:  # noqa: BLE001
             q.put((rank, type(e).__name__, getattr(e, "status", None), str(e), 0, 0, 0))
@@ -58,11 +78,12 @@ def _worker(rank, world, port, keys, key_range, q):
         dist.destroy_process_group()
 
 
-def run_ranks(keys, key_range, world):
+def run_ranks(keys, key_range, world, variant="rs"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, key_range, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, key_range, q, variant))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
@@ -109,3 +130,49 @@ def test_slice_and_shard_arithmetic():
     assert slice_words(1000, 3) == (33, 11)  # 32 words padded to 33
     bounds = [shard_bounds(10, r, 4) for r in range(4)]
     assert bounds == [(0, 2), (2, 5), (5, 7), (7, 10)]
+
+
+@pytest.mark.parametrize("world,key_range,n", [(2, 1 << 20, 100_000), (3, 1000, 1000), (3, 1 << 32, 50_000)])
+def test_distributed_sort_a2a_gloo(world, key_range, n):
+    """Key all-to-all variant: range split, all_to_all_single of the groups,
+    per-rank range sort; same global result as the reduce-scatter variant."""
+    rng = np.random.default_rng(world * 37 + n)
+    if key_range <= 1 << 24:
+        keys = rng.choice(key_range, size=n, replace=False).astype(np.uint32)
+    else:
+        keys = np.unique(rng.integers(0, key_range, size=2 * n, dtype=np.uint64).astype(np.uint32))[:n]
+        rng.shuffle(keys)
+    res = run_ranks(keys, key_range, world, "a2a")
+    w = part_width(key_range, world)
+    parts = []
+    for rank, status, out, offset, total, lo, hi in res:
+        assert status == "ok"
+        assert total == n
+        assert lo == min(rank * w, key_range) and hi == min((rank + 1) * w, key_range)
+        assert offset == sum(p.size for p in parts)
+        assert ((out >= lo) & (out < hi)).all()
+        parts.append(out)
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+
+
+@pytest.mark.parametrize("case", ["cross_rank_duplicate", "out_of_range"])
+def test_distributed_a2a_errors(case):
+    keys = np.arange(0, 2000, 2, dtype=np.uint32)
+    key_range = 1 << 12
+    if case == "cross_rank_duplicate":
+        keys[-1] = keys[0]  # different input shards, same destination rank
+    else:
+        keys[-1] = key_range + 5
+    res = run_ranks(keys, key_range, 2, "a2a")
+    for rank, status, code, msg, *_ in res:
+        assert status == "BitsortError"
+        assert int(code) == 2  # BWS_ERROR_DATA
+
+
+def test_part_width():
+    assert part_width(1 << 32, 8) == 1 << 29
+    assert part_width(1 << 28, 3) == 3 << 25  # 89478486 -> 3 * 2^25 = 100663296
+    assert part_width(1000, 3) == 1 << 12     # minimum width 2^12
+    for m, g in [(1 << 30, 7), (123456789, 5), (1 << 32, 1), ((1 << 32) - 1, 6)]:
+        w = part_width(m, g)
+        assert w * g >= m and w <= 2 * -(-m // g)

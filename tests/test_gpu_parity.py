@@ -382,6 +382,65 @@ def test_rank_building_blocks_emulated(capi, cuda, world, path):
     assert np.array_equal(np.concatenate(parts), np.sort(keys))
 
 
+@pytest.mark.parametrize("world,key_range,n", [(2, (1 << 22) - 7, 200_000), (3, 1 << 32, 300_000),
+                                               (8, 1 << 28, 1 << 22), (5, 1000, 1000)])
+def test_a2a_building_blocks_emulated(capi, cuda, world, key_range, n):
+    """dist.distributed_sort_a2a's per-rank calls on one GPU: range split of
+    every input shard, the all-to-all emulated by concatenating each
+    destination's groups, then each rank's range sort (keys offset by the
+    rank's first key)."""
+    from paper_1312_0138_b200.dist import CudaRankOps, part_width, shard_bounds
+
+    rng = np.random.default_rng(world * 7 + n)
+    if key_range <= 1 << 28:
+        keys = rng.choice(key_range, size=n, replace=False).astype(np.uint32)
+    else:
+        keys = np.unique(rng.integers(0, key_range, size=2 * n, dtype=np.uint64).astype(np.uint32))[:n]
+        rng.shuffle(keys)
+    ops = CudaRankOps()
+    inbox = [[] for _ in range(world)]
+    for r in range(world):
+        lo, hi = shard_bounds(n, r, world)
+        shard = cuda.from_numpy(keys[lo:hi].view(np.int32)).cuda()
+        grouped, counts, w, ok = ops.range_split(shard, key_range, world)
+        assert ok and w == part_width(key_range, world)
+        c = counts.cpu().tolist()
+        assert sum(c) == hi - lo
+        g = grouped[: hi - lo].cpu().numpy().view(np.uint32)
+        start = 0
+        for d in range(world):
+            part = g[start:start + c[d]]
+            assert ((part.astype(np.uint64) >= d * w) & (part.astype(np.uint64) < (d + 1) * w)).all()
+            inbox[d].append(part)
+            start += c[d]
+    parts = []
+    for d in range(world):
+        recv = np.concatenate(inbox[d])
+        key_lo, key_hi = min(d * w, key_range), min((d + 1) * w, key_range)
+        out, ok = ops.sort_range(cuda.from_numpy(recv.view(np.int32)).cuda(), key_lo, max(key_hi - key_lo, 1))
+        assert ok
+        parts.append(out.cpu().numpy().view(np.uint32))
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+
+
+def test_range_sort_rejects(capi, cuda):
+    """Range sort: keys below key_lo or at/after key_lo + key_range, and
+    duplicates, are BWS_ERROR_DATA; a valid offset range sorts exactly."""
+    from paper_1312_0138_b200.dist import CudaRankOps
+
+    ops = CudaRankOps()
+    lo, rng_ = 3 << 28, 1 << 24
+    keys = (np.random.default_rng(2).choice(rng_, size=1 << 21, replace=False) + lo).astype(np.uint32)
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    out, ok = ops.sort_range(t, lo, rng_)
+    assert ok and np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
+    for bad in (lo - 1, lo + rng_, int(keys[7])):
+        k2 = keys.copy()
+        k2[100] = bad
+        _, ok = ops.sort_range(cuda.from_numpy(k2.view(np.int32)).cuda(), lo, rng_)
+        assert not ok
+
+
 # --- full-size BASELINE configs -------------------------------------------
 
 def _config_sort(capi, cuda, name, path="AUTO"):
@@ -443,14 +502,19 @@ def test_c5_clustered_properties(capi, cuda, path):
     assert int(u[0]) == int(keys.min()) and int(u[-1]) == int(keys.max())
 
 
-def test_distributed_sort_nccl_single_rank(capi, cuda):
-    """dist.distributed_sort over a real NCCL process group (world size 1 on
-    the one GPU available): K1+K2 through the C ABI, NCCL reduce-scatter and
-    all-gather, K3 on the slice. Multi-rank host logic is covered on gloo in
+@pytest.mark.parametrize("variant", ["reduce_scatter", "all_to_all"])
+def test_distributed_sort_nccl_single_rank(capi, cuda, variant):
+    """dist.distributed_sort (bitset build, NCCL reduce-scatter, all-gather,
+    K3 on the slice) and dist.distributed_sort_a2a (range split, NCCL
+    all-to-all, range sort) over a real NCCL process group (world size 1 on
+    the one GPU available). Multi-rank host logic is covered on gloo in
     tests/test_dist_gloo.py."""
     import torch.distributed as dist
 
-    from paper_1312_0138_b200.dist import distributed_sort
+    from paper_1312_0138_b200.dist import distributed_sort as rs
+    from paper_1312_0138_b200.dist import distributed_sort_a2a as a2a
+
+    distributed_sort = a2a if variant == "all_to_all" else rs
 
     store = dist.HashStore()
     dist.init_process_group("nccl", store=store, rank=0, world_size=1,
