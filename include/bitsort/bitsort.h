@@ -20,9 +20,10 @@
  * handle (:101-143) entry points are not on the sort path and are not part of
  * this library.
  *
- * Domain of the GPU bws_sort: width 32, unsigned, BWS_ALG_BITWISE (or its
- * BWS_ALG_BITWISE_SKIP_EMPTY variant), DISTINCT keys. Other (width,
- * signedness, algorithm) combinations return BWS_ERROR_CONFIG; duplicate keys
+ * Domain of the GPU bws_sort: width 32, unsigned or signed (int32 keys are
+ * mapped onto the unsigned order by x ^ 0x80000000 on load and store),
+ * BWS_ALG_BITWISE (or its BWS_ALG_BITWISE_SKIP_EMPTY variant), DISTINCT keys.
+ * Other (width, algorithm) combinations return BWS_ERROR_CONFIG; duplicate keys
  * return BWS_ERROR_DATA and leave a host array unmodified. There is no CPU
  * fallback. Additive GPU extensions live in bitsort_gpu.h.
  */

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
         bool all_in = true;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t kk[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            const uint32_t kk[4] = {v[u].x ^ ks.xr, v[u].y ^ ks.xr, v[u].z ^ ks.xr, v[u].w ^ ks.xr};
             all_in &= in[u];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -171,9 +171,10 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
         int ne = c == 0 ? ks.n_head : 0;
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
-                atomicAdd(s_h + bucket_or_spill(extra[i], true, bm, nb), 1u);
-                mx = max(mx, extra[i]);
-                bad += (check && extra[i] - bm.lo >= limit) ? 1u : 0u;
+                const uint32_t e = extra[i] ^ ks.xr;
+                atomicAdd(s_h + bucket_or_spill(e, true, bm, nb), 1u);
+                mx = max(mx, e);
+                bad += (check && e - bm.lo >= limit) ? 1u : 0u;
             }
             extra = c == P - 1 ? ks.tail : nullptr;
             ne = c == P - 1 ? ks.n_tail : 0;
@@ -343,15 +344,16 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         int ne = c == 0 ? ks.n_head : 0;
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < ne; ++i) {
-                const uint32_t b = slot_of(extra[i], true);
+                const uint32_t e = extra[i] ^ ks.xr;
+                const uint32_t b = slot_of(e, true);
                 if constexpr (SLAB) {
-                    bad += (sa.check && extra[i] - bm.lo >= sa.limit) ? 1u : 0u;
+                    bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
                         const uint32_t pos = atomicAdd(sa.gcnt + b, 1u);
-                        if (pos < sa.cap) parted[b * sa.cap + pos] = extra[i];
+                        if (pos < sa.cap) parted[b * sa.cap + pos] = e;
                     }
                 } else {
-                    if (b != spill) parted[s_cur[b]++] = extra[i];
+                    if (b != spill) parted[s_cur[b]++] = e;
                 }
             }
             extra = c == P - 1 ? ks.tail : nullptr;
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             const bool in = vi < nvec;
             all_in &= in;
             const uint4 v = in ? reinterpret_cast<const uint4*>(buf)[vi] : make_uint4(0, 0, 0, 0);
-            const uint32_t kk[4] = {v.x, v.y, v.z, v.w};
+            const uint32_t kk[4] = {v.x ^ ks.xr, v.y ^ ks.xr, v.z ^ ks.xr, v.w ^ ks.xr};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 k[4 * j + q] = kk[q];
@@ -782,7 +784,9 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         }
         __syncthreads();
         uint32_t* o = out + base + s_warp[warp];
-        const uint32_t key_hi = bm.lo + static_cast<uint32_t>(b) * bm.width;
+        // output keys: bucket base + bit index, mapped back by the XOR (signed sorts use
+        // power-of-two widths, so no bucket straddles 2^31 and the XOR commutes with the add)
+        const uint32_t key_hi = (bm.lo + static_cast<uint32_t>(b) * bm.width) ^ bm.xr;
         if (sparse) {
             // lane-major over summary words: lane owns 32 consecutive bitset
             // words (one summary word) per round; its keys are contiguous in
@@ -1143,11 +1147,12 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
 }
 
 // K0: max key (only when no key-range hint is given).
-__global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl* __restrict__ ctrl) {
+__global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl* __restrict__ ctrl,
+                               uint32_t xr) {
     uint32_t mx = 0;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
-        mx = max(mx, __ldcs(keys + i));
+        mx = max(mx, __ldcs(keys + i) ^ xr);
     mx = __reduce_max_sync(kFull, mx);
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(&ctrl->max_key, mx);
 }
@@ -1220,8 +1225,8 @@ static bool narrow_partition(const BucketPlan& plan) {
 }
 
 cudaError_t launch_key_max(const uint32_t* keys, size_t n, Ctrl* ctrl, const LaunchGeometry& geo,
-                           cudaStream_t stream) {
-    key_max_kernel<<<geo.fill_blocks, 256, 0, stream>>>(keys, n, ctrl);
+                           cudaStream_t stream, uint32_t xr) {
+    key_max_kernel<<<geo.fill_blocks, 256, 0, stream>>>(keys, n, ctrl, xr);
     return cudaGetLastError();
 }
 
@@ -1371,6 +1376,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     ks.n_head = static_cast<int>(n_head);
     ks.tail = keys + n_head + 4 * ks.nv;
     ks.n_tail = static_cast<int>(n - n_head - 4 * ks.nv);
+    ks.xr = plan.map.xr;
 
     const uint64_t slab = slab_slots(plan, n);
     const bool use_slab = slab != 0 && slab <= parted_cap;
@@ -1420,7 +1426,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (timer) timer->before(stream);
         // xwide measured slightly slower (C4 KB3 121 vs 112 us, C5 1576 vs 1535 us):
         // opt-in only (BITSORT_XWIDE=1)
-        if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE"))
+        if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE") && !ks.xr)
             bucket_partition_xwide_kernel<<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
                 ks, plan.map, plan.nb, H, tot, parted, base);
         else if (narrow_partition(plan))

@@ -467,12 +467,14 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
 
 // Bucketed pipeline: [K0 max + host readback when no hint] -> KB1..KB4.
 // Leaves the cached bitset untouched.
+// key_lo: keys lie in [key_lo, key_lo + key_range) (range sorts). xr: keys
+// are XORed with it on load and store (signed int32 sorts: 0x80000000).
 void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
-                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0) {
+                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0) {
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
     cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
     if (key_range == 0) {
-        cuda_check(bws_gpu::launch_key_max(keys, count, ctx.ctrl(), ctx.geo, stream), "key_max launch");
+        cuda_check(bws_gpu::launch_key_max(keys, count, ctx.ctrl(), ctx.geo, stream, xr), "key_max launch");
         g_launches.fetch_add(1);
         unsigned int mx = 0;
         cuda_check(cudaMemcpyAsync(&mx, &ctx.ctrl()->max_key, sizeof(mx), cudaMemcpyDeviceToHost, stream),
@@ -480,8 +482,12 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
         cuda_check(cudaStreamSynchronize(stream), "key_max execution");
         key_range = static_cast<uint64_t>(mx) + 1;
     }
-    bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
+    // signed sorts keep power-of-two bucket widths (the output XOR then
+    // commutes with the in-bucket offsets) and no cluster plan
+    bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(
+        key_range, xr ? 0 : ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT], /*allow_cluster=*/xr == 0);
     plan.map.lo = key_lo;
+    plan.map.xr = xr;
     const size_t parted_cap = ctx.ensure_parted(count, plan);
     int launches = 0;
     cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
@@ -573,7 +579,7 @@ void stage_to_host(DeviceCtx& ctx, void* host, const void* dev, size_t bytes) {
 // owning `data` when it is device memory). Host arrays are staged through the
 // context's device buffer; they are written back only after validation, so a
 // rejected input is left untouched.
-void sort_u32(void* data, size_t count, uint64_t key_range) {
+void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0) {
     check_range(key_range);
     if (count == 0) return;
     visible_devices();
@@ -601,8 +607,17 @@ void sort_u32(void* data, size_t count, uint64_t key_range) {
     } restore{prev};
     ctx.init(device);
     uint32_t* keys = static_cast<uint32_t*>(data);
+    // signed keys (xr) always take the bucketed pipeline, which applies the XOR
+    auto enqueue = [&](const uint32_t* in, uint32_t* out) {
+        if (xr) {
+            if (count >= (size_t(1) << 32)) throw std::out_of_range("signed sorts take fewer than 2^32 keys");
+            enqueue_bucketed(ctx, in, count, out, key_range, ctx.stream, 0, xr);
+        } else {
+            enqueue_sort(ctx, in, count, out, key_range, ctx.stream);
+        }
+    };
     if (on_device) {
-        enqueue_sort(ctx, keys, count, keys, key_range, ctx.stream);
+        enqueue(keys, keys);
         validate(ctx, count, key_range, ctx.stream);
         return;
     }
@@ -615,7 +630,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range) {
     } else {
         stage_to_device(ctx, ctx.keys, data, bytes);
     }
-    enqueue_sort(ctx, ctx.keys, count, ctx.keys, key_range, ctx.stream);
+    enqueue(ctx.keys, ctx.keys);
     validate(ctx, count, key_range, ctx.stream);
     if (pinned) {
         cuda_check(cudaMemcpyAsync(data, ctx.keys, bytes, cudaMemcpyDeviceToHost, ctx.stream),
@@ -679,10 +694,13 @@ bws_status bws_sort(void* data, size_t count, uint32_t width, int is_unsigned,
         if (algorithm != BWS_ALG_BITWISE && algorithm != BWS_ALG_BITWISE_SKIP_EMPTY)
             throw config_error(std::string("algorithm '") + algorithm_name_of(algorithm) +
                                "' is not provided by the B200 build (bitwise only)");
-        if (width != 32 || is_unsigned == 0)
-            throw config_error("the B200 bitset sort supports width 32 unsigned keys only (got width " +
-                               std::to_string(width) + (is_unsigned ? " unsigned)" : " signed)"));
-        sort_u32(data, count, 0);
+        if (width != 32)
+            throw config_error("the B200 bitset sort supports width 32 keys only (got width " +
+                               std::to_string(width) + ")");
+        // signed int32: x ^ 0x80000000 maps the signed order onto the unsigned
+        // one (the reference splits negatives and non-negatives instead,
+        // bitsort.hpp:131-152); the same XOR maps the sorted keys back
+        sort_u32(data, count, 0, is_unsigned ? 0u : 0x80000000u);
     });
 }
 

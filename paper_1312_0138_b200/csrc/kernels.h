@@ -104,6 +104,8 @@ struct KeySplit {
     int n_head = 0;
     const std::uint32_t* tail = nullptr;
     int n_tail = 0;
+    std::uint32_t xr = 0;  // keys are XORed with this on load (signed int32: 0x80000000 maps
+                           // the signed order onto the unsigned one)
 };
 
 // Bucket of a key: floor(key / width), width = q * 2^ms with q <= 8, computed
@@ -115,6 +117,7 @@ struct BucketMap {
     std::uint32_t mq = 1u << 20;
     std::uint32_t width = 1u << 20;  // keys per bucket
     std::uint32_t lo = 0;            // first key of bucket 0 (range sorts); key - lo is bucketed
+    std::uint32_t xr = 0;            // output keys are XORed with this (signed sorts: 0x80000000)
 };
 
 struct BucketPlan {
@@ -214,6 +217,6 @@ cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::ui
                                std::uint64_t parted_cap = 0);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
-                           const LaunchGeometry& geo, cudaStream_t stream);
+                           const LaunchGeometry& geo, cudaStream_t stream, std::uint32_t xr = 0);
 
 }  // namespace bws_gpu

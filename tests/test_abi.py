@@ -94,7 +94,6 @@ def test_config_errors():
     assert "unsupported width 24" in capi.last_error()
     assert capi.sort_raw(p, 3, 32, 1, 99) == capi.Status.ERROR_CONFIG  # capi.cpp:69
     assert "unknown algorithm id" in capi.last_error()
-    assert capi.sort_raw(p, 3, 32, 0, 0) == capi.Status.ERROR_CONFIG  # signed: not on the GPU path
     assert capi.sort_raw(p, 3, 16, 1, 0) == capi.Status.ERROR_CONFIG
     for alg in (capi.Algorithm.INSERTION, capi.Algorithm.MERGE, capi.Algorithm.COUNTING,
                 capi.Algorithm.PLATFORM):
@@ -144,3 +143,7 @@ def test_no_cpu_fallback():
     assert capi.sort_raw(a.ctypes.data, 3, 32, 1, 0) == capi.Status.ERROR_INTERNAL
     assert "no CPU fallback" in capi.last_error()
     assert a.tolist() == [3, 1, 2]
+    s = np.array([3, -1, 2], dtype=np.int32)  # signed int32 goes to the GPU too
+    assert capi.sort_raw(s.ctypes.data, 3, 32, 0, 0) == capi.Status.ERROR_INTERNAL
+    assert "no CPU fallback" in capi.last_error()
+    assert s.tolist() == [3, -1, 2]

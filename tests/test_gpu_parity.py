@@ -99,7 +99,7 @@ def test_status_conventions(capi, path):
     assert capi.last_error() == ""
     assert b.tolist() == [1, 2, 3]
     assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.BITWISE_SKIP_EMPTY) == capi.Status.OK
-    assert capi.sort_raw(b.ctypes.data, 3, 32, 0, 0) == capi.Status.ERROR_CONFIG
+    assert capi.sort_raw(b.ctypes.data, 3, 16, 1, 0) == capi.Status.ERROR_CONFIG
     assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.PLATFORM) == capi.Status.ERROR_CONFIG
 
 
@@ -211,6 +211,56 @@ def test_duplicates_rejected_at_scale(capi, path):
     a = keys.copy()
     assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.ERROR_DATA
     assert np.array_equal(a, keys)
+
+
+# --- signed int32 (x ^ 0x80000000 on load and store, bucketed pipeline) ----
+
+def _reference_signed(keys: np.ndarray) -> np.ndarray:
+    import oracle
+
+    a = keys.copy()
+    if oracle.REFERENCE is not None:  # the reference's own signed bitwise sort
+        assert oracle.REFERENCE.bws_sort(a.ctypes.data, a.size, 32, 0, 0) == 0
+        return a
+    return np.sort(a)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 1000, 65537, 1 << 21])
+def test_signed_int32(capi, cuda, n):
+    rng = np.random.default_rng(n + 99)
+    keys = np.unique(rng.integers(-(1 << 31), 1 << 31, size=n + n // 4 + 8, dtype=np.int64)).astype(np.int32)
+    keys = rng.permutation(keys)[:n]
+    if n >= 5:
+        keys[:4] = [-(1 << 31), -1, 0, (1 << 31) - 1]
+        keys = np.unique(keys)
+        rng.shuffle(keys)
+    expected = _reference_signed(keys)
+    assert np.array_equal(expected, np.sort(keys))
+    a = keys.copy()
+    assert capi.sort_raw(a.ctypes.data, a.size, 32, 0, capi.Algorithm.BITWISE) == capi.Status.OK, capi.last_error()
+    assert np.array_equal(a, expected)
+    t = cuda.from_numpy(keys.copy()).cuda()  # device pointer, in place
+    assert capi.sort_raw(t.data_ptr(), t.numel(), 32, 0, capi.Algorithm.BITWISE) == capi.Status.OK
+    assert np.array_equal(t.cpu().numpy(), expected)
+
+
+@pytest.mark.parametrize("kind", ["all_negative", "dense_window", "duplicate"])
+def test_signed_int32_layouts(capi, kind):
+    rng = np.random.default_rng(5)
+    if kind == "all_negative":
+        keys = -(rng.choice(1 << 30, size=1 << 20, replace=False).astype(np.int64) + 1)
+    else:  # a dense window straddling zero (both signs, consecutive keys)
+        keys = np.arange(-(1 << 20), 1 << 20, dtype=np.int64)
+    keys = rng.permutation(keys).astype(np.int32)
+    if kind == "duplicate":
+        keys[10] = keys[12345]
+        a = keys.copy()
+        assert capi.sort_raw(a.ctypes.data, a.size, 32, 0, 0) == capi.Status.ERROR_DATA
+        assert np.array_equal(a, keys)
+        return
+    a = keys.copy()
+    assert capi.sort_raw(a.ctypes.data, a.size, 32, 0, 0) == capi.Status.OK
+    assert np.array_equal(a, np.sort(keys))
 
 
 # --- slab layout of the bucket buffer (KB3 fill counters, no KB1/KB2) -------
