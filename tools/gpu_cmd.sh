@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+timeout 900 python tools/bench_ladder.py --out gpurun_out/r01_gpu_ladder > gpurun_out/ladder.log 2>&1; echo exit=$? >> gpurun_out/ladder.log
