@@ -537,6 +537,28 @@ def test_c3_dense_permutation(capi, cuda, path):
     assert cuda.equal(out, cuda.arange(cfg.n, dtype=cuda.int32, device="cuda"))
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("path", PATHS)
+def test_more_than_2_31_keys(capi, cuda, path):
+    """n = 2^31 + 5 keys (a permutation of [0, n), n not a power of two): 64-bit
+    sizes and offsets everywhere, 32-bit bucket slots still in range; the
+    output must be the identity."""
+    from paper_1312_0138_b200 import datagen
+
+    capi.set_path(getattr(capi.Path, path))
+    n = (1 << 31) + 5
+    keys = datagen.permutation(n, seed=3)
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    del keys
+    out = cuda.empty_like(t)
+    stream = cuda.cuda.current_stream().cuda_stream
+    capi.sort_device_async(t.data_ptr(), n, out.data_ptr(), n, stream)
+    assert capi.sort_check(stream) == n
+    del t
+    ref = cuda.arange(n, dtype=cuda.int64, device="cuda").to(cuda.int32)  # wraps like uint32
+    assert cuda.equal(out, ref)
+
+
 @pytest.mark.parametrize("path", PATHS)
 def test_c5_clustered_properties(capi, cuda, path):
     """Size-independent properties: strictly ascending, same count, and the same

@@ -1,1 +1,1 @@
-timeout 900 python tools/bench_ladder.py --out gpurun_out/r01_gpu_ladder > gpurun_out/ladder.log 2>&1; echo exit=$? >> gpurun_out/ladder.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "more_than" > gpurun_out/pytest_big.log 2>&1; echo exit=$? >> gpurun_out/pytest_big.log
