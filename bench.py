@@ -55,6 +55,8 @@ def parse_args():
                     help="run the multi-GPU (NCCL reduce-scatter) path even with one rank")
     ap.add_argument("--a2a", action="store_true",
                     help="multi-GPU key all-to-all variant (range split + NCCL all-to-all + range sort)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="multi-GPU peer-to-peer variant (CUDA IPC OR-gather instead of the NCCL reduce-scatter)")
     return ap.parse_args()
 
 
@@ -259,7 +261,7 @@ def run_ours(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    use_dist = world > 1 or args.dist or args.a2a
+    use_dist = world > 1 or args.dist or args.a2a or args.p2p
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
@@ -274,8 +276,9 @@ def run_ours(args, cfg):
         from paper_1312_0138_b200.dist import CudaRankOps, shard_bounds
         from paper_1312_0138_b200.dist import distributed_sort as dist_rs
         from paper_1312_0138_b200.dist import distributed_sort_a2a as dist_a2a
+        from paper_1312_0138_b200.dist import distributed_sort_p2p as dist_p2p
 
-        distributed_sort = dist_a2a if args.a2a else dist_rs
+        distributed_sort = dist_a2a if args.a2a else (dist_p2p if args.p2p else dist_rs)
 
         lo, hi = shard_bounds(n_total, rank, world)
         shard_h = keys_h[lo:hi]
@@ -457,7 +460,9 @@ def run_ours(args, cfg):
                    "l2": "flushed between steps (256 MiB write, outside the step events)",
                    "path": args.path,
                    "parallelism": (f"key shards x{world} + " + ("NCCL all-to-all of range-split keys"
-                                                                  if args.a2a else "NCCL reduce-scatter"))
+                                                                  if args.a2a else
+                                                                  "CUDA IPC OR-gather" if args.p2p else
+                                                                  "NCCL reduce-scatter"))
                    if use_dist else "single GPU"},
         "step_ms": {"median": round(statistics.median(step_ms), 4), "best": round(min(step_ms), 4),
                     "worst": round(max(step_ms), 4)},

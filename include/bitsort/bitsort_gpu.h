@@ -73,6 +73,24 @@ BITSORT_API bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_word
                                            uint64_t out_capacity, uint64_t* d_total,
                                            void* stream);
 
+/* Peer-to-peer replacement of the reduce-scatter (one process per GPU on an
+ * NVLink/NVSwitch node): every rank exports its full bitset with
+ * bws_gpu_ipc_get_handle, opens the peers' with bws_gpu_ipc_open, and after a
+ * cross-rank barrier ORs the words of its own slice from all nsrc (<= 8)
+ * bitsets into `dst` with bws_gpu_bitset_or_gather (`srcs` is a host array of
+ * device pointers, each already offset to the slice; peer pointers read over
+ * NVLink). OR equals the SUM of the reduce-scatter on distinct keys and loses
+ * bits on duplicates, which the popcount total then reports. */
+#define BWS_GPU_IPC_HANDLE_BYTES 64
+BITSORT_API bws_status bws_gpu_bitset_or_gather(const uint32_t* const* srcs, int nsrc, uint64_t n_words,
+                                                uint32_t* dst, void* stream);
+/* handle_out: BWS_GPU_IPC_HANDLE_BYTES bytes naming dev_ptr's allocation;
+ * *offset_out: dev_ptr's byte offset in it (add it to the pointer
+ * bws_gpu_ipc_open returns in the peer process). */
+BITSORT_API bws_status bws_gpu_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
+BITSORT_API bws_status bws_gpu_ipc_open(const void* handle, void** dev_ptr_out);
+BITSORT_API bws_status bws_gpu_ipc_close(void* dev_ptr);
+
 /* Scatter-kernel staging switches (tests / ablations; default BWS_SCATTER_AUTO). */
 typedef enum bws_scatter_mode {
     BWS_SCATTER_AUTO = 0,      /* per tile: SMEM staging if the tile's span fits, else

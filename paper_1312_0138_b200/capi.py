@@ -89,6 +89,10 @@ def _load() -> ctypes.CDLL:
         "bws_gpu_sort_check": (i32, [vp, ctypes.POINTER(u64)]),
         "bws_gpu_sort_range_device_async": (i32, [vp, sz, vp, u32, u64, vp]),
         "bws_gpu_range_split": (i32, [vp, sz, u64, i32, vp, vp, ctypes.POINTER(u64), vp]),
+        "bws_gpu_bitset_or_gather": (i32, [ctypes.POINTER(vp), i32, u64, vp, vp]),
+        "bws_gpu_ipc_get_handle": (i32, [vp, vp, ctypes.POINTER(u64)]),
+        "bws_gpu_ipc_open": (i32, [vp, ctypes.POINTER(vp)]),
+        "bws_gpu_ipc_close": (i32, [vp]),
         "bws_gpu_bitset_build": (i32, [vp, sz, vp, u64, vp]),
         "bws_gpu_bitset_scan": (i32, [vp, u64, u32, vp, u64, vp, vp]),
         "bws_gpu_set_scatter_mode": (i32, [i32]),
@@ -114,6 +118,7 @@ EXPORTED = (
     "bws_version", "bws_last_error", "bws_algorithm_name", "bws_algorithm_from_name",
     "bws_sort", "bws_sort_u32_range", "bws_gpu_sort_device_async", "bws_gpu_sort_check",
     "bws_gpu_sort_range_device_async", "bws_gpu_range_split",
+    "bws_gpu_bitset_or_gather", "bws_gpu_ipc_get_handle", "bws_gpu_ipc_open", "bws_gpu_ipc_close",
     "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode", "bws_gpu_set_path",
     "bws_gpu_set_device_count", "bws_gpu_device_count", "bws_gpu_launch_count",
     "bws_gpu_set_kernel_timing", "bws_gpu_kernel_timings",
@@ -209,6 +214,33 @@ def bitset_scan(bits_ptr: int, n_words: int, key_base: int, out_ptr: int, out_ca
                 d_total_ptr: int, stream: int = 0) -> None:
     _check(lib.bws_gpu_bitset_scan(bits_ptr, n_words, key_base, out_ptr, out_capacity,
                                    d_total_ptr, stream or None))
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def bitset_or_gather(src_ptrs, n_words: int, dst_ptr: int, stream: int = 0) -> None:
+    """dst[i] = OR of src[i] over the (local or peer) device pointers src_ptrs."""
+    arr = (ctypes.c_void_p * len(src_ptrs))(*src_ptrs)
+    _check(lib.bws_gpu_bitset_or_gather(arr, len(src_ptrs), n_words, dst_ptr, stream or None))
+
+
+def ipc_get_handle(dev_ptr: int) -> tuple[bytes, int]:
+    """(handle of dev_ptr's allocation, dev_ptr's offset in it)."""
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    off = ctypes.c_uint64(0)
+    _check(lib.bws_gpu_ipc_get_handle(dev_ptr, buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    out = ctypes.c_void_p(0)
+    _check(lib.bws_gpu_ipc_open(ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES), ctypes.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(dev_ptr: int) -> None:
+    _check(lib.bws_gpu_ipc_close(dev_ptr))
 
 
 def set_scatter_mode(mode: int) -> None:

@@ -14,6 +14,7 @@
 // consumes), the K3 control block + tile-status array, a key staging buffer for
 // host arrays and an internal stream. Calls on one device are serialised by the
 // context mutex; calls on different devices run concurrently.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -794,6 +795,71 @@ bws_status bws_gpu_range_split(const uint32_t* keys, size_t count, uint64_t key_
         }
         cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
     });
+}
+
+bws_status bws_gpu_bitset_or_gather(const uint32_t* const* srcs, int nsrc, uint64_t n_words,
+                                    uint32_t* dst, void* stream) {
+    return wrap([&] {
+        if (nsrc < 1 || nsrc > bws_gpu::MAX_OR_SOURCES) throw std::out_of_range("nsrc must be in [1, 8]");
+        if (n_words > 0 && (srcs == nullptr || dst == nullptr)) throw data_error("null pointer");
+        bws_gpu::OrSources os{};
+        os.n = nsrc;
+        for (int s = 0; s < nsrc; ++s) {
+            if (n_words > 0 && srcs[s] == nullptr) throw data_error("null source pointer");
+            os.p[s] = srcs[s];
+        }
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cuda_check(timed_launch("bitset_or_gather", s,
+                                [&] { return bws_gpu::launch_or_gather(os, dst, n_words, ctx.geo, s); }),
+                   "or_gather launch");
+        g_launches.fetch_add(1);
+    });
+}
+
+bws_status bws_gpu_ipc_get_handle(const void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+    return wrap([&] {
+        if (dev_ptr == nullptr || handle_out == nullptr || offset_out == nullptr) throw data_error("null pointer");
+        static_assert(sizeof(cudaIpcMemHandle_t) == BWS_GPU_IPC_HANDLE_BYTES, "IPC handle size");
+        // the handle names the whole allocation (e.g. a caching allocator's
+        // segment): report dev_ptr's offset inside it (driver entry point, so
+        // the library needs no libcuda link)
+        using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static GetRange get_range = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<GetRange>(fn);
+        }();
+        if (get_range == nullptr) throw std::runtime_error("cuMemGetAddressRange is unavailable");
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+            throw std::runtime_error("cuMemGetAddressRange failed (not device memory?)");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+        std::memcpy(handle_out, &h, sizeof(h));
+        *offset_out = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+    });
+}
+
+bws_status bws_gpu_ipc_open(const void* handle, void** dev_ptr_out) {
+    return wrap([&] {
+        if (handle == nullptr || dev_ptr_out == nullptr) throw data_error("null pointer");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        cuda_check(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess),
+                   "cudaIpcOpenMemHandle");
+    });
+}
+
+bws_status bws_gpu_ipc_close(void* dev_ptr) {
+    return wrap([&] { cuda_check(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle"); });
 }
 
 bws_status bws_gpu_sort_check(void* stream, uint64_t* distinct_out) {

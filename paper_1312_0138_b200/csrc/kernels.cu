@@ -397,6 +397,52 @@ cudaError_t launch_scatter(const uint32_t* keys, size_t n, uint32_t* bits, uint6
                                       static_cast<int>(n_tail), bits, limit, ctrl, blocks, stream);
 }
 
+// OR-gather of up to 8 bitset slices (local and peer memory): 16-byte loads
+// from every source in flight before the OR, streaming store. Distinct keys
+// set disjoint bits, so OR equals the reduce-scatter's SUM; duplicates across
+// ranks lose bits either way and the popcount total exposes them.
+__global__ void __launch_bounds__(256)
+    or_gather_kernel(OrSources srcs, uint32_t* __restrict__ dst, unsigned long long n_words) {
+    const unsigned long long nv = n_words / 4;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && [&] {
+        for (int s = 0; s < srcs.n; ++s)
+            if (reinterpret_cast<uintptr_t>(srcs.p[s]) & 15) return false;
+        return true;
+    }();
+    if (aligned) {
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+            uint4 v[MAX_OR_SOURCES];
+#pragma unroll
+            for (int s = 0; s < MAX_OR_SOURCES; ++s)
+                if (s < srcs.n) v[s] = __ldcs(reinterpret_cast<const uint4*>(srcs.p[s]) + i);
+            uint4 r = v[0];
+#pragma unroll
+            for (int s = 1; s < MAX_OR_SOURCES; ++s)
+                if (s < srcs.n) {
+                    r.x |= v[s].x;
+                    r.y |= v[s].y;
+                    r.z |= v[s].z;
+                    r.w |= v[s].w;
+                }
+            __stcs(reinterpret_cast<uint4*>(dst) + i, r);
+        }
+    }
+    for (unsigned long long i = (aligned ? 4 * nv : 0) + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+         i < n_words; i += stride) {
+        uint32_t r = 0;
+        for (int s = 0; s < srcs.n; ++s) r |= srcs.p[s][i];
+        dst[i] = r;
+    }
+}
+
+cudaError_t launch_or_gather(const OrSources& srcs, uint32_t* dst, uint64_t n_words,
+                             const LaunchGeometry& geo, cudaStream_t stream) {
+    if (n_words == 0) return cudaSuccess;
+    or_gather_kernel<<<geo.fill_blocks, 256, 0, stream>>>(srcs, dst, n_words);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scan(const uint32_t* bits, uint64_t n_words, uint32_t key_base, uint32_t* out,
                         uint64_t out_capacity, Ctrl* ctrl, unsigned long long* status,
                         unsigned long long* d_total, int clear, const LaunchGeometry& geo,

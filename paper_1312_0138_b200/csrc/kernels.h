@@ -215,6 +215,16 @@ cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::ui
                                cudaStream_t stream, int* launches, KernelTimer* timer = nullptr,
                                std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0,
                                std::uint64_t parted_cap = 0);
+// Multi-GPU OR-gather (the P2P replacement of the reduce-scatter): dst[i] =
+// OR over s of srcs.p[s][i] for i < n_words; srcs may point into peer GPUs'
+// memory (CUDA IPC over NVLink/NVSwitch).
+constexpr int MAX_OR_SOURCES = 8;
+struct OrSources {
+    const std::uint32_t* p[MAX_OR_SOURCES];
+    int n;
+};
+cudaError_t launch_or_gather(const OrSources& srcs, std::uint32_t* dst, std::uint64_t n_words,
+                             const LaunchGeometry& geo, cudaStream_t stream);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream, std::uint32_t xr = 0);

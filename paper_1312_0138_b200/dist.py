@@ -11,6 +11,12 @@ Rank r of G holds an input-position shard of the keys. Each rank
      so the total only drops) -> BWS_ERROR_DATA.
 The global sorted array is the rank-order concatenation of the local outputs.
 
+Peer-to-peer variant (``distributed_sort_p2p``, NVLink/NVSwitch node): step 2
+is a custom collective instead of NCCL — every rank exports its full bitset
+through CUDA IPC, and after a cross-rank barrier ORs its own slice of all G
+bitsets straight out of the peers' memory (bws_gpu_bitset_or_gather), then
+scans it. OR is exact on distinct keys and only loses bits on duplicates.
+
 Key all-to-all variant (``distributed_sort_a2a``): rank r
 splits its shard by destination key range (range split, C ABI), the ranks
 exchange the groups with one all-to-all (4n/G bytes per rank instead of the
@@ -46,6 +52,16 @@ class RankOps(Protocol):
     def sort_range(self, keys: torch.Tensor, key_lo: int, key_range: int):
         """(sorted keys, ok) for keys in [key_lo, key_lo + key_range); ok is
         False on duplicates or keys outside the range."""
+
+    def export_bitset(self, bits: torch.Tensor):
+        """A picklable handle other ranks can open to read ``bits``."""
+
+    def import_peer(self, rank: int, handle):
+        """Source for or_gather of the bitset behind another rank's handle."""
+
+    def or_gather(self, sources, word_lo: int, n_words: int) -> torch.Tensor:
+        """OR of words [word_lo, word_lo + n_words) over all sources (local
+        tensor or imported peers)."""
 
 
 @dataclass
@@ -133,6 +149,29 @@ class CudaRankOps:
         except self._capi.BitsortError:
             return out, False
         return out, True
+
+    def export_bitset(self, bits: torch.Tensor):
+        return self._capi.ipc_get_handle(bits.data_ptr())
+
+    def import_peer(self, rank: int, handle):
+        raw, offset = handle
+        cache = self.__dict__.setdefault("_peers", {})
+        old = cache.get(rank)
+        if old is None or old[0] != raw:  # a new allocation behind the peer's bitset
+            if old is not None:
+                self._capi.ipc_close(old[1])
+            cache[rank] = (raw, self._capi.ipc_open(raw))
+        return cache[rank][1] + offset
+
+    def or_gather(self, sources, word_lo: int, n_words: int) -> torch.Tensor:
+        ptrs = [(src.data_ptr() if isinstance(src, torch.Tensor) else int(src)) + 4 * word_lo
+                for src in sources]
+        buf = self.__dict__.get("_slice")
+        if buf is None or buf.numel() < n_words:
+            buf = torch.empty(max(n_words, 1), dtype=torch.int32, device=self.device)
+            self._slice = buf
+        self._capi.bitset_or_gather(ptrs, n_words, buf.data_ptr(), self._stream())
+        return buf[:n_words]
 
     def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int):
         if self._out is None or self._out.numel() < capacity:
@@ -232,6 +271,51 @@ def distributed_sort_a2a(keys: torch.Tensor, key_range: int, n_total: Optional[i
     if errors or total != n_total:
         raise _data_error(f"keys are not distinct: {n_total} keys, duplicates within "
                           f"{errors} rank range(s)")
+    count = counts_h[rank]
+    return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
+                       key_lo=key_lo, key_hi=key_hi)
+
+
+def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[int] = None,
+                         ops: Optional[RankOps] = None, group=None) -> SliceResult:
+    """:func:`distributed_sort` with the reduce-scatter replaced by a
+    peer-to-peer OR-gather over CUDA IPC (same result layout)."""
+    if not 0 < key_range <= 1 << 32:
+        raise ValueError("key_range must be in [1, 2^32]")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ops = ops or CudaRankOps(keys.device)
+    dev = keys.device
+    words, per = slice_words(key_range, world)
+    if n_total is None:
+        t = torch.tensor([keys.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, group=group)
+        n_total = int(t.item())
+
+    bits = ops.bitset_build(keys, key_range, words)
+    if world == 1:
+        slice_ = bits[:per]
+    else:
+        handles = [None] * world
+        dist.all_gather_object(handles, ops.export_bitset(bits), group=group)
+        sources = [bits if r == rank else ops.import_peer(r, h) for r, h in enumerate(handles)]
+        # stream-ordered barrier: this rank's collective completes only after
+        # every rank's build (enqueued before its collective) has finished
+        fence = torch.zeros(1, dtype=torch.int32, device=dev)
+        dist.all_reduce(fence, group=group)
+        slice_ = ops.or_gather(sources, rank * per, per)
+
+    key_lo = rank * per * 32
+    key_hi = min((rank + 1) * per * 32, key_range)
+    capacity = max(0, min(n_total, key_hi - key_lo))
+    out, count_t = ops.bitset_scan(slice_, key_lo, capacity)
+    # the counts' all-gather doubles as the "peers are done reading" barrier
+    counts = [torch.empty_like(count_t) for _ in range(world)]
+    dist.all_gather(counts, count_t, group=group)
+    counts_h = [int(c.item()) for c in counts]
+    total = sum(counts_h)
+    if total != n_total:
+        raise _data_error(f"keys are not distinct or out of range: {n_total} keys, {total} distinct")
     count = counts_h[rank]
     return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
                        key_lo=key_lo, key_hi=key_hi)

@@ -17,8 +17,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1312_0138_b200.dist import (distributed_sort, distributed_sort_a2a, part_width,
-                                       shard_bounds, slice_words)
+from paper_1312_0138_b200.dist import (distributed_sort, distributed_sort_a2a, distributed_sort_p2p,
+                                       part_width, shard_bounds, slice_words)
 
 
 class OracleRankOps:
@@ -45,6 +45,25 @@ class OracleRankOps:
         grouped = k[order].astype(np.uint32)
         return torch.from_numpy(grouped.view(np.int32)), torch.from_numpy(counts.astype(np.int64)), w, True
 
+    # p2p variant: a rank "exports" its bitset as a file the other ranks map
+    # read-only (the CUDA build exports a CUDA IPC handle)
+    def export_bitset(self, bits):
+        import tempfile
+
+        fd, path = tempfile.mkstemp(prefix="bws_p2p_", suffix=".u32")
+        os.close(fd)
+        bits.numpy().view(np.uint32).tofile(path)
+        return path
+
+    def import_peer(self, rank, handle):
+        return torch.from_numpy(np.fromfile(handle, dtype=np.uint32).view(np.int32))
+
+    def or_gather(self, sources, word_lo, n_words):
+        acc = np.zeros(n_words, dtype=np.uint32)
+        for src in sources:
+            acc |= src.numpy().view(np.uint32)[word_lo:word_lo + n_words]
+        return torch.from_numpy(acc.view(np.int32))
+
     def sort_range(self, keys, key_lo, key_range):
         k = keys.numpy().view(np.uint32)
         ok = bool(((k.astype(np.uint64) >= key_lo) & (k.astype(np.uint64) < key_lo + key_range)).all())
@@ -69,7 +88,7 @@ def _worker(rank, world, port, keys, key_range, q, variant="rs"):
         lo, hi = shard_bounds(keys.size, rank, world)
         shard = torch.from_numpy(keys[lo:hi].view(np.int32).copy())
         try:
-            sorter = distributed_sort_a2a if variant == "a2a" else distributed_sort
+            sorter = {"a2a": distributed_sort_a2a, "p2p": distributed_sort_p2p}.get(variant, distributed_sort)
             r = sorter(shard, key_range, ops=OracleRankOps())
             q.put((rank, "ok", r.keys.numpy().view(np.uint32).copy(), r.offset, r.total, r.key_lo, r.key_hi))
         except Exception as e:  # noqa: BLE001
@@ -176,3 +195,27 @@ def test_part_width():
     for m, g in [(1 << 30, 7), (123456789, 5), (1 << 32, 1), ((1 << 32) - 1, 6)]:
         w = part_width(m, g)
         assert w * g >= m and w <= 2 * -(-m // g)
+
+
+@pytest.mark.parametrize("world,key_range,n", [(2, 1 << 20, 100_000), (3, 1000, 1000)])
+def test_distributed_sort_p2p_gloo(world, key_range, n):
+    """Peer-to-peer variant: handle exchange (all_gather_object), the fence,
+    each rank's OR-gather of its slice from every rank's bitset, the scan and
+    the offsets; same layout as the reduce-scatter variant."""
+    keys = np.random.default_rng(world * 41 + n).choice(key_range, size=n, replace=False).astype(np.uint32)
+    res = run_ranks(keys, key_range, world, "p2p")
+    words, per = slice_words(key_range, world)
+    parts = []
+    for rank, status, out, offset, total, lo, hi in res:
+        assert status == "ok", (status, out)
+        assert total == n and lo == rank * per * 32 and offset == sum(p.size for p in parts)
+        parts.append(out)
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+
+
+def test_distributed_p2p_duplicates_rejected():
+    keys = np.arange(0, 2000, 2, dtype=np.uint32)
+    keys[-1] = keys[0]
+    res = run_ranks(keys, 1 << 12, 2, "p2p")
+    for rank, status, code, msg, *_ in res:
+        assert status == "BitsortError" and int(code) == 2

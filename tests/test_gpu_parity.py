@@ -574,7 +574,49 @@ def test_c5_clustered_properties(capi, cuda, path):
     assert int(u[0]) == int(keys.min()) and int(u[-1]) == int(keys.max())
 
 
-@pytest.mark.parametrize("variant", ["reduce_scatter", "all_to_all"])
+@pytest.mark.parametrize("world,key_range,n", [(2, (1 << 22) - 7, 200_000), (8, 1 << 26, 1 << 22)])
+def test_p2p_or_gather_emulated(capi, cuda, world, key_range, n):
+    """dist.distributed_sort_p2p's per-rank calls on one GPU: every shard's
+    full bitset in its own buffer (the ranks' exported bitsets), each rank's
+    slice OR-gathered from all of them (bws_gpu_bitset_or_gather, here with
+    local pointers instead of IPC-opened peer pointers), then scanned."""
+    from paper_1312_0138_b200.dist import CudaRankOps, shard_bounds, slice_words
+
+    keys = np.random.default_rng(world + 5).choice(key_range, size=n, replace=False).astype(np.uint32)
+    words, per = slice_words(key_range, world)
+    ops = CudaRankOps()
+    bitsets = []
+    for r in range(world):
+        lo, hi = shard_bounds(n, r, world)
+        shard = cuda.from_numpy(keys[lo:hi].view(np.int32)).cuda()
+        bitsets.append(ops.bitset_build(shard, key_range, words).clone())
+    parts = []
+    for r in range(world):
+        sl = ops.or_gather(bitsets, r * per, per).clone()
+        ref = bitsets[0][r * per:(r + 1) * per].clone()
+        for b in bitsets[1:]:
+            ref |= b[r * per:(r + 1) * per]
+        assert cuda.equal(sl, ref)
+        out, cnt = ops.bitset_scan(sl, r * per * 32, n)
+        parts.append(out[: int(cnt.item())].cpu().numpy().view(np.uint32).copy())
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+    # odd word counts and misaligned pointers take the scalar path
+    a = cuda.arange(1, 1000, dtype=cuda.int32, device="cuda")
+    b = cuda.arange(1000, 1999, dtype=cuda.int32, device="cuda")
+    dst = cuda.zeros(998, dtype=cuda.int32, device="cuda")
+    capi.bitset_or_gather([a[1:].data_ptr(), b[1:].data_ptr()], 998, dst.data_ptr())
+    cuda.cuda.synchronize()
+    assert cuda.equal(dst, a[1:] | b[1:])
+
+
+def test_ipc_handle_offsets(capi, cuda):
+    t = cuda.empty(1 << 20, dtype=cuda.int32, device="cuda")
+    h0, off0 = capi.ipc_get_handle(t.data_ptr())
+    h1, off1 = capi.ipc_get_handle(t[1000:].data_ptr())
+    assert len(h0) == capi.IPC_HANDLE_BYTES and h0 == h1 and off1 == off0 + 4000
+
+
+@pytest.mark.parametrize("variant", ["reduce_scatter", "all_to_all", "p2p"])
 def test_distributed_sort_nccl_single_rank(capi, cuda, variant):
     """dist.distributed_sort (bitset build, NCCL reduce-scatter, all-gather,
     K3 on the slice) and dist.distributed_sort_a2a (range split, NCCL
@@ -585,8 +627,9 @@ def test_distributed_sort_nccl_single_rank(capi, cuda, variant):
 
     from paper_1312_0138_b200.dist import distributed_sort as rs
     from paper_1312_0138_b200.dist import distributed_sort_a2a as a2a
+    from paper_1312_0138_b200.dist import distributed_sort_p2p as p2p
 
-    distributed_sort = a2a if variant == "all_to_all" else rs
+    distributed_sort = {"all_to_all": a2a, "p2p": p2p}.get(variant, rs)
 
     store = dist.HashStore()
     dist.init_process_group("nccl", store=store, rank=0, world_size=1,
