@@ -493,162 +493,6 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 }
 
 
-// KB3 "xwide" for more than 1024 buckets: one 24576-key tile per iteration
-// (96 KB of the SMEM tile space, filled by two TMA bulk copies), so each
-// bucket's run per tile is 1.5x as long as with 16384-key tiles (at
-// 4096 buckets, 4-key runs measured +55% partial-sector DRAM traffic). The 24
-// keys of a thread stay in registers; ranks come from a counting pass
-// (SMEM atomics without return) and a fill pass (atomics with return).
-__global__ void __launch_bounds__(PART_THREADS, 1)
-    bucket_partition_xwide_kernel(KeySplit ks, BucketMap bm, int nb,
-                                  const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
-                                  uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int KPT = 24;
-    constexpr int TILE = PART_THREADS * KPT;  // 24576
-    constexpr int kSlots = MAX_BUCKETS + 1;
-    constexpr int NWARPS = PART_THREADS / 32;
-    uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // TILE keys
-    uint32_t* s_cnt = s_buf + TILE;        // keys per bucket in the tile, then fill pointers
-    uint32_t* s_start = s_cnt + kSlots;    // (unused slot kept for the shared layout)
-    uint32_t* s_cur = s_start + kSlots;    // next free global slot
-    uint32_t* s_delta = s_cur + kSlots;    // global slot - local index
-    __shared__ unsigned long long s_scratch[33];
-    __shared__ __align__(8) unsigned long long s_bar[2];
-    __shared__ uint32_t s_tile_valid;
-
-    const unsigned P = gridDim.x, c = blockIdx.x;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const size_t vlo = ks.nv * c / P, vhi = ks.nv * (c + 1) / P;
-    constexpr size_t kTileVec = TILE / 4;
-    constexpr size_t kHalfVec = kTileVec / 2;
-    const size_t ntiles = (vhi - vlo + kTileVec - 1) / kTileVec;
-    const uint32_t spill = static_cast<uint32_t>(nb);
-    auto load_tile = [&](size_t t, unsigned parity_unused) {  // thread 0
-        const size_t v0 = vlo + t * kTileVec;
-        const size_t nvec = min(kTileVec, vhi - v0);
-        const size_t n0 = min(kHalfVec, nvec), n1 = nvec - n0;
-        fence_proxy_async_smem();
-        tma_load_bytes(s_buf, ks.body + v0, static_cast<unsigned>(n0 * 16), &s_bar[0]);
-        if (n1) tma_load_bytes(s_buf + TILE / 2, ks.body + v0 + n0, static_cast<unsigned>(n1 * 16), &s_bar[1]);
-        (void)parity_unused;
-    };
-
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && ntiles > 0) load_tile(0, 0);
-
-    unsigned long long* s_base64 = reinterpret_cast<unsigned long long*>(s_cnt);  // spans cnt+start
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cur[b] = tot[b];
-    __syncthreads();
-    const unsigned long long total = block_exclusive_scan_u64(s_cur, nb, s_base64, s_scratch);
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        if (c == 0) g_base[b] = s_base64[b];
-        s_delta[b] = static_cast<uint32_t>(s_base64[b] + H[static_cast<size_t>(b) * P + c]);
-    }
-    if (c == 0 && threadIdx.x == 0) g_base[nb] = total;
-    __syncthreads();
-    for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
-        s_cur[b] = b < nb ? s_delta[b] : 0u;
-        s_cnt[b] = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // misaligned head (CTA 0) / tail (CTA P-1) keys
-        const uint32_t* extra = c == 0 ? ks.head : nullptr;
-        int ne = c == 0 ? ks.n_head : 0;
-        for (int pass = 0; pass < 2; ++pass) {
-            for (int i = 0; i < ne; ++i) {
-                const uint32_t b = bucket_or_spill(extra[i], true, bm, nb);
-                if (b != spill) parted[s_cur[b]++] = extra[i];
-            }
-            extra = c == P - 1 ? ks.tail : nullptr;
-            ne = c == P - 1 ? ks.n_tail : 0;
-        }
-    }
-    __syncthreads();
-
-    const int slots = nb + 1;
-    const int per = (slots + PART_THREADS - 1) / PART_THREADS;
-    const int sb = threadIdx.x * per;
-    for (size_t t = 0; t < ntiles; ++t) {
-        const size_t v0 = vlo + t * kTileVec;
-        const uint32_t nvec = static_cast<uint32_t>(min(kTileVec, vhi - v0));
-        mbar_wait(&s_bar[0], static_cast<unsigned>(t & 1));
-        if (nvec > kHalfVec) mbar_wait(&s_bar[1], static_cast<unsigned>(t & 1));  // only the last tile can be short
-        uint32_t k[KPT];
-#pragma unroll
-        for (int j = 0; j < KPT / 4; ++j) {
-            const uint32_t vi = j * PART_THREADS + threadIdx.x;
-            const uint4 v = vi < nvec ? reinterpret_cast<const uint4*>(s_buf)[vi] : make_uint4(0, 0, 0, 0);
-            k[4 * j] = vi < nvec ? v.x : 0xffffffffu;
-            k[4 * j + 1] = v.y;
-            k[4 * j + 2] = v.z;
-            k[4 * j + 3] = v.w;
-            if (vi >= nvec) k[4 * j] = k[4 * j + 1] = k[4 * j + 2] = k[4 * j + 3] = 0u;
-        }
-        // counting pass (padding lanes count into the spill slot)
-#pragma unroll
-        for (int j = 0; j < KPT / 4; ++j) {
-            const bool in = j * PART_THREADS + threadIdx.x < nvec;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) atomicAdd(s_cnt + bucket_or_spill(k[4 * j + q], in, bm, nb), 1u);
-        }
-        __syncthreads();  // counts complete; every thread holds its keys
-        {
-            uint32_t local = 0;
-            for (int q = 0; q < per; ++q)
-                if (sb + q < slots) local += s_cnt[sb + q];
-            const uint32_t incl = warp_incl_scan(local, lane);
-            if (lane == 31) s_scratch[warp] = incl;
-            __syncthreads();
-            if (warp == 0) {
-                const uint32_t w = lane < NWARPS ? static_cast<uint32_t>(s_scratch[lane]) : 0u;
-                const uint32_t wi = warp_incl_scan(w, lane);
-                if (lane < NWARPS) s_scratch[lane] = wi - w;
-            }
-            __syncthreads();
-            uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
-            for (int q = 0; q < per; ++q) {
-                const int b = sb + q;
-                if (b < slots) {
-                    const uint32_t cb = s_cnt[b];
-                    s_delta[b] = s_cur[b] - run;
-                    s_cur[b] += cb;
-                    s_cnt[b] = run;  // fill pointer for the scatter
-                    if (b == nb) s_tile_valid = run;
-                    run += cb;
-                }
-            }
-        }
-        __syncthreads();
-        // fill pass: in-place counting-sort scatter
-#pragma unroll
-        for (int j = 0; j < KPT / 4; ++j) {
-            const bool in = j * PART_THREADS + threadIdx.x < nvec;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t b = bucket_or_spill(k[4 * j + q], in, bm, nb);
-                s_buf[atomicAdd(s_cnt + b, 1u)] = k[4 * j + q];
-            }
-        }
-        __syncthreads();
-        const uint32_t tile_valid = s_tile_valid;
-#pragma unroll 4
-        for (uint32_t i = threadIdx.x; i < tile_valid; i += PART_THREADS) {
-            const uint32_t key = s_buf[i];
-            parted[s_delta[bucket_id(key, bm)] + i] = key;
-        }
-        for (int q = 0; q < per; ++q)
-            if (sb + q < slots) s_cnt[sb + q] = 0;
-        __syncthreads();  // tile buffer free
-        if (threadIdx.x == 0 && t + 1 < ntiles) load_tile(t + 1, 0);
-    }
-}
-
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
 // with 4 per thread in flight, tail.
@@ -858,256 +702,6 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
 }
 
 
-// ---- cluster / DSMEM / multicast helpers (PTX) ----
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                     : "memory");
-}
-// Address of the same SMEM object in CTA `rank` of the cluster.
-__device__ __forceinline__ uint32_t map_shared(const void* p, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_addr)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// Bulk copy global -> the same SMEM offset in every CTA of `mask`; each
-// destination CTA's mbarrier at `bar`'s offset receives complete_tx.
-__device__ __forceinline__ void tma_load_multicast(void* dst, const void* src, uint32_t bytes,
-                                                   unsigned long long* bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-        : "memory");
-}
-
-// KB4 with R > 1: a cluster of R CTAs sorts one bucket of range R * 2^20
-// (so KB1-KB3 need R times fewer buckets: their cost grows with the bucket
-// count). CTA r owns the 2^20-key sub-range r in its SMEM bitset. The
-// leader (rank 0) streams the bucket's keys in 16 KB chunks through a
-// double-buffered SMEM ring by TMA MULTICAST: one L2 read lands in all R
-// CTAs; each keeps the keys of its own sub-range. CTA totals are exchanged
-// through distributed shared memory for the output offsets; extraction is
-// the single-CTA code.
-template <int R>
-__global__ void __launch_bounds__(BUCKET_THREADS, 1)
-    bucket_sort_cluster_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
-                               const unsigned long long* __restrict__ g_base, int nb,
-                               uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
-    constexpr uint32_t W = 1u << (CLUSTER_SUB_SHIFT - 5);  // words per sub-range bitset
-    constexpr int kRank = R == 2 ? 1 : R == 4 ? 2 : 3;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* s_sum = s_bits + W;
-    uint32_t* s_ring = s_sum + W / 32;                     // 2 x CLUSTER_CHUNK keys (16B aligned)
-    uint32_t* s_stage_all = s_ring + 2 * CLUSTER_CHUNK;
-    __shared__ __align__(8) unsigned long long s_full[2];  // per CTA: chunk landed
-    __shared__ __align__(8) unsigned long long s_empty[2]; // leader: all R CTAs done with a buffer
-    __shared__ uint32_t s_warp[BUCKET_THREADS / 32];
-    __shared__ uint32_t s_tots[8];
-    __shared__ uint32_t s_b;
-
-    const uint32_t rank = cluster_ctarank();
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned warp = threadIdx.x >> 5;
-    constexpr int kStagePitch = CLUSTER_STAGE + CLUSTER_STAGE / 32;
-    uint32_t* s_stage = s_stage_all + warp * kStagePitch;
-    constexpr uint32_t seg_words = W / (BUCKET_THREADS / 32);
-    const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
-    constexpr uint16_t kMask = static_cast<uint16_t>((1u << R) - 1);
-
-    for (uint32_t i = threadIdx.x; i < W / 32; i += BUCKET_THREADS) s_sum[i] = 0u;
-    if (threadIdx.x == 0) {
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
-        mbar_init(&s_empty[0], R);
-        mbar_init(&s_empty[1], R);
-        fence_mbar_init();
-    }
-    cluster_sync_all();  // every CTA of the cluster runs and its barriers exist before any DSMEM use
-    if (rank == 0 && threadIdx.x == 0) {
-        const unsigned t = atomicAdd(&ctrl->ticket, 1u);
-        for (uint32_t q = 0; q < R; ++q) st_cluster_u32(map_shared(&s_b, q), t);
-    }
-    cluster_sync_all();
-
-    uint32_t g = 0;  // running chunk number (identical in every CTA of the cluster)
-    bool dirty = true;
-    const uint32_t empty0 = map_shared(&s_empty[0], 0);
-    const uint32_t empty1 = map_shared(&s_empty[1], 0);
-    for (;;) {
-        const unsigned b = s_b;
-        if (b >= static_cast<unsigned>(nb)) break;
-        const unsigned long long base = g_base[b];
-        const uint32_t cnt = tot[b];
-        const unsigned long long a = base & ~3ull;  // 16-byte aligned chunk origin
-        const uint32_t off = static_cast<uint32_t>(base - a);
-        const uint32_t span = off + cnt;
-        const uint32_t nch = (span + CLUSTER_CHUNK - 1) / CLUSTER_CHUNK;
-        auto issue = [&](uint32_t k) {  // leader thread 0: chunk k of this bucket
-            const uint32_t gg = g + k;
-            const int p = static_cast<int>(gg & 1);
-            if (gg >= 2) mbar_wait_cluster(&s_empty[p], ((gg - 2) >> 1) & 1);
-            const uint32_t len = min(static_cast<uint32_t>(CLUSTER_CHUNK), span - k * CLUSTER_CHUNK);
-            tma_load_multicast(s_ring + p * CLUSTER_CHUNK, parted + a + static_cast<size_t>(k) * CLUSTER_CHUNK,
-                               ((len * 4) + 15) & ~15u, &s_full[p], kMask);
-        };
-        if (rank == 0 && threadIdx.x == 0) {
-            if (nch > 0) issue(0);
-            if (nch > 1) issue(1);
-        }
-        if (dirty) {
-            uint4* b4 = reinterpret_cast<uint4*>(s_bits);
-            for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
-        }
-        const bool sparse = static_cast<unsigned long long>(cnt) * 4 < static_cast<unsigned long long>(W) * R;
-        __syncthreads();
-        for (uint32_t k = 0; k < nch; ++k) {
-            const uint32_t gg = g + k;
-            const int p = static_cast<int>(gg & 1);
-            const uint32_t len = min(static_cast<uint32_t>(CLUSTER_CHUNK), span - k * CLUSTER_CHUNK);
-            if (threadIdx.x == 0) mbar_expect_tx(&s_full[p], ((len * 4) + 15) & ~15u);
-            mbar_wait(&s_full[p], (gg >> 1) & 1);
-            const uint4* r4 = reinterpret_cast<const uint4*>(s_ring + p * CLUSTER_CHUNK);
-            for (uint32_t v = threadIdx.x; v < CLUSTER_CHUNK / 4; v += BUCKET_THREADS) {
-                const uint4 kv = r4[v];
-                const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t i = k * CLUSTER_CHUNK + 4 * v + q - off;  // index in the bucket
-                    const uint32_t key = kk[q];
-                    if (i < cnt && ((key >> CLUSTER_SUB_SHIFT) & (R - 1)) == rank) {
-                        const uint32_t x = key & ((1u << CLUSTER_SUB_SHIFT) - 1);
-                        const uint32_t w = x >> 5;
-                        atomicOr(s_bits + w, 1u << (x & 31));
-                        if (sparse) atomicOr(s_sum + (w >> 5), 1u << (w & 31));
-                    }
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                fence_proxy_async_smem();
-                mbar_arrive_remote(p ? empty1 : empty0);
-                if (rank == 0 && k + 2 < nch) issue(k + 2);
-            }
-        }
-        g += nch;
-        // phase 1: per-warp popcount of this CTA's sub-range
-        const uint32_t seg = warp * seg_words;
-        uint32_t c = 0;
-        if (sparse) {
-            for (uint32_t i = lane; i < seg_words / 32; i += 32) {
-                const uint32_t si = seg / 32 + i;
-                for (uint32_t m = s_sum[si]; m; m &= m - 1) c += __popc(s_bits[si * 32 + (__ffs(m) - 1)]);
-            }
-        } else {
-            for (uint32_t i = lane; i < seg_words / 4; i += 32) {
-                const uint4 v = s4[seg / 4 + i];
-                c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-            }
-        }
-        c = __reduce_add_sync(kFull, c);
-        if (lane == 0) s_warp[warp] = c;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = s_warp[lane];
-            const uint32_t incl = warp_incl_scan(v, lane);
-            s_warp[lane] = incl - v;
-            if (lane == 31) {
-                if (incl) atomicAdd(&ctrl->total, static_cast<unsigned long long>(incl));
-                for (uint32_t q = 0; q < R; ++q) st_cluster_u32(map_shared(&s_tots[rank], q), incl);
-            }
-        }
-        cluster_sync_all();  // every CTA's total is visible in every CTA
-        uint32_t before = 0;
-#pragma unroll
-        for (int q = 0; q < R; ++q) before += q < static_cast<int>(rank) ? s_tots[q] : 0u;
-        uint32_t* o = out + base + before + s_warp[warp];
-        const uint32_t key_hi = (static_cast<uint32_t>(b) << (CLUSTER_SUB_SHIFT + kRank)) +
-                                (rank << CLUSTER_SUB_SHIFT);
-        if (sparse) {
-            for (uint32_t i0 = 0; i0 < seg_words / 32; i0 += 32) {
-                const uint32_t si = seg / 32 + i0 + lane;
-                uint32_t m = i0 + lane < seg_words / 32 ? s_sum[si] : 0u;
-                uint32_t cl = 0;
-                for (uint32_t mm = m; mm; mm &= mm - 1) cl += __popc(s_bits[si * 32 + (__ffs(mm) - 1)]);
-                const uint32_t incl = warp_incl_scan(cl, lane);
-                const uint32_t ctot = __shfl_sync(kFull, incl, 31);
-                if (ctot == 0) continue;
-                uint32_t* ol = o + (incl - cl);
-                if (m) s_sum[si] = 0u;
-                while (m) {
-                    const uint32_t t = static_cast<uint32_t>(__ffs(m) - 1);
-                    m &= m - 1;
-                    const uint32_t wi = si * 32 + t;
-                    uint32_t x = s_bits[wi];
-                    s_bits[wi] = 0u;
-                    const uint32_t kb = key_hi + (wi << 5);
-                    while (x) {
-                        const int bt = __ffs(x) - 1;
-                        x &= x - 1;
-                        __stcs(ol++, kb + static_cast<uint32_t>(bt));
-                    }
-                }
-                o += ctot;
-            }
-        } else {
-            for (uint32_t w0 = 0; w0 < seg_words; w0 += 128) {
-                const uint4 v = s4[(seg + w0) / 4 + lane];
-                const uint32_t cl = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-                const uint32_t incl = warp_incl_scan(cl, lane);
-                const uint32_t ctot = __shfl_sync(kFull, incl, 31);
-                if (ctot == 0) continue;
-                if (ctot <= static_cast<uint32_t>(CLUSTER_STAGE)) {
-                    uint32_t p = incl - cl;
-                    const uint32_t kb = key_hi + ((seg + w0 + 4 * lane) << 5);
-                    stage_bits(v.x, kb, p, s_stage);
-                    stage_bits(v.y, kb + 32, p, s_stage);
-                    stage_bits(v.z, kb + 64, p, s_stage);
-                    stage_bits(v.w, kb + 96, p, s_stage);
-                    drain_stage(s_stage, ctot, o, lane);
-                    o += ctot;
-                    continue;
-                }
-#pragma unroll 1
-                for (uint32_t q = 0; q < 128; q += 32)
-                    o += extract_words32<CLUSTER_STAGE>(s_bits, seg + w0 + q, key_hi, o, s_stage, lane);
-            }
-        }
-        dirty = !sparse;
-        if (rank == 0 && threadIdx.x == 0) {
-            const unsigned t = atomicAdd(&ctrl->ticket, 1u);
-            for (uint32_t q = 0; q < R; ++q) st_cluster_u32(map_shared(&s_b, q), t);
-        }
-        cluster_sync_all();  // next ticket visible; s_tots and the ring free for reuse
-    }
-}
-
 // KB4b (multi-GPU per-rank build): like KB4, but instead of extracting keys
 // each bucket's SMEM bitset is written to the global bitset, coalesced and
 // without atomics; every word below n_words is written, so the caller's
@@ -1162,60 +756,6 @@ __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl
 // The narrow KB3 variant (2 CTAs/SM, 8192-key tiles) measured slower than the
 // wide one on C2 (profiles/r01_*): shorter bucket runs add partial-sector
 // DRAM traffic. It stays selectable for experiments (BITSORT_PART=narrow).
-template <int R>
-static cudaError_t launch_cluster_kb4_t(int clusters, const uint32_t* parted, const uint32_t* tot,
-                                        const unsigned long long* base, int nb, uint32_t* out,
-                                        Ctrl* ctrl, cudaStream_t stream) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(clusters * R));
-    cfg.blockDim = dim3(BUCKET_THREADS);
-    cfg.dynamicSmemBytes = cluster_sort_smem_bytes();
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = R;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, bucket_sort_cluster_kernel<R>, parted, tot, base, nb, out, ctrl);
-}
-
-static cudaError_t launch_cluster_kb4(int r, const LaunchGeometry& geo, const uint32_t* parted,
-                                      const uint32_t* tot, const unsigned long long* base, int nb,
-                                      uint32_t* out, Ctrl* ctrl, cudaStream_t stream) {
-    switch (r) {
-        case 2: return launch_cluster_kb4_t<2>(geo.clusters[1], parted, tot, base, nb, out, ctrl, stream);
-        case 4: return launch_cluster_kb4_t<4>(geo.clusters[2], parted, tot, base, nb, out, ctrl, stream);
-        case 8: return launch_cluster_kb4_t<8>(geo.clusters[3], parted, tot, base, nb, out, ctrl, stream);
-    }
-    return cudaErrorInvalidValue;
-}
-
-template <int R>
-static cudaError_t configure_cluster_kb4(int* clusters) {
-    cudaError_t err = cudaFuncSetAttribute(bucket_sort_cluster_kernel<R>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(cluster_sort_smem_bytes()));
-    if (err != cudaSuccess) return err;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(R * 64);
-    cfg.blockDim = dim3(BUCKET_THREADS);
-    cfg.dynamicSmemBytes = cluster_sort_smem_bytes();
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = R;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    err = cudaOccupancyMaxActiveClusters(&n, bucket_sort_cluster_kernel<R>, &cfg);
-    if (err != cudaSuccess) return err;
-    *clusters = n > 0 ? n : 1;
-    return cudaSuccess;
-}
-
 static bool narrow_partition(const BucketPlan& plan) {
     static const bool want = [] {
         const char* e = std::getenv("BITSORT_PART");
@@ -1238,31 +778,17 @@ static BucketMap pow2_map(int shift) {
     return m;
 }
 
-BucketPlan plan_buckets(uint64_t key_range, int kb4_ctas, bool allow_cluster) {
+BucketPlan plan_buckets(uint64_t key_range, int kb4_ctas) {
     BucketPlan p;
     int log2m = 0;
     while ((1ull << log2m) < key_range) ++log2m;
     // About 256 buckets: KB3 runs faster with fewer buckets (longer runs per
     // tile; measured C2: 256 buckets 177 us vs 1024 buckets 256 us) and KB4
-    // still has enough of them. A bucket wider than one SMEM bitset (2^20
-    // keys) is sorted by a cluster of R CTAs, R <= MAX_CLUSTER.
+    // still has enough of them. Ranges above 2^28 take 2^20-key buckets (the
+    // largest SMEM bitset) and more of them, up to MAX_BUCKETS. (A cluster
+    // KB4 with DSMEM bitsets for wider buckets measured 6.7x slower on C3:
+    // profiles/r01_cluster_kb4_experiment.json.)
     int shift = log2m - 8;
-    p.cluster = 1;
-    // Off by default: measured slower (C3 KB4 1.5 ms -> 10 ms, profiles/r01_*): every CTA
-    // of a cluster must hold every in-flight multicast chunk, so a cluster streams
-    // at one SM's share of HBM bandwidth while occupying R SMs. BITSORT_CLUSTER=1
-    // enables it for experiments.
-    if (allow_cluster && shift > MAX_BUCKET_SHIFT && std::getenv("BITSORT_CLUSTER")) {
-        int r = shift - MAX_BUCKET_SHIFT;
-        if ((1 << r) > MAX_CLUSTER) r = 0;
-        while ((1 << (r + 1)) <= MAX_CLUSTER && r < shift - MAX_BUCKET_SHIFT) ++r;
-        p.cluster = 1 << r;
-        const uint64_t nbc = (key_range + (1ull << (MAX_BUCKET_SHIFT + r)) - 1) >> (MAX_BUCKET_SHIFT + r);
-        p.shift = MAX_BUCKET_SHIFT + r;
-        p.map = pow2_map(p.shift);
-        p.nb = static_cast<int>(nbc);
-        return p;
-    }
     const char* env = std::getenv("BITSORT_BUCKET_SHIFT");  // experiments
     if (env) shift = std::atoi(env);
     while (shift < MAX_BUCKET_SHIFT && ((key_range + (1ull << shift) - 1) >> shift) > MAX_BUCKETS) ++shift;
@@ -1333,9 +859,7 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
         const char* e = std::getenv("BITSORT_SLAB");
         return e && std::string(e) == "0";
     }();
-    if (off || plan.cluster > 1 || plan.partition_only ||
-        (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE")))
-        return 0;
+    if (off || plan.partition_only) return 0;
     uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
     if (cap > plan.map.width) cap = plan.map.width;
     const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_DUMP;  // + dump tile
@@ -1424,12 +948,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (timer) timer->after("bucket_colscan", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         if (timer) timer->before(stream);
-        // xwide measured slightly slower (C4 KB3 121 vs 112 us, C5 1576 vs 1535 us):
-        // opt-in only (BITSORT_XWIDE=1)
-        if (plan.nb > PART_NARROW_MAXB && std::getenv("BITSORT_XWIDE") && !ks.xr)
-            bucket_partition_xwide_kernel<<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
-                ks, plan.map, plan.nb, H, tot, parted, base);
-        else if (narrow_partition(plan))
+        if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
@@ -1458,18 +977,13 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         return cudaSuccess;
     }
     if (timer) timer->before(stream);
-    if (plan.cluster > 1) {
-        err = launch_cluster_kb4(plan.cluster, geo, parted, tot, base, plan.nb, out, ctrl, stream);
-        if (err != cudaSuccess) return err;
-    } else {
-        const size_t smem = bucket_sort_smem_bytes(plan.shift);
-        if (plan.shift >= MAX_BUCKET_SHIFT)
-            bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-                parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
-        else  // narrower buckets: a smaller stage lets two CTAs share an SM
-            bucket_sort_kernel<BUCKET_STAGE_SMALL><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-                parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
-    }
+    const size_t smem = bucket_sort_smem_bytes(plan.shift);
+    if (plan.shift >= MAX_BUCKET_SHIFT)
+        bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
+    else  // narrower buckets: a smaller stage lets two CTAs share an SM
+        bucket_sort_kernel<BUCKET_STAGE_SMALL><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;
@@ -1496,9 +1010,6 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
-    if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_xwide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
@@ -1530,10 +1041,6 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
         if (err != cudaSuccess) return err;
         geo->bucket_blocks[shift] = sms * (per > 0 ? per : 1);
     }
-    geo->clusters[0] = geo->bucket_blocks[MAX_BUCKET_SHIFT];
-    if ((err = configure_cluster_kb4<2>(&geo->clusters[1])) != cudaSuccess) return err;
-    if ((err = configure_cluster_kb4<4>(&geo->clusters[2])) != cudaSuccess) return err;
-    if ((err = configure_cluster_kb4<8>(&geo->clusters[3])) != cudaSuccess) return err;
     return cudaSuccess;
 }
 

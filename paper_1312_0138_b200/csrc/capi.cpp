@@ -484,9 +484,9 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
         key_range = static_cast<uint64_t>(mx) + 1;
     }
     // signed sorts keep power-of-two bucket widths (the output XOR then
-    // commutes with the in-bucket offsets) and no cluster plan
-    bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(
-        key_range, xr ? 0 : ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT], /*allow_cluster=*/xr == 0);
+    // commutes with the in-bucket offsets)
+    bws_gpu::BucketPlan plan =
+        bws_gpu::plan_buckets(key_range, xr ? 0 : ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
     plan.map.lo = key_lo;
     plan.map.xr = xr;
     const size_t parted_cap = ctx.ensure_parted(count, plan);
@@ -897,8 +897,8 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
                               (path == BWS_PATH_BUCKETED || (path == BWS_PATH_AUTO && count >= kBucketedMinKeys));
         if (bucketed) {
             // KB1-KB3 + KB4b: SMEM-staged, coalesced, no atomics to global, no memset
-            const bws_gpu::BucketPlan plan = bws_gpu::plan_buckets(
-                key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT], /*allow_cluster=*/false);
+            const bws_gpu::BucketPlan plan =
+                bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
             const size_t parted_cap = ctx.ensure_parted(count, plan);
             int launches = 0;
             cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, nullptr, ctx.parted,

@@ -63,10 +63,6 @@ constexpr int PART_NARROW_MAXB = 1024;
 constexpr int BUCKET_THREADS = 1024;
 constexpr int BUCKET_STAGE = 640;        // keys per warp in the extraction stage (2^20 buckets)
 constexpr int BUCKET_STAGE_SMALL = 256;  // narrower buckets: fits two CTAs per SM
-constexpr int MAX_CLUSTER = 8;          // CTAs per bucket in the cluster KB4 (portable limit)
-constexpr int CLUSTER_SUB_SHIFT = 20;   // each cluster CTA owns a 2^20-key sub-range
-constexpr int CLUSTER_CHUNK = 4096;     // keys per multicast chunk (16 KB), two buffers
-constexpr int CLUSTER_STAGE = 256;      // keys per warp in the cluster kernel's stage
 
 constexpr int PART_KPT_SLAB = 20;   // slab KB3 with <= 1024 buckets: 20480-key tiles
 constexpr int PART_DUMP = 32768;    // slab overflow tile (>= any KB3 tile)
@@ -79,10 +75,6 @@ constexpr std::size_t bucket_sort_smem_bytes(int shift) {
            (BUCKET_THREADS / 32) * (stage + stage / 32) * 4;
 }
 
-constexpr std::size_t cluster_sort_smem_bytes() {
-    return (std::size_t(1) << (CLUSTER_SUB_SHIFT - 3)) + (std::size_t(1) << (CLUSTER_SUB_SHIFT - 8)) +
-           2 * CLUSTER_CHUNK * 4 + (BUCKET_THREADS / 32) * (CLUSTER_STAGE + CLUSTER_STAGE / 32) * 4;
-}
 
 struct LaunchGeometry {
     int scatter_blocks = 0;
@@ -91,7 +83,6 @@ struct LaunchGeometry {
     int part_blocks = 0;                         // KB1/KB3 shares, wide KB3 variant
     int part_blocks_narrow = 0;                  // KB1/KB3 shares, narrow KB3 variant
     int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
-    int clusters[4] = {};                          // cluster KB4: max clusters for R = 1,2,4,8
     int scan2_blocks = 0;                          // K3 v2 CTAs
 };
 
@@ -123,7 +114,6 @@ struct BucketMap {
 struct BucketPlan {
     int shift = 20;   // SMEM bitset class of a bucket: 2^shift bits >= map.width
     int nb = 1;       // number of buckets, <= MAX_BUCKETS
-    int cluster = 1;  // CTAs per bucket in KB4 (bucket range = cluster * 2^20 when > 1)
     BucketMap map;
     bool partition_only = false;  // stop after KB3 (range split: packed groups, totals in scratch)
 };
@@ -194,9 +184,8 @@ cudaError_t launch_scan2(std::uint32_t* bits, std::uint64_t n_words, std::uint32
 BucketPlan plan_range_split(std::uint64_t key_range, int parts);
 // Bucket totals (uint32 per bucket) in the scratch of the last launch_bucket_sort.
 const std::uint32_t* bucket_totals(const void* scratch, const BucketPlan& plan, const LaunchGeometry& geo);
-// kb4_ctas: resident KB4 CTAs (0: power-of-two widths only). With
-// allow_cluster, ranges above 2^28 may use the opt-in cluster KB4.
-BucketPlan plan_buckets(std::uint64_t key_range, int kb4_ctas, bool allow_cluster = true);
+// kb4_ctas: resident KB4 CTAs (0: power-of-two widths only).
+BucketPlan plan_buckets(std::uint64_t key_range, int kb4_ctas);
 // Bucket-buffer slots the slab layout needs for n keys (0: use the packed
 // histogram layout: the slab would exceed 4n slots or 2^32).
 std::uint64_t slab_slots(const BucketPlan& plan, std::size_t n);
