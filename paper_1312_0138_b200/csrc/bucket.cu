@@ -241,15 +241,15 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
     __threadfence();
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         const uint32_t v = __ldcg(sa.gcnt + b);
-        s_vals[b] = v <= sa.cap ? v : 0u;
+        const bool ok = v <= sa.cap;
+        sa.tot[b] = ok ? v : 0u;  // slots KB4 reads
+        s_vals[b] = ok ? (sa.gtrue ? __ldcg(sa.gtrue + b) : v) : 0u;  // keys, for the offsets
         sa.gcnt[b] = 0u;  // the counters start the next sort at zero
+        if (sa.gtrue) sa.gtrue[b] = 0u;
     }
     __syncthreads();
     const unsigned long long total = block_exclusive_scan_u64(s_vals, nb, s_out64, s_scratch);
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        sa.g_base[b] = s_out64[b];
-        sa.tot[b] = s_vals[b];
-    }
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) sa.g_base[b] = s_out64[b];
     if (threadIdx.x == 0) sa.g_base[nb] = total;
 }
 
@@ -490,6 +490,210 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         }
     }
     if constexpr (SLAB) slab_finish(sa, nb, bad, s_cur, s_base64, s_scratch, &s_last);
+}
+
+
+// KB3, slab layout with bulk-copy (TMA) run stores — the default for <= 1024
+// buckets. Same tile pipeline as bucket_partition_kernel, but the tile is
+// counting-sorted into a separate SMEM buffer whose bucket runs start on
+// 16-byte boundaries, and each bucket's run leaves with ONE cp.async.bulk
+// store issued by the thread owning the bucket, instead of every thread
+// copying keys and looking up their bucket's destination (that write loop was
+// ~20% of KB3's instructions; 293 bulk stores of ~224 B per SM per tile
+// measured ~2 us, tools/tma_store_bench.cu). The stores drain while the next
+// tile is ranked; their SMEM reads are waited for just before the next
+// scatter. Runs are padded to a multiple of 4 keys with copies of the run's
+// first key (a bitset ignores repeats: KB4 reads the padded slot count, the
+// output offsets use the true count), so every claim in the slab is 16-byte
+// aligned. The TMA ring is freed as soon as a tile's keys are in registers,
+// so the next-but-one tile's load starts a phase earlier than in the
+// in-place variant.
+template <int MAXB>
+__global__ void __launch_bounds__(PART_THREADS, 1)
+    bucket_partition_tma_kernel(KeySplit ks, BucketMap bm, int nb, uint32_t* __restrict__ parted, SlabArgs sa) {
+    constexpr int THREADS = PART_THREADS;
+    constexpr int KPT = PART_KPT;
+    constexpr int TILE = THREADS * KPT;
+    constexpr int NWARPS = THREADS / 32;
+    constexpr int kSlots = MAXB + 1;
+    constexpr int PER_MAX = (kSlots + THREADS - 1) / THREADS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint32_t* s_ring = reinterpret_cast<uint32_t*>(smem_raw);  // 2 x TILE (TMA destination)
+    uint32_t* s_sorted = s_ring + 2 * TILE;                     // TILE + 4 * kSlots (runs 16B-aligned)
+    uint32_t* s_cnt = s_sorted + TILE + 4 * kSlots;             // keys per bucket in the tile
+    uint32_t* s_start = s_cnt + kSlots;                         // run start in s_sorted (multiple of 4)
+    __shared__ unsigned long long s_scratch[33];
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    __shared__ uint32_t s_last;
+
+    const unsigned P = gridDim.x, c = blockIdx.x;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t vlo = ks.nv * c / P, vhi = ks.nv * (c + 1) / P;
+    constexpr size_t kTileVec = TILE / 4;
+    const size_t ntiles = (vhi - vlo + kTileVec - 1) / kTileVec;
+    const uint32_t spill = static_cast<uint32_t>(nb);
+    const uint32_t last = sa.check ? sa.limit - 1u : 0xffffffffu;
+    auto slot_of = [&](uint32_t key, bool in) -> uint32_t {
+        return in && key - bm.lo <= last ? bucket_id(key, bm) : spill;
+    };
+    auto load_tile = [&](size_t t, int p) {  // thread 0
+        const size_t v0 = vlo + t * kTileVec;
+        const size_t nvec = min(kTileVec, vhi - v0);
+        fence_proxy_async_smem();
+        tma_load_bytes(s_ring + p * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16), &s_bar[p]);
+    };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    for (int b = threadIdx.x; b < kSlots; b += THREADS) s_cnt[b] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (size_t t = 0; t < 2 && t < ntiles; ++t) load_tile(t, static_cast<int>(t));
+    uint32_t bad = 0;
+    if (threadIdx.x == 0) {  // misaligned head (CTA 0) / tail (CTA P-1): one padded claim each
+        const uint32_t* extra = c == 0 ? ks.head : nullptr;
+        int ne = c == 0 ? ks.n_head : 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = 0; i < ne; ++i) {
+                const uint32_t e = extra[i] ^ ks.xr;
+                bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
+                const uint32_t b = slot_of(e, true);
+                if (b == spill) continue;
+                atomicAdd(sa.gtrue + b, 1u);
+                const uint32_t pos = atomicAdd(sa.gcnt + b, 4u);
+                if (pos + 4 <= sa.cap)
+                    for (int q = 0; q < 4; ++q) parted[b * sa.cap + pos + q] = e;
+            }
+            extra = c == P - 1 ? ks.tail : nullptr;
+            ne = c == P - 1 ? ks.n_tail : 0;
+        }
+    }
+
+    constexpr int VPT = KPT / 4;
+    const int slots = nb + 1;
+    const int per = (slots + THREADS - 1) / THREADS;
+    const int sb = threadIdx.x * per;
+    bool stores_pending = false;  // this thread has bulk stores reading s_sorted
+    for (size_t t = 0; t < ntiles; ++t) {
+        const int p = static_cast<int>(t & 1);
+        const uint32_t* buf = s_ring + p * TILE;
+        const size_t v0 = vlo + t * kTileVec;
+        const uint32_t nvec = static_cast<uint32_t>(min(kTileVec, vhi - v0));
+        mbar_wait(&s_bar[p], static_cast<unsigned>((t >> 1) & 1));
+
+        uint32_t k[KPT];
+        uint32_t rb[KPT];  // bucket << 16 | rank inside the bucket (rank < TILE)
+        uint32_t kmin = 0xffffffffu, kmax = 0;
+        bool all_in = true;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const uint32_t vi = j * THREADS + threadIdx.x;
+            const bool in = vi < nvec;
+            all_in &= in;
+            const uint4 v = in ? reinterpret_cast<const uint4*>(buf)[vi] : make_uint4(0, 0, 0, 0);
+            const uint32_t kk[4] = {v.x ^ ks.xr, v.y ^ ks.xr, v.z ^ ks.xr, v.w ^ ks.xr};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                k[4 * j + q] = kk[q];
+                rb[4 * j + q] = slot_of(kk[q], in);
+                kmin = min(kmin, kk[q]);
+                kmax = max(kmax, kk[q]);
+            }
+        }
+        const uint32_t blo = slot_of(__reduce_min_sync(kFull, kmin), true);
+        const uint32_t bhi = slot_of(__reduce_max_sync(kFull, kmax), true);
+        if (blo == bhi && __all_sync(kFull, all_in)) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(s_cnt + blo, 32u * KPT);
+            base = __shfl_sync(kFull, base, 0) + lane * KPT;
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) rb[q] = (blo << 16) | (base + q);
+        } else {
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) rb[q] = (rb[q] << 16) | atomicAdd(s_cnt + rb[q], 1u);
+        }
+        __syncthreads();  // A: counts complete; the ring slot is free
+        if (threadIdx.x == 0 && t + 2 < ntiles) load_tile(t + 2, p);
+        // padded run starts (multiples of 4) and the slab claims
+        uint32_t claim[PER_MAX];
+        uint32_t ccnt[PER_MAX];
+        {
+            uint32_t local = 0;
+            for (int q = 0; q < per; ++q)
+                if (sb + q < nb) local += (s_cnt[sb + q] + 3u) & ~3u;
+            const uint32_t incl = warp_incl_scan(local, lane);
+            if (lane == 31) s_scratch[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = lane < NWARPS ? static_cast<uint32_t>(s_scratch[lane]) : 0u;
+                const uint32_t wi = warp_incl_scan(w, lane);
+                if (lane < NWARPS) s_scratch[lane] = wi - w;
+            }
+            __syncthreads();
+            uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
+#pragma unroll
+            for (int q = 0; q < PER_MAX; ++q) {
+                const int b = sb + q;
+                ccnt[q] = 0;
+                if (q < per && b < slots) {
+                    const uint32_t cb = s_cnt[b];
+                    s_cnt[b] = 0;
+                    if (b == nb) {
+                        bad += cb - (TILE - 4 * nvec);  // out-of-range keys (padding lanes spill too)
+                    } else {
+                        s_start[b] = run;
+                        if (cb) {
+                            const uint32_t pc = (cb + 3u) & ~3u;
+                            claim[q] = atomicAdd(sa.gcnt + b, pc);
+                            atomicAdd(sa.gtrue + b, cb);
+                            ccnt[q] = cb;
+                        }
+                        run += (cb + 3u) & ~3u;
+                    }
+                }
+            }
+        }
+        // the previous tile's bulk stores must have read s_sorted before it is rewritten
+        if (stores_pending) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            stores_pending = false;
+        }
+        __syncthreads();  // B
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) {
+            const uint32_t b = rb[q] >> 16;
+            if (b != spill) s_sorted[s_start[b] + (rb[q] & 0xffffu)] = k[q];
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk copies
+        __syncthreads();  // C
+#pragma unroll
+        for (int q = 0; q < PER_MAX; ++q) {
+            if (ccnt[q]) {
+                const uint32_t b = sb + q;
+                const uint32_t cb = ccnt[q], pc = (cb + 3u) & ~3u;
+                const uint32_t st = s_start[b];
+                for (uint32_t i = cb; i < pc; ++i) s_sorted[st + i] = s_sorted[st];  // pad with a repeat
+                fence_proxy_async_smem();
+                // a claim past the bucket's capacity (only duplicates cause one) goes to the dump tile
+                uint32_t* dst = parted + (claim[q] + pc <= sa.cap ? static_cast<size_t>(b) * sa.cap + claim[q]
+                                                                  : static_cast<size_t>(sa.dump));
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                             "r"(smem_u32(s_sorted + st)), "r"(pc * 4)
+                             : "memory");
+                stores_pending = true;
+            }
+        }
+        if (stores_pending) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (stores_pending) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    slab_finish(sa, nb, bad, s_cnt, reinterpret_cast<unsigned long long*>(s_sorted), s_scratch, &s_last);
+}
+
+constexpr std::size_t part_tma_smem_bytes(int maxb) {
+    return (2 * std::size_t(PART_TILE) + PART_TILE + 4 * std::size_t(maxb + 1) + 2 * std::size_t(maxb + 1)) * 4;
 }
 
 
@@ -851,7 +1055,18 @@ BucketPlan plan_range_split(uint64_t key_range, int parts) {
 
 const uint32_t* bucket_totals(const void* scratch, const BucketPlan& plan, const LaunchGeometry& geo) {
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
-    return static_cast<const uint32_t*>(scratch) + MAX_BUCKETS + static_cast<size_t>(P) * plan.nb;
+    return static_cast<const uint32_t*>(scratch) + 2 * MAX_BUCKETS + static_cast<size_t>(P) * plan.nb;
+}
+
+// The bulk-store KB3 (bucket_partition_tma_kernel) takes slab sorts with <= 1024 buckets.
+static bool tma_store_kb3(const BucketPlan& plan) {
+    static const bool off = [] {
+        const char* e = std::getenv("BITSORT_TMA_STORE");
+        return e && std::string(e) == "0";
+    }();
+    // runs average TILE / nb keys per tile: at 1024 buckets (C3, 16-key runs)
+    // the padding and ~1000 small copies per tile cost more than they save
+    return !off && plan.nb <= 512 && !narrow_partition(plan);
 }
 
 uint64_t slab_slots(const BucketPlan& plan, size_t n) {
@@ -862,6 +1077,9 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
     if (off || plan.partition_only) return 0;
     uint64_t cap = (static_cast<uint64_t>(n) + 3) & ~uint64_t(3);
     if (cap > plan.map.width) cap = plan.map.width;
+    // bulk-store runs are padded to multiples of 4: at most 3 extra slots per
+    // bucket per tile (KB3 CTAs <= 1024) plus the head/tail claims
+    if (tma_store_kb3(plan)) cap += 3 * (static_cast<uint64_t>(n) / PART_TILE + 1024 + 8);
     const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_DUMP;  // + dump tile
     // the slab trades memory (up to 4.5 slots per key) for the histogram pass
     if (slots > 4 * static_cast<uint64_t>(n) + n / 2 + PART_DUMP || slots >= (1ull << 32)) return 0;
@@ -872,7 +1090,7 @@ size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
     return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H
            + (MAX_BUCKETS + 1) * sizeof(uint32_t)                          // tot
            + (MAX_BUCKETS + 2) * sizeof(unsigned long long)                // base (8-aligned)
-           + MAX_BUCKETS * sizeof(uint32_t);                               // slab fill counters
+           + 2 * MAX_BUCKETS * sizeof(uint32_t);                           // slab fill + true counts
 }
 
 cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* out,
@@ -883,8 +1101,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     // scratch: slab fill counters (fixed place: they persist across sorts), then H, tot, base
-    uint32_t* gcnt = static_cast<uint32_t*>(scratch);
-    uint32_t* H = gcnt + MAX_BUCKETS;
+    uint32_t* gcnt = static_cast<uint32_t*>(scratch);  // then the true counts (bulk-store KB3)
+    uint32_t* H = gcnt + 2 * MAX_BUCKETS;
     uint32_t* tot = H + static_cast<size_t>(P) * plan.nb;
     unsigned long long* base =
         reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(tot + MAX_BUCKETS + 1) & ~uintptr_t(7));
@@ -911,7 +1129,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         // KB3 (slab) claims slots with fill counters: no KB1/KB2. The counters
         // are zeroed once at allocation and re-zeroed by the last KB3 CTA.
         sa.gcnt = gcnt;
-        sa.cap = static_cast<uint32_t>((slab - PART_DUMP) / plan.nb);
+        sa.gtrue = tma_store_kb3(plan) ? gcnt + MAX_BUCKETS : nullptr;
+        sa.cap = static_cast<uint32_t>((slab - PART_DUMP) / plan.nb) & ~3u;
         sa.dump = static_cast<uint32_t>(slab - PART_DUMP);
         sa.limit = limit;
         sa.check = check;
@@ -919,7 +1138,10 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.tot = tot;
         sa.g_base = base;
         if (timer) timer->before(stream);
-        if (narrow_partition(plan))
+        if (sa.gtrue)
+            bucket_partition_tma_kernel<PART_NARROW_MAXB>
+                <<<P, PART_THREADS, part_tma_smem_bytes(PART_NARROW_MAXB), stream>>>(ks, plan.map, plan.nb, parted, sa);
+        else if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
@@ -1002,6 +1224,9 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_tma_kernel<PART_NARROW_MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_tma_smem_bytes(PART_NARROW_MAXB)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -131,8 +131,10 @@ struct SlabArgs {
     std::uint32_t limit = 0;               // keys >= limit are counted as bad (check != 0)
     int check = 0;
     Ctrl* ctrl = nullptr;
-    std::uint32_t* tot = nullptr;          // out: keys per bucket
+    std::uint32_t* tot = nullptr;          // out: keys per bucket (slots to read, padding included)
     unsigned long long* g_base = nullptr;  // out: output offset per bucket (+ total at [nb])
+    std::uint32_t* gtrue = nullptr;        // TMA-store KB3: true keys per bucket (gcnt counts
+                                           // slots, padded to multiples of 4); zeroed like gcnt
 };
 
 // Optional per-kernel timing hook (bench.py's live roofline): before() and
