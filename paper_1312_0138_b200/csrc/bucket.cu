@@ -700,7 +700,7 @@ constexpr std::size_t part_tma_smem_bytes(int maxb) {
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
 // with 4 per thread in flight, tail.
-template <bool SPARSE>
+template <bool SPARSE, int NT = BUCKET_THREADS>
 __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__ src, uint32_t cnt,
                                                     uint32_t key_lo, uint32_t* s_bits,
                                                     uint32_t* s_sum) {
@@ -716,12 +716,12 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
     const uint4* v4 = reinterpret_cast<const uint4*>(src + head);
     const uint32_t nv = (cnt - head) / 4;
     constexpr int U = 4;
-    constexpr uint32_t kBatch = BUCKET_THREADS * U;
+    constexpr uint32_t kBatch = NT * U;
     uint32_t i0 = 0;
     for (; i0 + kBatch <= nv; i0 += kBatch) {
         uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(v4 + i0 + u * BUCKET_THREADS + threadIdx.x);
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(v4 + i0 + u * NT + threadIdx.x);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             set_key(v[u].x);
@@ -730,7 +730,7 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
             set_key(v[u].w);
         }
     }
-    for (uint32_t i = i0 + threadIdx.x; i < nv; i += BUCKET_THREADS) {
+    for (uint32_t i = i0 + threadIdx.x; i < nv; i += NT) {
         const uint4 v = __ldcs(v4 + i);
         set_key(v.x);
         set_key(v.y);
@@ -752,8 +752,8 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
 // each touched word in a summary bitset (one bit per word), visit only
 // touched words, and zero exactly those words again, so a sparse bucket costs
 // O(keys) SMEM work instead of O(2^shift / 32) and leaves the bitset clean.
-template <int STAGE>
-__global__ void __launch_bounds__(BUCKET_THREADS, 2)
+template <int STAGE, int NT = BUCKET_THREADS>
+__global__ void __launch_bounds__(NT, 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
@@ -761,8 +761,8 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     const uint32_t W = bm.width >> 5;  // words per bucket bitset (>= 1024; 2^k or a multiple of 4096)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* s_sum = s_bits + W;             // bit w set <=> word w touched (sparse buckets)
-    uint32_t* s_stage_all = s_sum + W / 32;   // BUCKET_THREADS/32 x stage pitch
-    __shared__ uint32_t s_warp[BUCKET_THREADS / 32];
+    uint32_t* s_stage_all = s_sum + W / 32;   // NT/32 x stage pitch
+    __shared__ uint32_t s_warp[NT / 32];
     // next bucket (ticket, offset, count), fetched by thread 0 one bucket ahead
     // so its latency hides behind the current bucket (sparse buckets are short)
     __shared__ unsigned s_b[2];
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
     const unsigned warp = threadIdx.x >> 5;
     constexpr int kStagePitch = STAGE + STAGE / 32;
     uint32_t* s_stage = s_stage_all + warp * kStagePitch;
-    const uint32_t seg_words = W / (BUCKET_THREADS / 32);
+    const uint32_t seg_words = W / (NT / 32);
     const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
 
     auto fetch = [&](int slot) {  // thread 0
@@ -784,14 +784,14 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
             s_bcnt[slot] = tot[nbk];
         }
     };
-    for (uint32_t i = threadIdx.x; i < W / 32; i += BUCKET_THREADS) s_sum[i] = 0u;
+    for (uint32_t i = threadIdx.x; i < W / 32; i += NT) s_sum[i] = 0u;
     if (threadIdx.x == 0) fetch(0);
     bool dirty = true;  // block-uniform: bitset needs zeroing before the next bucket
     for (unsigned it = 0;; ++it) {
         const int slot = static_cast<int>(it & 1u);
         if (dirty) {  // the previous bucket's readers finished at the loop-end barrier
             uint4* b4 = reinterpret_cast<uint4*>(s_bits);
-            for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = threadIdx.x; i < W / 4; i += NT) b4[i] = make_uint4(0, 0, 0, 0);
         }
         __syncthreads();
         const unsigned b = s_b[slot];
@@ -802,9 +802,9 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         if (sparse)
-            scatter_bucket_keys<true>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
+            scatter_bucket_keys<true, NT>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
         else
-            scatter_bucket_keys<false>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
+            scatter_bucket_keys<false, NT>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
         __syncthreads();
         // phase 1: per-warp popcount of its segment (128-bit SMEM reads; sparse
         // buckets read only the touched words, found through the summary)
@@ -825,9 +825,10 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 2)
         if (lane == 0) s_warp[warp] = c;
         __syncthreads();
         if (warp == 0) {
-            const uint32_t v = s_warp[lane];
+            constexpr unsigned NWARP = NT / 32;
+            const uint32_t v = lane < NWARP ? s_warp[lane] : 0u;
             const uint32_t incl = warp_incl_scan(v, lane);
-            s_warp[lane] = incl - v;
+            if (lane < NWARP) s_warp[lane] = incl - v;
             if (lane == 31 && incl) atomicAdd(&ctrl->total, static_cast<unsigned long long>(incl));
         }
         __syncthreads();
@@ -1203,8 +1204,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (plan.shift >= MAX_BUCKET_SHIFT)
         bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
             parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
-    else  // narrower buckets: a smaller stage lets two CTAs share an SM
-        bucket_sort_kernel<BUCKET_STAGE_SMALL><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
+    else  // narrower buckets: two 512-thread CTAs per SM
+        bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
             parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
@@ -1245,7 +1246,7 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bucket_sort_smem_bytes(20)));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bucket_sort_smem_bytes(19)));
     if (err != cudaSuccess) return err;
     int per = 0;
@@ -1261,8 +1262,8 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
         err = shift >= MAX_BUCKET_SHIFT
                   ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel<BUCKET_STAGE>,
                                                                   BUCKET_THREADS, bucket_sort_smem_bytes(shift))
-                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel<BUCKET_STAGE_SMALL>,
-                                                                  BUCKET_THREADS, bucket_sort_smem_bytes(shift));
+                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_sort_kernel<BUCKET_STAGE, 512>,
+                                                                  512, bucket_sort_smem_bytes(shift));
         if (err != cudaSuccess) return err;
         geo->bucket_blocks[shift] = sms * (per > 0 ? per : 1);
     }

@@ -62,17 +62,19 @@ constexpr int PART_NARROW_THREADS = 512;
 constexpr int PART_NARROW_MAXB = 1024;
 constexpr int BUCKET_THREADS = 1024;
 constexpr int BUCKET_STAGE = 640;        // keys per warp in the extraction stage (2^20 buckets)
-constexpr int BUCKET_STAGE_SMALL = 256;  // narrower buckets: fits two CTAs per SM
 
 constexpr int PART_KPT_SLAB = 20;   // slab KB3 with <= 1024 buckets: 20480-key tiles
 constexpr int PART_DUMP = 32768;    // slab overflow tile (>= any KB3 tile)
 constexpr std::size_t part_smem_bytes(int threads, int maxb, int kpt = PART_KPT) {
     return 2 * std::size_t(threads) * kpt * 4 + std::size_t(maxb + 1) * 16;  // TMA ring + 4 slot arrays
 }
+// KB4 CTA shape per bucket class: 2^20-bit buckets (128 KB bitset) one
+// 1024-thread CTA per SM; narrower buckets 512-thread CTAs, two per SM, so
+// one CTA's scatter (HBM reads) overlaps the other's extraction.
+constexpr int bucket_sort_threads(int shift) { return shift >= MAX_BUCKET_SHIFT ? BUCKET_THREADS : 512; }
 constexpr std::size_t bucket_sort_smem_bytes(int shift) {
-    const int stage = shift >= MAX_BUCKET_SHIFT ? BUCKET_STAGE : BUCKET_STAGE_SMALL;
     return (std::size_t(1) << (shift - 3)) + (std::size_t(1) << (shift - 8)) +  // bitset + summary
-           (BUCKET_THREADS / 32) * (stage + stage / 32) * 4;
+           (bucket_sort_threads(shift) / 32) * (BUCKET_STAGE + BUCKET_STAGE / 32) * 4;
 }
 
 
