@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(NT, 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t W = bm.width >> 5;  // words per bucket bitset (>= 1024; 2^k or a multiple of 4096)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* s_sum = s_bits + W;             // bit w set <=> word w touched (sparse buckets)
@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
                          const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                          uint32_t src_cap, uint32_t* __restrict__ bits, unsigned long long n_words,
                          uint32_t last_mask, Ctrl* __restrict__ ctrl) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t W = bm.width >> 5;
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
     __shared__ unsigned s_b;
