@@ -616,7 +616,8 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             for (int q = 0; q < KPT; ++q) rb[q] = (rb[q] << 16) | atomicAdd(s_cnt + rb[q], 1u);
         }
         __syncthreads();  // A: counts complete; the ring slot is free
-        if (threadIdx.x == 0 && t + 2 < ntiles) load_tile(t + 2, p);
+        // the refill is issued by the last warp: warp 0 is on the scan's critical path
+        if (threadIdx.x == THREADS - 32 && t + 2 < ntiles) load_tile(t + 2, p);
         // padded run starts (multiples of 4) and the slab claims
         uint32_t claim[PER_MAX];
         uint32_t ccnt[PER_MAX];
