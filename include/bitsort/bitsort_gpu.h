@@ -115,9 +115,6 @@ typedef enum bws_path {
 } bws_path;
 BITSORT_API bws_status bws_gpu_set_path(bws_path path);
 
-/* GPUs used by bws_sort in this process (default 1, or env BITSORT_GPUS). */
-BITSORT_API bws_status bws_gpu_set_device_count(int count);
-BITSORT_API int bws_gpu_device_count(void);
 
 /* Number of kernels this library has launched in this process (evidence for
  * bench.py's gpu_launches). */

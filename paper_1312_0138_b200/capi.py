@@ -97,8 +97,6 @@ def _load() -> ctypes.CDLL:
         "bws_gpu_bitset_scan": (i32, [vp, u64, u32, vp, u64, vp, vp]),
         "bws_gpu_set_scatter_mode": (i32, [i32]),
         "bws_gpu_set_path": (i32, [i32]),
-        "bws_gpu_set_device_count": (i32, [i32]),
-        "bws_gpu_device_count": (i32, []),
         "bws_gpu_launch_count": (u64, []),
         "bws_gpu_set_kernel_timing": (i32, [i32]),
         "bws_gpu_kernel_timings": (i32, [ctypes.c_char_p, sz]),
@@ -120,7 +118,7 @@ EXPORTED = (
     "bws_gpu_sort_range_device_async", "bws_gpu_range_split",
     "bws_gpu_bitset_or_gather", "bws_gpu_ipc_get_handle", "bws_gpu_ipc_open", "bws_gpu_ipc_close",
     "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode", "bws_gpu_set_path",
-    "bws_gpu_set_device_count", "bws_gpu_device_count", "bws_gpu_launch_count",
+    "bws_gpu_launch_count",
     "bws_gpu_set_kernel_timing", "bws_gpu_kernel_timings",
     "bws_gpu_shutdown",
 )
@@ -249,14 +247,6 @@ def set_scatter_mode(mode: int) -> None:
 
 def set_path(path: int) -> None:
     _check(lib.bws_gpu_set_path(int(path)))
-
-
-def set_device_count(count: int) -> None:
-    _check(lib.bws_gpu_set_device_count(count))
-
-
-def device_count() -> int:
-    return lib.bws_gpu_device_count()
 
 
 def launch_count() -> int:

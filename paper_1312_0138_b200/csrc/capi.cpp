@@ -4,16 +4,19 @@
 //   wrap()            <- proj/src/capi.cpp:19-41 (exception -> bws_status,
 //                        thread-local message cleared on success)
 //   bws_sort          <- proj/src/capi.cpp:186-197 -> dispatch.hpp:17-55
-//                        (only width 32 / unsigned / bitwise reaches a GPU;
+//                        (width 32, unsigned or signed (XOR bias), bitwise:
 //                        every other combination is BWS_ERROR_CONFIG: there is
 //                        no CPU fallback)
 //   algorithm names   <- proj/src/capi.cpp:164-184, baselines.hpp:24-43
 //
-// Device state: one lazily created context per CUDA device holding a cached
-// 2^32-bit bitset that is all-zero between sorts (K3 clears every word it
-// consumes), the K3 control block + tile-status array, a key staging buffer for
-// host arrays and an internal stream. Calls on one device are serialised by the
-// context mutex; calls on different devices run concurrently.
+// Device state: one lazily created context per CUDA device (the calling
+// thread's current device, or the device owning a device pointer) holding a
+// cached 2^32-bit bitset that is all-zero between sorts (the direct path's K3
+// clears every word it consumes), the control block + tile-status array, the
+// bucket buffer and scratch of the bucketed path, a key staging buffer and
+// pinned bounce buffers for host arrays, and an internal stream. Calls on one
+// device are serialised by the context mutex; calls on different devices run
+// concurrently. Multi-GPU sorting runs one process per GPU (dist.py).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -88,7 +91,6 @@ constexpr size_t kCtrlBytes = sizeof(Ctrl) + 4 * kMaxTiles * sizeof(unsigned lon
 
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_scatter_mode{bws_gpu::kAuto};
-std::atomic<int> g_device_count{0};  // 0 = not yet resolved
 std::atomic<int> g_path{-1};         // bws_path; -1 = not yet read from BITSORT_PATH
 constexpr size_t kBucketedMinKeys = size_t(1) << 21;
 
@@ -969,21 +971,6 @@ bws_status bws_gpu_set_path(bws_path path) {
         if (path < BWS_PATH_AUTO || path > BWS_PATH_BUCKETED) throw config_error("unknown path");
         g_path.store(static_cast<int>(path));
     });
-}
-
-bws_status bws_gpu_set_device_count(int count) {
-    return wrap([&] {
-        if (count < 1) throw config_error("device count must be >= 1");
-        g_device_count.store(count);
-    });
-}
-
-int bws_gpu_device_count(void) {
-    int c = g_device_count.load();
-    if (c > 0) return c;
-    const char* env = std::getenv("BITSORT_GPUS");
-    c = env ? std::atoi(env) : 1;
-    return c > 0 ? c : 1;
 }
 
 uint64_t bws_gpu_launch_count(void) { return g_launches.load(); }
