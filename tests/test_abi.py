@@ -125,6 +125,24 @@ def test_extension_argument_checks():
     assert capi.lib.bws_gpu_set_scatter_mode(7) == capi.Status.ERROR_CONFIG
     assert capi.lib.bws_gpu_bitset_scan(None, 0, 0, None, 0, None, None) == capi.Status.ERROR_DATA
     assert capi.launch_count() >= 0
+    import ctypes
+
+    w = ctypes.c_uint64(0)
+    # range split: parts and range are checked before any device is touched
+    assert capi.lib.bws_gpu_range_split(None, 0, 1 << 20, 0, None, None, ctypes.byref(w), None) == \
+        capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_range_split(None, 0, 0, 2, None, None, ctypes.byref(w), None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_range_split(None, 5, 1 << 20, 2, None, None, ctypes.byref(w), None) == \
+        capi.Status.ERROR_DATA
+    # range sort: [key_lo, key_lo + key_range) must be non-empty and within 2^32
+    assert capi.lib.bws_gpu_sort_range_device_async(None, 0, None, 5, 0, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_sort_range_device_async(None, 0, None, 1 << 31, 1 << 31 | 1, None) == \
+        capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_sort_range_device_async(None, 3, None, 0, 16, None) == capi.Status.ERROR_DATA
+    # OR-gather: 1..8 sources
+    assert capi.lib.bws_gpu_bitset_or_gather(None, 0, 0, None, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_bitset_or_gather(None, 9, 0, None, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_ipc_get_handle(None, None, None) == capi.Status.ERROR_DATA
 
 
 def _has_gpu():
