@@ -1,2 +1,2 @@
-for i in 1; do timeout 300 python bench.py --config C2 --steps 30 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_C2_x.json 2>&1; done
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "C2 or slab or BUCKETED" > gpurun_out/pytest_q.log 2>&1; echo exit=$? >> gpurun_out/pytest_q.log
+for v in "" "BITSORT_TMA_HALF=1"; do env $v timeout 300 python bench.py --config C2 --steps 30 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_C2_$v.json 2>&1; done
+BITSORT_TMA_HALF=1 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "C2 or slab or BUCKETED" > gpurun_out/pytest_q.log 2>&1; echo exit=$? >> gpurun_out/pytest_q.log
