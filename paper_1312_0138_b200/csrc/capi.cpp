@@ -214,7 +214,6 @@ struct DeviceCtx {
         cuda_check(bws_gpu::configure_bucket_kernels(dev, &geo), "bucket kernel configuration");
         cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        cuda_check(cudaMalloc(&bits, kMaxWords * sizeof(uint32_t)), "cudaMalloc(bitset 512 MiB)");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes), "cudaMalloc(control block)");
         cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
         bws_gpu::BucketPlan widest;
@@ -226,6 +225,14 @@ struct DeviceCtx {
         cuda_check(cudaMemset(bucket_scratch, 0, scratch_bytes), "bucket scratch clear");
         bits_dirty = true;
         ready = true;
+    }
+
+    // The direct path's 2^32-bit bitset (512 MiB), allocated on its first use
+    // (bucketed sorts never need it).
+    void ensure_bits() {
+        if (bits) return;
+        cuda_check(cudaMalloc(&bits, kMaxWords * sizeof(uint32_t)), "cudaMalloc(bitset 512 MiB)");
+        bits_dirty = true;
     }
 
     void ensure_keys(size_t n) {
@@ -279,7 +286,7 @@ struct DeviceCtx {
             bounce[i] = nullptr;
             bounce_ev[i] = nullptr;
         }
-        cudaFree(bits);
+        if (bits) cudaFree(bits);
         cudaFree(ctrl_mem);
         if (keys) cudaFree(keys);
         if (parted) cudaFree(parted);
@@ -438,6 +445,7 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
     const bool derived = key_range == 0;
     const uint64_t words = derived ? 0 : (key_range + 31) / 32;
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
+    ctx.ensure_bits();
     if (ctx.bits_dirty) {
         cuda_check(cudaMemsetAsync(ctx.bits, 0, kMaxWords * sizeof(uint32_t), stream),
                    "bitset reset");
