@@ -701,6 +701,16 @@ constexpr std::size_t part_tma_smem_bytes(int maxb) {
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
 // with 4 per thread in flight, tail.
+// 16-byte streaming load that does not allocate in L1: KB4 keeps ~200 KB of
+// SMEM per SM, leaving a small L1 for the loads in flight
+__device__ __forceinline__ uint4 ld_na(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 template <bool SPARSE, int NT = BUCKET_THREADS>
 __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__ src, uint32_t cnt,
                                                     uint32_t key_lo, uint32_t* s_bits,
@@ -722,7 +732,7 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
     for (; i0 + kBatch <= nv; i0 += kBatch) {
         uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(v4 + i0 + u * NT + threadIdx.x);
+        for (int u = 0; u < U; ++u) v[u] = ld_na(v4 + i0 + u * NT + threadIdx.x);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             set_key(v[u].x);
@@ -732,7 +742,7 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
         }
     }
     for (uint32_t i = i0 + threadIdx.x; i < nv; i += NT) {
-        const uint4 v = __ldcs(v4 + i);
+        const uint4 v = ld_na(v4 + i);
         set_key(v.x);
         set_key(v.y);
         set_key(v.z);
