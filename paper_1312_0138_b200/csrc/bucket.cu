@@ -764,7 +764,7 @@ __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__
 // touched words, and zero exactly those words again, so a sparse bucket costs
 // O(keys) SMEM work instead of O(2^shift / 32) and leaves the bitset clean.
 template <int STAGE, int NT = BUCKET_THREADS>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
@@ -779,11 +779,28 @@ __global__ void __launch_bounds__(NT, 2)
     __shared__ unsigned s_b[2];
     __shared__ unsigned long long s_bbase[2];
     __shared__ uint32_t s_bcnt[2];
+    __shared__ __align__(8) unsigned long long s_lbar[2];  // dense scatter: bulk-load ring (full)
+    __shared__ __align__(8) unsigned long long s_ebar[2];  // ... and its slots consumed (NT arrivals)
 
     const unsigned lane = threadIdx.x & 31;
     const unsigned warp = threadIdx.x >> 5;
     constexpr int kStagePitch = STAGE + STAGE / 32;
     uint32_t* s_stage = s_stage_all + warp * kStagePitch;
+    // Dense buckets stream their keys through the (then idle) stage area with
+    // bulk copies: two chunks in flight, no L1 or registers tied up by the
+    // loads (the SMEM bitset + stage leave KB4 a small L1).
+    constexpr uint32_t kChunk = ((NT / 32) * kStagePitch * 4 / 2) / 16 * 4;  // keys per ring slot
+    // (measured: the ring takes C5's packed-layout KB4 from 1025 to 959 us and
+    // makes C2's and C3's slab-layout KB4 2-5% slower, so slab buckets keep
+    // register loads)
+    unsigned chunk_seq = 0;  // bulk chunks this CTA has consumed (block-uniform)
+    if (threadIdx.x == 0) {
+        mbar_init(&s_lbar[0], 1);
+        mbar_init(&s_lbar[1], 1);
+        mbar_init(&s_ebar[0], NT);
+        mbar_init(&s_ebar[1], NT);
+        fence_mbar_init();
+    }
     const uint32_t seg_words = W / (NT / 32);
     const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
 
@@ -812,10 +829,52 @@ __global__ void __launch_bounds__(NT, 2)
         if (threadIdx.x == 0) fetch(slot ^ 1);  // read again only after two more barriers
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
-        if (sparse)
-            scatter_bucket_keys<true, NT>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
-        else
-            scatter_bucket_keys<false, NT>(src, cnt, bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, s_sum);
+        const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
+        if (sparse) {
+            scatter_bucket_keys<true, NT>(src, cnt, key_lo, s_bits, s_sum);
+        } else if (src_cap) {  // slab-layout buckets: register loads measured faster (C2, C3)
+            scatter_bucket_keys<false, NT>(src, cnt, key_lo, s_bits, s_sum);
+        } else {
+            const uint32_t head = min(cnt, static_cast<uint32_t>(
+                                               ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
+            const uint32_t body = (cnt - head) & ~3u;
+            const uint32_t nchunks = (body + kChunk - 1) / kChunk;
+            auto set_key = [&](uint32_t key) {
+                const uint32_t x = key - key_lo;
+                atomicOr(s_bits + (x >> 5), 1u << (x & 31));
+            };
+            auto issue = [&](uint32_t c) {  // thread 0
+                const unsigned g = chunk_seq + c;
+                const uint32_t len = min(kChunk, body - c * kChunk);
+                fence_proxy_async_smem();
+                tma_load_bytes(s_stage_all + (g & 1u) * kChunk, src + head + c * kChunk, len * 4, &s_lbar[g & 1u]);
+            };
+            if (threadIdx.x == 0) {
+                if (nchunks > 0) issue(0);
+                if (nchunks > 1) issue(1);
+            }
+            if (threadIdx.x < head) set_key(__ldcs(src + threadIdx.x));
+            if (threadIdx.x < cnt - head - body) set_key(__ldcs(src + head + body + threadIdx.x));
+            for (uint32_t c = 0; c < nchunks; ++c) {
+                const unsigned g = chunk_seq + c;
+                mbar_wait(&s_lbar[g & 1u], (g >> 1) & 1u);
+                const uint4* r4 = reinterpret_cast<const uint4*>(s_stage_all + (g & 1u) * kChunk);
+                const uint32_t nv = min(kChunk, body - c * kChunk) / 4;
+                for (uint32_t i = threadIdx.x; i < nv; i += NT) {
+                    const uint4 v = r4[i];
+                    set_key(v.x);
+                    set_key(v.y);
+                    set_key(v.z);
+                    set_key(v.w);
+                }
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_ebar[g & 1u])) : "memory");
+                if (threadIdx.x == 0 && c + 2 < nchunks) {  // refill once every thread is done with the slot
+                    mbar_wait(&s_ebar[g & 1u], (g >> 1) & 1u);
+                    issue(c + 2);
+                }
+            }
+            chunk_seq += nchunks;
+        }
         __syncthreads();
         // phase 1: per-warp popcount of its segment (128-bit SMEM reads; sparse
         // buckets read only the touched words, found through the summary)
