@@ -880,10 +880,14 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         // buckets read only the touched words, found through the summary)
         const uint32_t seg = warp * seg_words;
         uint32_t c = 0;
+        uint32_t c_first = 0;  // sparse: this lane's count of its first summary word (reused below)
         if (sparse) {
             for (uint32_t i = lane; i < seg_words / 32; i += 32) {
                 const uint32_t si = seg / 32 + i;
-                for (uint32_t m = s_sum[si]; m; m &= m - 1) c += __popc(s_bits[si * 32 + (__ffs(m) - 1)]);
+                uint32_t ci = 0;
+                for (uint32_t m = s_sum[si]; m; m &= m - 1) ci += __popc(s_bits[si * 32 + (__ffs(m) - 1)]);
+                if (i == lane) c_first = ci;
+                c += ci;
             }
         } else {
             for (uint32_t i = lane; i < seg_words / 4; i += 32) {
@@ -913,8 +917,11 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
             for (uint32_t i0 = 0; i0 < seg_words / 32; i0 += 32) {
                 const uint32_t si = seg / 32 + i0 + lane;
                 uint32_t m = i0 + lane < seg_words / 32 ? s_sum[si] : 0u;
-                uint32_t cl = 0;
-                for (uint32_t mm = m; mm; mm &= mm - 1) cl += __popc(s_bits[si * 32 + (__ffs(mm) - 1)]);
+                uint32_t cl = c_first;  // the first round's counts come from phase 1
+                if (i0 > 0) {
+                    cl = 0;
+                    for (uint32_t mm = m; mm; mm &= mm - 1) cl += __popc(s_bits[si * 32 + (__ffs(mm) - 1)]);
+                }
                 const uint32_t incl = warp_incl_scan(cl, lane);
                 const uint32_t ctot = __shfl_sync(kFull, incl, 31);
                 if (ctot == 0) continue;
