@@ -898,15 +898,16 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         c = __reduce_add_sync(kFull, c);
         if (lane == 0) s_warp[warp] = c;
         __syncthreads();
-        if (warp == 0) {
+        // every warp scans the (<= 32) segment counts itself: no second barrier
+        uint32_t wprefix;
+        {
             constexpr unsigned NWARP = NT / 32;
             const uint32_t v = lane < NWARP ? s_warp[lane] : 0u;
             const uint32_t incl = warp_incl_scan(v, lane);
-            if (lane < NWARP) s_warp[lane] = incl - v;
-            if (lane == 31 && incl) atomicAdd(&ctrl->total, static_cast<unsigned long long>(incl));
+            wprefix = __shfl_sync(kFull, incl - v, warp);
+            if (warp == 0 && lane == 31 && incl) atomicAdd(&ctrl->total, static_cast<unsigned long long>(incl));
         }
-        __syncthreads();
-        uint32_t* o = out + base + s_warp[warp];
+        uint32_t* o = out + base + wprefix;
         // output keys: bucket base + bit index, mapped back by the XOR (signed sorts use
         // power-of-two widths, so no bucket straddles 2^31 and the XOR commutes with the add)
         const uint32_t key_hi = (bm.lo + static_cast<uint32_t>(b) * bm.width) ^ bm.xr;
