@@ -415,13 +415,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             const uint32_t incl = warp_incl_scan(local, lane);
             if (lane == 31) s_scratch[warp] = incl;
             __syncthreads();
-            if (warp == 0) {
+            uint32_t run;
+            {  // every warp scans the warp totals itself (one barrier less per tile)
                 const uint32_t w = lane < NWARPS ? static_cast<uint32_t>(s_scratch[lane]) : 0u;
                 const uint32_t wi = warp_incl_scan(w, lane);
-                if (lane < NWARPS) s_scratch[lane] = wi - w;
+                run = __shfl_sync(kFull, wi - w, warp) + (incl - local);
             }
-            __syncthreads();
-            uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
             if constexpr (SLAB) {
 #pragma unroll
                 for (int q = 0; q < PER_MAX; ++q) {
@@ -628,13 +627,12 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             const uint32_t incl = warp_incl_scan(local, lane);
             if (lane == 31) s_scratch[warp] = incl;
             __syncthreads();
-            if (warp == 0) {
+            uint32_t run;
+            {  // every warp scans the warp totals itself (one barrier less per tile)
                 const uint32_t w = lane < NWARPS ? static_cast<uint32_t>(s_scratch[lane]) : 0u;
                 const uint32_t wi = warp_incl_scan(w, lane);
-                if (lane < NWARPS) s_scratch[lane] = wi - w;
+                run = __shfl_sync(kFull, wi - w, warp) + (incl - local);
             }
-            __syncthreads();
-            uint32_t run = static_cast<uint32_t>(s_scratch[warp]) + (incl - local);
 #pragma unroll
             for (int q = 0; q < PER_MAX; ++q) {
                 const int b = sb + q;
