@@ -521,6 +521,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
     uint32_t* s_sorted = s_ring + 2 * TILE;                     // TILE + 4 * kSlots (runs 16B-aligned)
     uint32_t* s_cnt = s_sorted + TILE + 4 * kSlots;             // keys per bucket in the tile
     uint32_t* s_start = s_cnt + kSlots;                         // run start in s_sorted (multiple of 4)
+    // 16 copies of every run start (16-bit): lane l reads copy l & 15, so a
+    // warp's 32 random lookups spread over 8x more banks than one copy allows
+    uint16_t* s_start16 =
+        reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(s_start + kSlots) + 15) & ~uintptr_t(15));
     __shared__ unsigned long long s_scratch[33];
     __shared__ __align__(8) unsigned long long s_bar[2];
     __shared__ uint32_t s_last;
@@ -645,6 +649,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
                     } else {
                         s_start[b] = run;
                         if (cb) {
+                            uint4 rep;  // 8 x 16-bit copies
+                            rep.x = rep.y = rep.z = rep.w = run | (run << 16);
+                            reinterpret_cast<uint4*>(s_start16 + 16 * b)[0] = rep;
+                            reinterpret_cast<uint4*>(s_start16 + 16 * b)[1] = rep;
                             const uint32_t pc = (cb + 3u) & ~3u;
                             claim[q] = atomicAdd(sa.gcnt + b, pc);
                             atomicAdd(sa.gtrue + b, cb);
@@ -664,7 +672,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < KPT; ++q) {
             const uint32_t b = rb[q] >> 16;
-            if (b != spill) s_sorted[s_start[b] + (rb[q] & 0xffffu)] = k[q];
+            if (b != spill) s_sorted[s_start16[(b << 4) | (lane & 15u)] + (rb[q] & 0xffffu)] = k[q];
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk copies
         __syncthreads();  // C
@@ -692,7 +700,8 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
 }
 
 constexpr std::size_t part_tma_smem_bytes(int maxb) {
-    return (2 * std::size_t(PART_TILE) + PART_TILE + 4 * std::size_t(maxb + 1) + 2 * std::size_t(maxb + 1)) * 4;
+    return (2 * std::size_t(PART_TILE) + PART_TILE + 4 * std::size_t(maxb + 1) + 2 * std::size_t(maxb + 1) +
+            8 * std::size_t(maxb + 1) + 4) * 4;  // ... + 16 x 16-bit start copies (16B-aligned)
 }
 
 
@@ -1216,8 +1225,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.g_base = base;
         if (timer) timer->before(stream);
         if (sa.gtrue)
-            bucket_partition_tma_kernel<PART_NARROW_MAXB>
-                <<<P, PART_THREADS, part_tma_smem_bytes(PART_NARROW_MAXB), stream>>>(ks, plan.map, plan.nb, parted, sa);
+            bucket_partition_tma_kernel<512>
+                <<<P, PART_THREADS, part_tma_smem_bytes(512), stream>>>(ks, plan.map, plan.nb, parted, sa);
         else if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
@@ -1302,8 +1311,8 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_tma_kernel<PART_NARROW_MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(part_tma_smem_bytes(PART_NARROW_MAXB)));
+    err = cudaFuncSetAttribute(bucket_partition_tma_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_tma_smem_bytes(512)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
