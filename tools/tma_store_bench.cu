@@ -3,7 +3,7 @@
 // Each CTA fills a 80 KB SMEM buffer, then repeatedly issues `runs` bulk
 // stores of `bytes` each (run i -> a different 2 MB-strided global region),
 // waits for their SMEM reads, and repeats. Reports GB/s and copies/s.
-// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tma_store_bench tma_store_bench.cu
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/bin/tma_store_bench tools/tma_store_bench.cu
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
