@@ -1,0 +1,90 @@
+"""`bitsort sort` (tools/bitsort_cli.cpp): the reference CLI's sort subcommand
+(proj/tools/main.cpp:97-144, :206-223) over the B200 library. Parsing,
+option and exit-status behaviour run on CPU; sorting needs the GPU.
+"""
+from __future__ import annotations
+
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+CLI = ROOT / "paper_1312_0138_b200" / "lib" / "bitsort"
+
+
+def run(args, stdin=None):
+    return subprocess.run([str(CLI), *args], input=stdin, capture_output=True, text=True)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not CLI.exists():
+        pytest.skip("bitsort CLI not built (run __graft_entry__.build())")
+
+
+def test_parse_errors_report_file_and_line(tmp_path):
+    f = tmp_path / "in.txt"
+    f.write_text("5\n# comment\n\n  7 \nseven\n")
+    r = run(["sort", str(f)])
+    assert r.returncode == 2  # main.cpp:20-31: data errors exit 2
+    assert f"{f}:5: cannot parse 'seven' as an integer" in r.stderr
+    r = run(["sort", "-"], stdin="1\n-2147483649\n")
+    assert r.returncode == 2 and "<stdin>:2: value -2147483649 out of range for signed 32-bit" in r.stderr
+    r = run(["sort", "-", "--unsigned"], stdin="4294967296\n")
+    assert r.returncode == 2 and "out of range for unsigned 32-bit" in r.stderr
+
+
+def test_usage_and_config_errors(tmp_path):
+    assert run([]).returncode == 1
+    assert run(["bits", "5"]).returncode == 1
+    assert run(["sort"]).returncode == 1
+    f = tmp_path / "in.txt"
+    f.write_text("3\n1\n")
+    r = run(["sort", str(f), "--width", "16"])
+    assert r.returncode == 1 and "width 32" in r.stderr
+    r = run(["sort", str(f), "--algorithm", "nonsense"])
+    assert r.returncode == 1 and "unknown algorithm" in r.stderr
+    assert run(["sort", str(f), "--bogus"]).returncode == 1
+
+
+def _has_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU behaviour")
+def test_no_device_is_an_error(tmp_path):
+    f = tmp_path / "in.txt"
+    f.write_text("3\n1\n")
+    r = run(["sort", str(f)])
+    assert r.returncode == 1 and "no CPU fallback" in r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("signed", [True, False])
+def test_sort_file_on_gpu(tmp_path, signed):
+    rng = np.random.default_rng(3)
+    if signed:
+        keys = np.unique(rng.integers(-(1 << 31), 1 << 31, size=300_000, dtype=np.int64))
+    else:
+        keys = np.unique(rng.integers(0, 1 << 32, size=300_000, dtype=np.uint64))
+    keys = rng.permutation(keys)
+    f = tmp_path / "in.txt"
+    f.write_text("# header\n" + "\n".join(str(int(k)) for k in keys) + "\n\n")
+    out = tmp_path / "out.txt"
+    args = ["sort", str(f), "--out", str(out), "--threads", "4"] + ([] if signed else ["--unsigned"])
+    r = run(args)
+    assert r.returncode == 0, r.stderr
+    got = [int(x) for x in out.read_text().split()]
+    assert got == sorted(int(k) for k in keys)
+    # stdin -> stdout, and duplicates are a data error (exit 2)
+    r = run(["sort", "-"] + ([] if signed else ["--unsigned"]), stdin="3\n1\n2\n")
+    assert r.returncode == 0 and r.stdout == "1\n2\n3\n"
+    r = run(["sort", "-"], stdin="3\n1\n3\n")
+    assert r.returncode == 2 and "distinct" in r.stderr
