@@ -1167,8 +1167,10 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
     // bucket per tile (KB3 CTAs <= 1024) plus the head/tail claims
     if (tma_store_kb3(plan)) cap += 3 * (static_cast<uint64_t>(n) / PART_TILE + 1024 + 8);
     const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_DUMP;  // + dump tile
-    // the slab trades memory (up to 4.5 slots per key) for the histogram pass
-    if (slots > 4 * static_cast<uint64_t>(n) + n / 2 + PART_DUMP || slots >= (1ull << 32)) return 0;
+    // the slab trades memory (up to 4.5 slots per key, or 256 MiB for small
+    // sorts) for the histogram pass
+    const bool small = slots * 4 <= (uint64_t(256) << 20);
+    if ((!small && slots > 4 * static_cast<uint64_t>(n) + n / 2 + PART_DUMP) || slots >= (1ull << 32)) return 0;
     return slots;
 }
 
