@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
 
         uint32_t k[KPT];
         uint32_t rb[KPT];  // bucket << 16 | rank inside the bucket (rank < TILE)
-        uint32_t kmin = 0xffffffffu, kmax = 0;
+        uint32_t rmin = 0xffffffffu, rmax = 0;  // over key - lo
         bool all_in = true;
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
@@ -601,13 +601,27 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 k[4 * j + q] = kk[q];
-                rb[4 * j + q] = slot_of(kk[q], in);
-                kmin = min(kmin, kk[q]);
-                kmax = max(kmax, kk[q]);
+                rmin = min(rmin, kk[q] - bm.lo);
+                rmax = max(rmax, kk[q] - bm.lo);
             }
         }
-        const uint32_t blo = slot_of(__reduce_min_sync(kFull, kmin), true);
-        const uint32_t bhi = slot_of(__reduce_max_sync(kFull, kmax), true);
+        rmin = __reduce_min_sync(kFull, rmin);
+        rmax = __reduce_max_sync(kFull, rmax);
+        // a warp step with every key in range (and no padding lanes) needs no
+        // per-key range check: the common case
+        if (__all_sync(kFull, all_in) && rmax <= last) {
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) rb[q] = __umulhi(((k[q] - bm.lo) >> bm.ms) << 12, bm.mq);
+        } else {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const bool in = j * THREADS + threadIdx.x < nvec;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rb[4 * j + q] = slot_of(k[4 * j + q], in);
+            }
+        }
+        const uint32_t blo = slot_of(rmin + bm.lo, true);
+        const uint32_t bhi = slot_of(rmax + bm.lo, true);
         if (blo == bhi && __all_sync(kFull, all_in)) {
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(s_cnt + blo, 32u * KPT);
