@@ -300,6 +300,11 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     // layout, which has no KB1 to count them) keys beyond the range, so the
     // spill count of a tile gives the out-of-range keys for free.
     const uint32_t last = SLAB && sa.check ? sa.limit - 1u : 0xffffffffu;
+    // largest key - lo that maps to a real bucket under slot_of: the slab's
+    // range limit, or (packed layout) the end of the last bucket
+    const uint64_t bucket_end = static_cast<uint64_t>(nb) * bm.width;
+    const uint32_t fast_last = SLAB ? last : (bucket_end > 0xffffffffull ? 0xffffffffu
+                                                                         : static_cast<uint32_t>(bucket_end - 1));
     auto slot_of = [&](uint32_t key, bool in) -> uint32_t {
         if constexpr (SLAB) return in && key - bm.lo <= last ? bucket_id(key, bm) : spill;
         else return bucket_or_spill(key, in, bm, nb);
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 
         uint32_t k[KPT];
         uint32_t rb[KPT];  // bucket << 16 | rank inside the bucket (rank < TILE)
-        uint32_t kmin = 0xffffffffu, kmax = 0;
+        uint32_t rmin = 0xffffffffu, rmax = 0;  // over key - lo
         bool all_in = true;
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
@@ -387,13 +392,27 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 k[4 * j + q] = kk[q];
-                rb[4 * j + q] = slot_of(kk[q], in);
-                kmin = min(kmin, kk[q]);
-                kmax = max(kmax, kk[q]);
+                rmin = min(rmin, kk[q] - bm.lo);
+                rmax = max(rmax, kk[q] - bm.lo);
             }
         }
-        const uint32_t blo = slot_of(__reduce_min_sync(kFull, kmin), true);
-        const uint32_t bhi = slot_of(__reduce_max_sync(kFull, kmax), true);
+        rmin = __reduce_min_sync(kFull, rmin);
+        rmax = __reduce_max_sync(kFull, rmax);
+        // every key of the warp step below the fast limit (and no padding
+        // lanes): buckets without per-key range checks
+        if (__all_sync(kFull, all_in) && rmax <= fast_last) {
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) rb[q] = __umulhi(((k[q] - bm.lo) >> bm.ms) << 12, bm.mq);
+        } else {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const bool in = j * THREADS + threadIdx.x < nvec;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rb[4 * j + q] = slot_of(k[4 * j + q], in);
+            }
+        }
+        const uint32_t blo = slot_of(rmin + bm.lo, true);
+        const uint32_t bhi = slot_of(rmax + bm.lo, true);
         if (blo == bhi && __all_sync(kFull, all_in)) {
             // the whole warp step lies in one bucket: one atomic, ranks by lane
             uint32_t base = 0;
