@@ -113,6 +113,11 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
     const size_t vhi = clo + (chi - clo) * (part + 1) / HIST_SPLIT;
     const unsigned lane = threadIdx.x & 31;
     uint32_t mx = 0, bad = 0;
+    // largest key - lo that is in range and in a real bucket (fast path bound)
+    const uint64_t bucket_end = static_cast<uint64_t>(nb) * bm.width;
+    uint64_t fl = bucket_end - 1;
+    if (check && limit - 1ull < fl) fl = limit - 1ull;
+    const uint32_t fast_last = fl > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(fl);
     constexpr int U = 4;  // uint4 per thread per step: 16 keys
     const size_t step = static_cast<size_t>(blockDim.x) * U;
     // software pipelined: the next step's loads are in flight while this
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
             vn[u] = inn[u] ? __ldcs(ks.body + i) : make_uint4(0, 0, 0, 0);
         }
         uint32_t bk[U * 4];
-        uint32_t kmin = 0xffffffffu, kmax = 0;
+        uint32_t rmin = 0xffffffffu, rmax = 0;  // over key - lo
         bool all_in = true;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -143,22 +148,37 @@ __global__ void __launch_bounds__(BUCKET_HIST_THREADS)
             all_in &= in[u];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                bk[u * 4 + q] = bucket_or_spill(kk[q], in[u], bm, nb);
-                kmin = min(kmin, in[u] ? kk[q] : 0xffffffffu);
-                kmax = max(kmax, in[u] ? kk[q] : 0u);
-                bad += (check && in[u] && kk[q] - bm.lo >= limit) ? 1u : 0u;
+                bk[u * 4 + q] = kk[q];
+                rmin = min(rmin, kk[q] - bm.lo);
+                rmax = max(rmax, kk[q] - bm.lo);
             }
         }
-        mx = max(mx, kmax);
-        const uint32_t wlo = __reduce_min_sync(kFull, kmin);
-        const uint32_t whi = __reduce_max_sync(kFull, kmax);
-        const uint32_t blo = bucket_or_spill(wlo, true, bm, nb);
-        if (blo == bucket_or_spill(whi, true, bm, nb) && __all_sync(kFull, all_in)) {
-            // sorted / clustered input: one bucket for the whole warp step
-            if (lane == 0) atomicAdd(s_h + blo, 32u * U * 4);
-        } else {
+        rmin = __reduce_min_sync(kFull, rmin);
+        rmax = __reduce_max_sync(kFull, rmax);
+        if (__all_sync(kFull, all_in) && rmax <= fast_last) {
+            // every key in range and in a real bucket: no per-key checks
+            mx = max(mx, rmax + bm.lo);
+            const uint32_t blo = __umulhi((rmin >> bm.ms) << 12, bm.mq);
+            if (blo == __umulhi((rmax >> bm.ms) << 12, bm.mq)) {
+                // sorted / clustered input: one bucket for the whole warp step
+                if (lane == 0) atomicAdd(s_h + blo, 32u * U * 4);
+            } else {
 #pragma unroll
-            for (int q = 0; q < U * 4; ++q) atomicAdd(s_h + bk[q], 1u);
+                for (int q = 0; q < U * 4; ++q) atomicAdd(s_h + __umulhi(((bk[q] - bm.lo) >> bm.ms) << 12, bm.mq), 1u);
+            }
+        } else {
+            uint32_t kmax = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t kq = bk[u * 4 + q];
+                    kmax = max(kmax, in[u] ? kq : 0u);
+                    bad += (check && in[u] && kq - bm.lo >= limit) ? 1u : 0u;
+                    atomicAdd(s_h + bucket_or_spill(kq, in[u], bm, nb), 1u);
+                }
+            }
+            mx = max(mx, kmax);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
