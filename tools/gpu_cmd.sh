@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
-for c in C4 C5; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${c}_hf.json 2>&1; done
+timeout 900 python bench.py --config all --steps 20 --warmup 3 > gpurun_out/bench_all_v8.jsonl 2> gpurun_out/bench_all_v8.err
+timeout 300 python bench.py > gpurun_out/bench_default.json 2>&1
