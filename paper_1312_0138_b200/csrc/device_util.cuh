@@ -72,11 +72,27 @@ __device__ __forceinline__ void stage_bits(uint32_t x, uint32_t kb, uint32_t& p,
     }
 }
 
-// Copies `count` staged keys to o[0, count) with coalesced stores.
+// Copies `count` staged keys to o[0, count) with coalesced stores. Staged key
+// i = lane + 32 r sits at stage[lane + 33 r] (one pad word per 32), so both
+// sides advance by a constant stride: no per-key index arithmetic.
 __device__ __forceinline__ void drain_stage(const uint32_t* stage, uint32_t count,
                                             uint32_t* __restrict__ o, unsigned lane) {
     __syncwarp();
-    for (uint32_t i = lane; i < count; i += 32) __stcs(o + i, stage[i + (i >> 5)]);
+    const uint32_t* sp = stage + lane;
+    uint32_t* gp = o + lane;
+    const uint32_t rows = count >> 5;  // full rows of 32 keys
+    uint32_t r = 0;
+#pragma unroll 1
+    for (; r + 4 <= rows; r += 4, sp += 4 * 33, gp += 4 * 32) {
+        const uint32_t a = sp[0], b = sp[33], c = sp[66], d = sp[99];
+        __stcs(gp, a);
+        __stcs(gp + 32, b);
+        __stcs(gp + 64, c);
+        __stcs(gp + 96, d);
+    }
+#pragma unroll 1
+    for (; r < rows; ++r, sp += 33, gp += 32) __stcs(gp, sp[0]);
+    if (lane < (count & 31u)) __stcs(gp, sp[0]);
     __syncwarp();
 }
 

@@ -1,2 +1,2 @@
-timeout 900 python bench.py --config all --steps 20 --warmup 3 > gpurun_out/bench_all_v8.jsonl 2> gpurun_out/bench_all_v8.err
-timeout 300 python bench.py > gpurun_out/bench_default.json 2>&1
+timeout 900 python -m pytest tests -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+for c in C2 C3 C1; do timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${c}_dr.json 2>&1; done
