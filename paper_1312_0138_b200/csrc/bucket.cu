@@ -562,8 +562,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
     uint32_t* s_start = s_cnt + kSlots;                         // run start in s_sorted (multiple of 4)
     // 16 copies of every run start (16-bit): lane l reads copy l & 15, so a
     // warp's 32 random lookups spread over 8x more banks than one copy allows
-    uint16_t* s_start16 =
-        reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(s_start + kSlots) + 15) & ~uintptr_t(15));
+    // (offset from the 128-byte-aligned SMEM base rounded up to 16 bytes at
+    // compile time: no integer round trip, so the compiler keeps LDS addressing)
+    constexpr int kStart16Words = (3 * TILE + 6 * kSlots + 3) & ~3;
+    uint16_t* s_start16 = reinterpret_cast<uint16_t*>(reinterpret_cast<uint32_t*>(smem_raw) + kStart16Words);
     __shared__ unsigned long long s_scratch[33];
     __shared__ __align__(8) unsigned long long s_bar[2];
     __shared__ uint32_t s_last;
