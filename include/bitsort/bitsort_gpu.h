@@ -84,6 +84,18 @@ BITSORT_API bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_word
 #define BWS_GPU_IPC_HANDLE_BYTES 64
 BITSORT_API bws_status bws_gpu_bitset_or_gather(const uint32_t* const* srcs, int nsrc, uint64_t n_words,
                                                 uint32_t* dst, void* stream);
+/* The exchange fused into the scan: bws_gpu_bitset_scan over the virtual
+ * slice OR_s srcs[s][0, n_words) (srcs[0] the local bitset's slice, the rest
+ * peers' slices opened through CUDA IPC). One kernel: every scan tile ORs the
+ * peers' words (16-byte loads over NVLink/NVSwitch) into its shared-memory
+ * copy of the local words, so no gathered slice is written to HBM and read
+ * back. Same outputs and d_total as bws_gpu_bitset_or_gather followed by
+ * bws_gpu_bitset_scan. Sources not 16-byte aligned take exactly that
+ * two-kernel route. */
+BITSORT_API bws_status bws_gpu_bitset_scan_sources(const uint32_t* const* srcs, int nsrc,
+                                                   uint64_t n_words, uint32_t key_base,
+                                                   uint32_t* out, uint64_t out_capacity,
+                                                   uint64_t* d_total, void* stream);
 /* handle_out: BWS_GPU_IPC_HANDLE_BYTES bytes naming dev_ptr's allocation;
  * *offset_out: dev_ptr's byte offset in it (add it to the pointer
  * bws_gpu_ipc_open returns in the peer process). */

@@ -966,6 +966,69 @@ bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t 
     });
 }
 
+bws_status bws_gpu_bitset_scan_sources(const uint32_t* const* srcs, int nsrc, uint64_t n_words,
+                                       uint32_t key_base, uint32_t* out, uint64_t out_capacity,
+                                       uint64_t* d_total, void* stream) {
+    return wrap([&] {
+        if (nsrc < 1 || nsrc > bws_gpu::MAX_OR_SOURCES) throw std::out_of_range("nsrc must be in [1, 8]");
+        if (d_total == nullptr) throw data_error("null total pointer");
+        if (n_words > 0 && (srcs == nullptr || out == nullptr)) throw data_error("null device pointer");
+        if (n_words > kMaxWords) throw std::out_of_range("slice exceeds 2^27 words");
+        bws_gpu::OrSources os{};
+        os.n = nsrc;
+        bool aligned = true;
+        for (int i = 0; i < nsrc; ++i) {
+            if (n_words > 0 && srcs[i] == nullptr) throw data_error("null source pointer");
+            os.p[i] = srcs[i];
+            aligned &= bws_gpu::scan2_supported(srcs[i]);
+        }
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (n_words == 0) {
+            cuda_check(cudaMemsetAsync(d_total, 0, sizeof(uint64_t), s), "total reset");
+            return;
+        }
+        const size_t tiles = bws_gpu::scan_tiles(n_words);
+        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl) + tiles * sizeof(unsigned long long), s),
+                   "control block reset");
+        if (aligned) {
+            // one kernel: the peers' words are ORed into the scan's SMEM tiles
+            cuda_check(timed_launch("bitset_scan_sources", s,
+                                    [&] {
+                                        return bws_gpu::launch_scan2_sources(
+                                            os, n_words, key_base, out, out_capacity, ctx.ctrl(),
+                                            ctx.status(), reinterpret_cast<unsigned long long*>(d_total),
+                                            ctx.geo, s);
+                                    }),
+                       "bitset_scan_sources launch");
+            g_launches.fetch_add(1);
+        } else {
+            // a source not 16-byte aligned (no TMA / vector loads): OR-gather
+            // into a stream-ordered temporary, then the plain scan
+            void* tmp = nullptr;
+            cuda_check(cudaMallocAsync(&tmp, n_words * sizeof(uint32_t), s), "slice allocation");
+            uint32_t* slice = static_cast<uint32_t*>(tmp);
+            cudaError_t err = timed_launch("bitset_or_gather", s, [&] {
+                return bws_gpu::launch_or_gather(os, slice, n_words, ctx.geo, s);
+            });
+            if (err == cudaSuccess)
+                err = timed_launch("bitset_scan", s, [&] {
+                    return launch_scan_any(slice, n_words, key_base, out, out_capacity, ctx.ctrl(),
+                                           ctx.status(), reinterpret_cast<unsigned long long*>(d_total),
+                                           /*clear=*/0, ctx.geo, s);
+                });
+            cudaFreeAsync(tmp, s);
+            cuda_check(err, "or_gather + bitset_scan launch");
+            g_launches.fetch_add(2);
+        }
+        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+    });
+}
+
 bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode) {
     return wrap([&] {
         if (mode < BWS_SCATTER_AUTO || mode > BWS_SCATTER_SMEM)

@@ -218,6 +218,14 @@ struct OrSources {
 };
 cudaError_t launch_or_gather(const OrSources& srcs, std::uint32_t* dst, std::uint64_t n_words,
                              const LaunchGeometry& geo, cudaStream_t stream);
+// K3 v2 over the OR of srcs (the fused P2P exchange + scan): same contract as
+// launch_scan2 (lookback variant, no clearing) on the virtual bitset
+// OR_s srcs.p[s][0, n_words); every source 16-byte aligned (scan2_supported).
+// srcs.p[0] (the local slice) arrives by TMA, peers by 16-byte loads.
+cudaError_t launch_scan2_sources(const OrSources& srcs, std::uint64_t n_words, std::uint32_t key_base,
+                                 std::uint32_t* out, std::uint64_t out_capacity, Ctrl* ctrl,
+                                 unsigned long long* status, unsigned long long* d_total,
+                                 const LaunchGeometry& geo, cudaStream_t stream);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream, std::uint32_t xr = 0);

@@ -221,11 +221,18 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
-template <bool CLEAR, bool PRECOUNT>
+// MULTI: the scanned bitset is the OR of srcs.p[0 .. srcs.n) (bits == srcs.p[0],
+// the local one, arrives by TMA; the others — peer GPUs' memory over
+// NVLink/NVSwitch through CUDA IPC — are loaded with 16-byte loads while that
+// copy is in flight and ORed into the SMEM tile). This fuses the multi-GPU
+// exchange into the scan: no gathered slice is written or re-read.
+template <bool CLEAR, bool PRECOUNT, bool MULTI = false>
 __global__ void __launch_bounds__(SCAN2_THREADS, 2)
     scan2_kernel(uint32_t* __restrict__ bits, unsigned long long n_words_param, uint32_t key_base,
                  uint32_t* __restrict__ out, unsigned long long out_cap, Ctrl* __restrict__ ctrl,
-                 unsigned long long* __restrict__ status, unsigned long long* __restrict__ d_total) {
+                 unsigned long long* __restrict__ status, unsigned long long* __restrict__ d_total,
+                 OrSources srcs = OrSources{}) {
+    static_assert(!(MULTI && (CLEAR || PRECOUNT)), "the source-OR scan is lookback-only and read-only");
     constexpr int NW = SCAN2_THREADS / 32;
     constexpr uint32_t kSeg = SCAN2_TILE_WORDS / NW;  // words per warp segment (512)
     constexpr int kPitch = SCAN2_STAGE + SCAN2_STAGE / 32;
@@ -294,11 +301,56 @@ __global__ void __launch_bounds__(SCAN2_THREADS, 2)
         const unsigned long long w0 = static_cast<unsigned long long>(tile) * SCAN2_TILE_WORDS;
         const uint32_t len = static_cast<uint32_t>(min(static_cast<unsigned long long>(SCAN2_TILE_WORDS), n_words - w0));
         uint32_t* t32 = s_tiles + slot * SCAN2_TILE_WORDS;
+        constexpr int kPV = SCAN2_TILE_WORDS / 4 / SCAN2_THREADS;  // uint4 per thread per tile
+        uint4 acc[kPV];
+        uint32_t acc_tail = 0u;
+        if (MULTI) {
+            // the other sources' words of this tile, ORed in registers while
+            // the local copy is in flight (one round trip per source)
+            const uint32_t nv = len >> 2;
+#pragma unroll
+            for (int k = 0; k < kPV; ++k) acc[k] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int s = 1; s < MAX_OR_SOURCES; ++s) {  // static indices: srcs stays in param space
+                if (s >= srcs.n) break;
+                const uint4* p4 = reinterpret_cast<const uint4*>(srcs.p[s] + w0);
+                uint4 v[kPV];
+#pragma unroll
+                for (int k = 0; k < kPV; ++k) {
+                    const uint32_t i = threadIdx.x + k * SCAN2_THREADS;
+                    v[k] = i < nv ? __ldcs(p4 + i) : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int k = 0; k < kPV; ++k) {
+                    acc[k].x |= v[k].x;
+                    acc[k].y |= v[k].y;
+                    acc[k].z |= v[k].z;
+                    acc[k].w |= v[k].w;
+                }
+                if (threadIdx.x < (len & 3u)) acc_tail |= srcs.p[s][w0 + (len & ~3u) + threadIdx.x];
+            }
+        }
         mbar_wait(&s_bar[slot], s_par[slot]);
         // tail words (< 4) the bulk copy did not cover; zero padding past the end
         if (threadIdx.x < 4) {
             const uint32_t i = (len & ~3u) + threadIdx.x;
-            if (i < SCAN2_TILE_WORDS) t32[i] = i < len ? bits[w0 + i] : 0u;
+            if (i < SCAN2_TILE_WORDS) t32[i] = i < len ? (bits[w0 + i] | acc_tail) : 0u;
+        }
+        if (MULTI) {
+            uint4* t4 = reinterpret_cast<uint4*>(t32);
+            const uint32_t nv = len >> 2;
+#pragma unroll
+            for (int k = 0; k < kPV; ++k) {
+                const uint32_t i = threadIdx.x + k * SCAN2_THREADS;
+                if (i < nv) {
+                    uint4 t = t4[i];
+                    t.x |= acc[k].x;
+                    t.y |= acc[k].y;
+                    t.z |= acc[k].z;
+                    t.w |= acc[k].w;
+                    t4[i] = t;
+                }
+            }
         }
         if (len < SCAN2_TILE_WORDS)
             for (uint32_t i = (len & ~3u) + 4 + threadIdx.x; i < SCAN2_TILE_WORDS; i += SCAN2_THREADS) t32[i] = 0u;
@@ -383,6 +435,19 @@ __global__ void __launch_bounds__(SCAN2_THREADS, 2)
 
 }  // namespace
 
+cudaError_t launch_scan2_sources(const OrSources& srcs, uint64_t n_words, uint32_t key_base, uint32_t* out,
+                                 uint64_t out_capacity, Ctrl* ctrl, unsigned long long* status,
+                                 unsigned long long* d_total, const LaunchGeometry& geo,
+                                 cudaStream_t stream) {
+    if (n_words == 0) return cudaSuccess;
+    int blocks = geo.scan2_blocks;
+    const uint64_t tiles = (n_words + SCAN2_TILE_WORDS - 1) / SCAN2_TILE_WORDS;
+    if (tiles < static_cast<uint64_t>(blocks)) blocks = static_cast<int>(tiles);
+    scan2_kernel<false, false, true><<<blocks, SCAN2_THREADS, scan2_smem_bytes(), stream>>>(
+        const_cast<uint32_t*>(srcs.p[0]), n_words, key_base, out, out_capacity, ctrl, status, d_total, srcs);
+    return cudaGetLastError();
+}
+
 bool scan2_supported(const uint32_t* bits) { return (reinterpret_cast<uintptr_t>(bits) & 15) == 0; }
 
 cudaError_t configure_scan2(int device, LaunchGeometry* geo) {
@@ -391,7 +456,7 @@ cudaError_t configure_scan2(int device, LaunchGeometry* geo) {
     if (err != cudaSuccess) return err;
     const int smem = static_cast<int>(scan2_smem_bytes());
     for (auto k : {scan2_kernel<true, false>, scan2_kernel<false, false>, scan2_kernel<true, true>,
-                   scan2_kernel<false, true>}) {
+                   scan2_kernel<false, true>, scan2_kernel<false, false, true>}) {
         err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
     }

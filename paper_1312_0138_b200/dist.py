@@ -11,11 +11,13 @@ Rank r of G holds an input-position shard of the keys. Each rank
      so the total only drops) -> BWS_ERROR_DATA.
 The global sorted array is the rank-order concatenation of the local outputs.
 
-Peer-to-peer variant (``distributed_sort_p2p``, NVLink/NVSwitch node): step 2
-is a custom collective instead of NCCL — every rank exports its full bitset
-through CUDA IPC, and after a cross-rank barrier ORs its own slice of all G
-bitsets straight out of the peers' memory (bws_gpu_bitset_or_gather), then
-scans it. OR is exact on distinct keys and only loses bits on duplicates.
+Peer-to-peer variant (``distributed_sort_p2p``, NVLink/NVSwitch node): steps 2
+and 3 become ONE kernel instead of NCCL + scan — every rank exports its full
+bitset through CUDA IPC, and after a cross-rank barrier scans its own slice of
+the OR of all G bitsets, the scan's tiles reading the peers' words straight
+out of their memory over NVLink (bws_gpu_bitset_scan_sources): no gathered
+slice is written to HBM or read back. OR is exact on distinct keys and only
+loses bits on duplicates.
 
 Key all-to-all variant (``distributed_sort_a2a``): rank r
 splits its shard by destination key range (range split, C ABI), the ranks
@@ -62,6 +64,11 @@ class RankOps(Protocol):
     def or_gather(self, sources, word_lo: int, n_words: int) -> torch.Tensor:
         """OR of words [word_lo, word_lo + n_words) over all sources (local
         tensor or imported peers)."""
+
+    def or_scan(self, sources, word_lo: int, n_words: int, key_base: int,
+                capacity: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """bitset_scan of or_gather(sources, word_lo, n_words) in one step
+        (the CUDA build fuses the peer reads into the scan kernel)."""
 
 
 @dataclass
@@ -173,6 +180,15 @@ class CudaRankOps:
         self._capi.bitset_or_gather(ptrs, n_words, buf.data_ptr(), self._stream())
         return buf[:n_words]
 
+    def or_scan(self, sources, word_lo: int, n_words: int, key_base: int, capacity: int):
+        ptrs = [(src.data_ptr() if isinstance(src, torch.Tensor) else int(src)) + 4 * word_lo
+                for src in sources]
+        if self._out is None or self._out.numel() < capacity:
+            self._out = torch.empty(max(capacity, 1), dtype=torch.int32, device=self.device)
+        self._capi.bitset_scan_sources(ptrs, n_words, key_base, self._out.data_ptr(), capacity,
+                                       self._total.data_ptr(), self._stream())
+        return self._out, self._total
+
     def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int):
         if self._out is None or self._out.numel() < capacity:
             self._out = torch.empty(max(capacity, 1), dtype=torch.int32, device=self.device)
@@ -278,8 +294,9 @@ def distributed_sort_a2a(keys: torch.Tensor, key_range: int, n_total: Optional[i
 
 def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[int] = None,
                          ops: Optional[RankOps] = None, group=None) -> SliceResult:
-    """:func:`distributed_sort` with the reduce-scatter replaced by a
-    peer-to-peer OR-gather over CUDA IPC (same result layout)."""
+    """:func:`distributed_sort` with the reduce-scatter and the slice scan
+    replaced by one fused kernel that scans the OR of every rank's bitset
+    slice, reading the peers' words over CUDA IPC (same result layout)."""
     if not 0 < key_range <= 1 << 32:
         raise ValueError("key_range must be in [1, 2^32]")
     world = dist.get_world_size(group)
@@ -293,22 +310,21 @@ def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[i
         n_total = int(t.item())
 
     bits = ops.bitset_build(keys, key_range, words)
+    key_lo = rank * per * 32
+    key_hi = min((rank + 1) * per * 32, key_range)
+    capacity = max(0, min(n_total, key_hi - key_lo))
     if world == 1:
-        slice_ = bits[:per]
+        sources = [bits]
     else:
         handles = [None] * world
         dist.all_gather_object(handles, ops.export_bitset(bits), group=group)
-        sources = [bits if r == rank else ops.import_peer(r, h) for r, h in enumerate(handles)]
+        # the local bitset first: the fused scan copies it by TMA, peers by loads
+        sources = [bits] + [ops.import_peer(r, h) for r, h in enumerate(handles) if r != rank]
         # stream-ordered barrier: this rank's collective completes only after
         # every rank's build (enqueued before its collective) has finished
         fence = torch.zeros(1, dtype=torch.int32, device=dev)
         dist.all_reduce(fence, group=group)
-        slice_ = ops.or_gather(sources, rank * per, per)
-
-    key_lo = rank * per * 32
-    key_hi = min((rank + 1) * per * 32, key_range)
-    capacity = max(0, min(n_total, key_hi - key_lo))
-    out, count_t = ops.bitset_scan(slice_, key_lo, capacity)
+    out, count_t = ops.or_scan(sources, rank * per, per, key_lo, capacity)
     # the counts' all-gather doubles as the "peers are done reading" barrier
     counts = [torch.empty_like(count_t) for _ in range(world)]
     dist.all_gather(counts, count_t, group=group)

@@ -142,6 +142,8 @@ def test_extension_argument_checks():
     # OR-gather: 1..8 sources
     assert capi.lib.bws_gpu_bitset_or_gather(None, 0, 0, None, None) == capi.Status.ERROR_RANGE
     assert capi.lib.bws_gpu_bitset_or_gather(None, 9, 0, None, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_bitset_scan_sources(None, 0, 0, 0, None, 0, None, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_bitset_scan_sources(None, 9, 0, 0, None, 0, None, None) == capi.Status.ERROR_RANGE
     assert capi.lib.bws_gpu_ipc_get_handle(None, None, None) == capi.Status.ERROR_DATA
 
 

@@ -64,6 +64,9 @@ class OracleRankOps:
             acc |= src.numpy().view(np.uint32)[word_lo:word_lo + n_words]
         return torch.from_numpy(acc.view(np.int32))
 
+    def or_scan(self, sources, word_lo, n_words, key_base, capacity):
+        return self.bitset_scan(self.or_gather(sources, word_lo, n_words), key_base, capacity)
+
     def sort_range(self, keys, key_lo, key_range):
         k = keys.numpy().view(np.uint32)
         ok = bool(((k.astype(np.uint64) >= key_lo) & (k.astype(np.uint64) < key_lo + key_range)).all())

@@ -598,7 +598,13 @@ def test_p2p_or_gather_emulated(capi, cuda, world, key_range, n):
             ref |= b[r * per:(r + 1) * per]
         assert cuda.equal(sl, ref)
         out, cnt = ops.bitset_scan(sl, r * per * 32, n)
-        parts.append(out[: int(cnt.item())].cpu().numpy().view(np.uint32).copy())
+        got = out[: int(cnt.item())].cpu().numpy().view(np.uint32).copy()
+        parts.append(got)
+        # the fused exchange + scan (bws_gpu_bitset_scan_sources, local source first)
+        srcs = [bitsets[r]] + [b for q, b in enumerate(bitsets) if q != r]
+        out2, cnt2 = ops.or_scan(srcs, r * per, per, r * per * 32, n)
+        assert int(cnt2.item()) == got.size
+        assert np.array_equal(out2[: got.size].cpu().numpy().view(np.uint32), got)
     assert np.array_equal(np.concatenate(parts), np.sort(keys))
     # odd word counts and misaligned pointers take the scalar path
     a = cuda.arange(1, 1000, dtype=cuda.int32, device="cuda")
@@ -607,6 +613,35 @@ def test_p2p_or_gather_emulated(capi, cuda, world, key_range, n):
     capi.bitset_or_gather([a[1:].data_ptr(), b[1:].data_ptr()], 998, dst.data_ptr())
     cuda.cuda.synchronize()
     assert cuda.equal(dst, a[1:] | b[1:])
+
+
+@pytest.mark.parametrize("nsrc", [1, 2, 3, 8])
+@pytest.mark.parametrize("n_words,offset", [(1, 0), (8191, 0), (8192, 4), (8195, 4), (50_003, 0),
+                                            (300_000, 4), (1000, 1), (77_777, 3)])
+def test_scan_sources_vs_numpy(capi, cuda, nsrc, n_words, offset):
+    """bws_gpu_bitset_scan_sources on random disjoint-bit slices: ragged tile
+    tails, aligned (fused kernel) and misaligned (OR-gather + scan) sources,
+    against numpy. offset shifts every source by that many words."""
+    rng = np.random.default_rng(nsrc * 1000 + n_words + offset)
+    owner = rng.integers(0, nsrc, size=n_words * 32)
+    present = rng.random(n_words * 32) < 0.3
+    bufs = []
+    for s in range(nsrc):
+        bits = np.zeros(n_words * 32, dtype=bool)
+        bits[(owner == s) & present] = True
+        words = np.packbits(bits.reshape(-1, 8)[:, ::-1]).view("<u4")
+        t = cuda.zeros(n_words + offset, dtype=cuda.int32, device="cuda")
+        t[offset:] = cuda.from_numpy(words.view(np.int32).copy()).cuda()
+        bufs.append(t)
+    expected = (np.flatnonzero(present).astype(np.uint64) + 12345).astype(np.uint32)
+    out = cuda.full((expected.size + 7,), -1, dtype=cuda.int32, device="cuda")
+    total = cuda.zeros(1, dtype=cuda.int64, device="cuda")
+    capi.bitset_scan_sources([b.data_ptr() + 4 * offset for b in bufs], n_words, 12345, out.data_ptr(),
+                             out.numel(), total.data_ptr())
+    cuda.cuda.synchronize()
+    assert int(total.item()) == expected.size
+    assert np.array_equal(out[: expected.size].cpu().numpy().view(np.uint32), expected)
+    assert bool((out[expected.size:] == -1).all())
 
 
 def test_ipc_handle_offsets(capi, cuda):
