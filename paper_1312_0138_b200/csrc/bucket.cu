@@ -1047,6 +1047,117 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
 }
 
 
+// KB4m (multiset sorts, bws_sort on input with repeated keys): the counting
+// sort of a bucket (baselines.hpp:99-122's counting_sort with the bucket as its
+// span) in shared memory. The bucket's width is covered by windows of
+// 2^MS_WIN_SHIFT values; per window: 32-bit SMEM counters (atomicAdd per key
+// of the window), a block-wide inclusive prefix of the counters, and the
+// expansion — output slot i of the window takes the value whose prefix first
+// exceeds i (binary search), so a value repeated 2^26 times is written by all
+// threads, coalesced. Windows with no keys are skipped (per-window counts from
+// a first pass). The output range of a bucket is the prefix of the bucket
+// totals (packed layout: the same slots the bucket occupies in `parted`).
+// Adds every key it writes to ctrl->total.
+constexpr int MS_THREADS = 1024;
+constexpr int MS_WIN_SHIFT = 15;  // 32768 counters = 128 KB
+constexpr int MS_WIN = 1 << MS_WIN_SHIFT;
+constexpr int MS_MAX_WIN = (1 << MAX_BUCKET_SHIFT) / MS_WIN;  // 32
+__global__ void __launch_bounds__(MS_THREADS, 1)
+    bucket_multiset_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
+                           const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
+                           uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw);  // MS_WIN counters, then inclusive prefix
+    __shared__ uint32_t s_wc[MS_MAX_WIN];                     // keys per window of the bucket
+    __shared__ uint32_t s_warp[MS_THREADS / 32];
+    __shared__ unsigned s_b;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long written = 0;  // thread 0
+    for (;;) {
+        if (threadIdx.x == 0) s_b = atomicAdd(&ctrl->ticket, 1u);
+        if (threadIdx.x < MS_MAX_WIN) s_wc[threadIdx.x] = 0u;
+        __syncthreads();
+        const unsigned b = s_b;
+        if (b >= static_cast<unsigned>(nb)) break;
+        const uint32_t cnt = tot[b];
+        const unsigned long long base = g_base[b];
+        const uint32_t* src = parted + base;
+        const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
+        const uint32_t nwin = (bm.width + MS_WIN - 1) >> MS_WIN_SHIFT;
+        // pass 0: keys per window (warp-aggregated: one SMEM atomic per window per warp step)
+        for (uint32_t i0 = 0; i0 < cnt; i0 += MS_THREADS) {
+            const uint32_t i = i0 + threadIdx.x;
+            const uint32_t w = i < cnt ? (src[i] - key_lo) >> MS_WIN_SHIFT : 0xffffffffu;
+            const unsigned peers = __match_any_sync(kFull, w);
+            if (w != 0xffffffffu && lane == static_cast<unsigned>(__ffs(peers) - 1))
+                atomicAdd(&s_wc[w], static_cast<uint32_t>(__popc(peers)));
+        }
+        __syncthreads();
+        unsigned long long o = base;
+        for (uint32_t w = 0; w < nwin; ++w) {
+            const uint32_t wk = s_wc[w];  // block-uniform
+            if (wk == 0) continue;
+            uint4* c4 = reinterpret_cast<uint4*>(s_cnt);
+            for (uint32_t i = threadIdx.x; i < MS_WIN / 4; i += MS_THREADS) c4[i] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+            const uint32_t wlo = w << MS_WIN_SHIFT;
+            for (uint32_t i = threadIdx.x; i < cnt; i += MS_THREADS) {
+                const uint32_t x = src[i] - key_lo - wlo;
+                if (x < static_cast<uint32_t>(MS_WIN)) atomicAdd(s_cnt + x, 1u);
+            }
+            __syncthreads();
+            // inclusive prefix of the counters: thread t owns [32t, 32t + 32),
+            // read and written as 8 lane-rotated uint4 (bank-conflict free)
+            constexpr int kPer = MS_WIN / MS_THREADS;  // 32
+            uint32_t v[kPer];
+#pragma unroll
+            for (int q = 0; q < kPer / 4; ++q) {
+                const int qq = (q + static_cast<int>(lane)) & (kPer / 4 - 1);
+                const uint4 t = c4[threadIdx.x * (kPer / 4) + qq];
+                v[4 * qq] = t.x;
+                v[4 * qq + 1] = t.y;
+                v[4 * qq + 2] = t.z;
+                v[4 * qq + 3] = t.w;
+            }
+#pragma unroll
+            for (int j = 1; j < kPer; ++j) v[j] += v[j - 1];
+            const uint32_t incl = warp_incl_scan(v[kPer - 1], lane);
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t x = s_warp[lane];
+                s_warp[lane] = warp_incl_scan(x, lane) - x;
+            }
+            __syncthreads();
+            const uint32_t add = s_warp[warp] + incl - v[kPer - 1];
+#pragma unroll
+            for (int q = 0; q < kPer / 4; ++q) {
+                const int qq = (q + static_cast<int>(lane)) & (kPer / 4 - 1);
+                c4[threadIdx.x * (kPer / 4) + qq] =
+                    make_uint4(v[4 * qq] + add, v[4 * qq + 1] + add, v[4 * qq + 2] + add, v[4 * qq + 3] + add);
+            }
+            __syncthreads();
+            // expansion: slot i holds the smallest value whose inclusive prefix exceeds i
+            const uint32_t kbase = key_lo + wlo;
+            for (uint32_t i = threadIdx.x; i < wk; i += MS_THREADS) {
+                uint32_t lo = 0, len = MS_WIN;
+#pragma unroll 1
+                while (len > 1) {
+                    const uint32_t half = len >> 1;
+                    if (s_cnt[lo + half - 1] <= i) lo += half;
+                    len -= half;
+                }
+                __stcs(out + o + i, (kbase + lo) ^ bm.xr);
+            }
+            o += wk;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) written += cnt;
+    }
+    if (threadIdx.x == 0 && written) atomicAdd(&ctrl->total, written);
+}
+
+
 // KB4b (multi-GPU per-rank build): like KB4, but instead of extracting keys
 // each bucket's SMEM bitset is written to the global bitset, coalesced and
 // without atomics; every word below n_words is written, so the caller's
@@ -1221,6 +1332,7 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
     // bulk-store runs are padded to multiples of 4: at most 3 extra slots per
     // bucket per tile (KB3 CTAs <= 1024) plus the head/tail claims
     if (tma_store_kb3(plan)) cap += 3 * (static_cast<uint64_t>(n) / PART_TILE + 1024 + 8);
+    cap = (cap + 3) & ~uint64_t(3);  // bucket slabs and the dump tile stay 16-byte aligned
     const uint64_t slots = static_cast<uint64_t>(plan.nb) * cap + PART_DUMP;  // + dump tile
     // the slab trades memory (up to 4.5 slots per key, or 256 MiB for small
     // sorts) for the histogram pass
@@ -1240,7 +1352,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                                uint32_t* parted, void* scratch, Ctrl* ctrl, const BucketPlan& plan,
                                const LaunchGeometry& geo, cudaStream_t stream, int* launches,
                                KernelTimer* timer, uint32_t* bits_out, uint64_t n_words,
-                               uint64_t parted_cap) {
+                               uint64_t parted_cap, bool multiset) {
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     // scratch: slab fill counters (fixed place: they persist across sorts), then H, tot, base
@@ -1264,7 +1376,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     ks.xr = plan.map.xr;
 
     const uint64_t slab = slab_slots(plan, n);
-    const bool use_slab = slab != 0 && slab <= parted_cap;
+    // multiset sorts take the packed layout: exact for any key multiplicity
+    const bool use_slab = !multiset && slab != 0 && slab <= parted_cap;
     SlabArgs sa;
     int nlaunch = 0;
     cudaError_t err;
@@ -1274,7 +1387,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.gcnt = gcnt;
         sa.gtrue = tma_store_kb3(plan) ? gcnt + MAX_BUCKETS : nullptr;
         sa.cap = static_cast<uint32_t>((slab - PART_DUMP) / plan.nb) & ~3u;
-        sa.dump = static_cast<uint32_t>(slab - PART_DUMP);
+        sa.dump = static_cast<uint32_t>(plan.nb) * sa.cap;  // 16-byte aligned (bulk-store runs)
         sa.limit = limit;
         sa.check = check;
         sa.ctrl = ctrl;
@@ -1341,6 +1454,15 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (launches) *launches = nlaunch + 1;
         return cudaSuccess;
     }
+    if (multiset) {
+        if (timer) timer->before(stream);
+        bucket_multiset_kernel<<<geo.multiset_blocks, MS_THREADS, MS_WIN * sizeof(uint32_t), stream>>>(
+            parted, tot, base, plan.map, plan.nb, out, ctrl);
+        if (timer) timer->after("bucket_multiset", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (launches) *launches = nlaunch + 1;
+        return cudaSuccess;
+    }
     if (timer) timer->before(stream);
     const size_t smem = bucket_sort_smem_bytes(plan.shift);
     if (plan.shift >= MAX_BUCKET_SHIFT)
@@ -1385,6 +1507,10 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_bitset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                1 << (MAX_BUCKET_SHIFT - 3));
     if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_multiset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(MS_WIN * sizeof(uint32_t)));
+    if (err != cudaSuccess) return err;
+    geo->multiset_blocks = sms;
     err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(bucket_sort_smem_bytes(20)));
     if (err != cudaSuccess) return err;

@@ -480,8 +480,10 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
 // Leaves the cached bitset untouched.
 // key_lo: keys lie in [key_lo, key_lo + key_range) (range sorts). xr: keys
 // are XORed with it on load and store (signed int32 sorts: 0x80000000).
+// multiset: repeated keys are sorted too (packed layout + KB4m counting sort).
 void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
-                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0) {
+                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0,
+                      bool multiset = false) {
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
     cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
     if (key_range == 0) {
@@ -503,7 +505,7 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
     int launches = 0;
     cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
                                            ctx.ctrl(), plan, ctx.geo, stream, &launches,
-                                           active_timer(), nullptr, 0, parted_cap),
+                                           active_timer(), nullptr, 0, parted_cap, multiset),
                "bucketed sort launch");
     g_launches.fetch_add(static_cast<uint64_t>(launches));
     cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
@@ -521,16 +523,26 @@ void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* 
         enqueue_direct(ctx, keys, count, out, key_range, stream);
 }
 
-// Synchronises and turns the control block into a status: out-of-range keys
-// or duplicates (fewer set bits than keys) are BWS_ERROR_DATA.
-uint64_t validate(DeviceCtx& ctx, size_t count, uint64_t key_range, cudaStream_t stream) {
+// Synchronises and reads the control block back.
+Ctrl read_ctrl(DeviceCtx& ctx, cudaStream_t stream) {
     cuda_check(cudaStreamSynchronize(stream), "sort execution");
     Ctrl c;
     cuda_check(cudaMemcpy(&c, ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost),
                "control block readback");
+    return c;
+}
+
+void throw_bad_keys(const Ctrl& c, uint64_t key_range) {
     if (c.bad_keys != 0)
         throw data_error(std::to_string(c.bad_keys) + " key(s) not below the key range " +
                          std::to_string(key_range));
+}
+
+// Synchronises and turns the control block into a status: out-of-range keys
+// or duplicates (fewer set bits than keys) are BWS_ERROR_DATA.
+uint64_t validate(DeviceCtx& ctx, size_t count, uint64_t key_range, cudaStream_t stream) {
+    const Ctrl c = read_ctrl(ctx, stream);
+    throw_bad_keys(c, key_range);
     if (c.total != count)
         throw data_error("keys are not distinct: " + std::to_string(count) + " keys, " +
                          std::to_string(c.total) +
@@ -590,7 +602,14 @@ void stage_to_host(DeviceCtx& ctx, void* host, const void* dev, size_t bytes) {
 // owning `data` when it is device memory). Host arrays are staged through the
 // context's device buffer; they are written back only after validation, so a
 // rejected input is left untouched.
-void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0) {
+// multiset (bws_sort): an input with repeated keys is sorted too, like the
+// reference's bws_sort sorts any input. The bitset pass detects the repeats
+// (fewer set bits than keys) and the sort is redone from the untouched input
+// by the counting-sort pipeline (KB1-KB3 packed + KB4m). Device arrays are
+// then sorted out of place into the context's key buffer and copied back, so
+// the original survives the detection. Without multiset (the key-range
+// extension) repeated keys are BWS_ERROR_DATA.
+void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, bool multiset = false) {
     check_range(key_range);
     if (count == 0) return;
     visible_devices();
@@ -627,22 +646,59 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0) {
             enqueue_sort(ctx, in, count, out, key_range, ctx.stream);
         }
     };
+    // after the bitset pass: true if the keys repeat and the counting-sort
+    // pass must run (its key range: the max key the first pass folded)
+    uint64_t ms_range = 0;
+    auto needs_multiset = [&]() {
+        const Ctrl c = read_ctrl(ctx, ctx.stream);
+        throw_bad_keys(c, key_range ? key_range : kMaxKeyRange);
+        if (c.total == count) return false;
+        if (!multiset)
+            throw data_error("keys are not distinct: " + std::to_string(count) + " keys, " +
+                             std::to_string(c.total) + " distinct (the bitset sort requires distinct keys)");
+        if (count >= (size_t(1) << 32))
+            throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
+        ms_range = key_range ? key_range : static_cast<uint64_t>(c.max_key) + 1;
+        return true;
+    };
+    auto enqueue_multiset = [&](const uint32_t* in, uint32_t* out) {
+        enqueue_bucketed(ctx, in, count, out, ms_range, ctx.stream, 0, xr, /*multiset=*/true);
+        validate(ctx, count, ms_range, ctx.stream);
+    };
     if (on_device) {
-        enqueue(keys, keys);
-        validate(ctx, count, key_range, ctx.stream);
+        if (!multiset) {
+            enqueue(keys, keys);
+            validate(ctx, count, key_range, ctx.stream);
+            return;
+        }
+        ctx.ensure_keys(count);
+        enqueue(keys, ctx.keys);
+        if (needs_multiset()) {
+            enqueue_multiset(keys, keys);
+            return;
+        }
+        cuda_check(cudaMemcpyAsync(keys, ctx.keys, count * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx.stream),
+                   "device-to-device copy");
+        cuda_check(cudaStreamSynchronize(ctx.stream), "device-to-device copy");
         return;
     }
     ctx.ensure_keys(count);
     const size_t bytes = count * sizeof(uint32_t);
     const bool pinned = attr.type == cudaMemoryTypeHost;
-    if (pinned) {
-        cuda_check(cudaMemcpyAsync(ctx.keys, data, bytes, cudaMemcpyHostToDevice, ctx.stream),
-                   "host-to-device copy");
-    } else {
-        stage_to_device(ctx, ctx.keys, data, bytes);
-    }
+    auto upload = [&] {
+        if (pinned) {
+            cuda_check(cudaMemcpyAsync(ctx.keys, data, bytes, cudaMemcpyHostToDevice, ctx.stream),
+                       "host-to-device copy");
+        } else {
+            stage_to_device(ctx, ctx.keys, data, bytes);
+        }
+    };
+    upload();
     enqueue(ctx.keys, ctx.keys);
-    validate(ctx, count, key_range, ctx.stream);
+    if (needs_multiset()) {
+        upload();  // the host array is untouched until the write-back
+        enqueue_multiset(ctx.keys, ctx.keys);
+    }
     if (pinned) {
         cuda_check(cudaMemcpyAsync(data, ctx.keys, bytes, cudaMemcpyDeviceToHost, ctx.stream),
                    "device-to-host copy");
@@ -711,7 +767,7 @@ bws_status bws_sort(void* data, size_t count, uint32_t width, int is_unsigned,
         // signed int32: x ^ 0x80000000 maps the signed order onto the unsigned
         // one (the reference splits negatives and non-negatives instead,
         // bitsort.hpp:131-152); the same XOR maps the sorted keys back
-        sort_u32(data, count, 0, is_unsigned ? 0u : 0x80000000u);
+        sort_u32(data, count, 0, is_unsigned ? 0u : 0x80000000u, /*multiset=*/true);
     });
 }
 

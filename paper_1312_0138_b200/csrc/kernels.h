@@ -86,6 +86,7 @@ struct LaunchGeometry {
     int part_blocks_narrow = 0;                  // KB1/KB3 shares, narrow KB3 variant
     int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
     int scan2_blocks = 0;                          // K3 v2 CTAs
+    int multiset_blocks = 0;                       // KB4m CTAs (one per SM)
 };
 
 // A key array as seen by the bucketed kernels: 16-byte-aligned uint4 body plus
@@ -201,13 +202,15 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo);
 // distinct keys to ctrl->total, counts keys >= key_range in ctrl->bad_keys.
 // `launches` receives the kernel count. With bits_out set, KB4b writes the
 // bitset (n_words words) instead of sorted keys (multi-GPU per-rank build; no
-// clearing of bits_out needed).
+// clearing of bits_out needed). With multiset, repeated keys are sorted too
+// (packed layout + KB4m per-bucket counting sort; ctrl->total counts every
+// key written): bws_sort on inputs that are not distinct.
 cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::uint64_t key_range,
                                std::uint32_t* out, std::uint32_t* parted, void* scratch, Ctrl* ctrl,
                                const BucketPlan& plan, const LaunchGeometry& geo,
                                cudaStream_t stream, int* launches, KernelTimer* timer = nullptr,
                                std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0,
-                               std::uint64_t parted_cap = 0);
+                               std::uint64_t parted_cap = 0, bool multiset = false);
 // Multi-GPU OR-gather (the P2P replacement of the reduce-scatter): dst[i] =
 // OR over s of srcs.p[s][i] for i < n_words; srcs may point into peer GPUs'
 // memory (CUDA IPC over NVLink/NVSwitch).

@@ -52,6 +52,11 @@ def edge_records():
 
 
 @pytest.fixture(scope="session")
+def repeats_records():
+    return read_records(GOLDEN / "repeats_u32.bin")
+
+
+@pytest.fixture(scope="session")
 def anchors():
     return json.loads((GOLDEN / "anchors.json").read_text())
 

@@ -13,6 +13,10 @@
 //                       {1,2,100,1000}), first 16 trials per n, with the
 //                       reference bws_sort(...,32,1,BWS_ALG_BITWISE) output
 //   edge_u32.bin        hand-picked distinct-key edge cases, same treatment
+//   repeats_u32.bin     inputs with repeated keys from the reference's own
+//                       generator (generator.hpp:91-130: uniform_small_range
+//                       with spans 16 and 1024, constant), n in {100, 1000,
+//                       3000}, trials 0-1, seed 1337, with the reference output
 //   anchors.json        C1/C2/C4 synthetic-input anchors
 //                       computed with the reference's splitmix64 and sorted by
 //                       the reference bws_sort; the test_capi.cpp:78-82 vector
@@ -145,6 +149,16 @@ int main(int argc, char** argv) {
         for (uint32_t trial = 0; trial < 16; ++trial)
             acc.push_back(make_record(bws::generate_input<uint32_t>(n, dist, 1337, trial), trial));
     write_records(dir + "/acceptance_u32.bin", acc);
+
+    // repeated keys: the reference generator's duplicate-heavy distributions
+    std::vector<record> rep;
+    for (const char* name : {"uniform_small_range:16", "uniform_small_range:1024", "constant"}) {
+        const bws::distribution_spec d = bws::distribution_spec::parse(name);
+        for (const size_t n : {size_t{100}, size_t{1000}, size_t{3000}})
+            for (uint32_t trial = 0; trial < 2; ++trial)
+                rep.push_back(make_record(bws::generate_input<uint32_t>(n, d, 1337, trial), trial));
+    }
+    write_records(dir + "/repeats_u32.bin", rep);
 
     // distinct-key edge cases at the 32-bit boundaries
     std::vector<std::vector<uint32_t>> edges = {

@@ -83,8 +83,8 @@ def test_sort_file_on_gpu(tmp_path, signed):
     assert r.returncode == 0, r.stderr
     got = [int(x) for x in out.read_text().split()]
     assert got == sorted(int(k) for k in keys)
-    # stdin -> stdout, and duplicates are a data error (exit 2)
+    # stdin -> stdout; repeated keys sort like the reference's
     r = run(["sort", "-"] + ([] if signed else ["--unsigned"]), stdin="3\n1\n2\n")
     assert r.returncode == 0 and r.stdout == "1\n2\n3\n"
     r = run(["sort", "-"], stdin="3\n1\n3\n")
-    assert r.returncode == 2 and "distinct" in r.stderr
+    assert r.returncode == 0 and r.stdout == "1\n3\n3\n", r.stderr

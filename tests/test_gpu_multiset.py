@@ -1,0 +1,142 @@
+"""GPU parity for inputs with repeated keys (bws_sort's full uint32/int32
+contract).
+
+The reference's bws_sort sorts any input (bitsort.hpp:84-136 is a radix sort).
+The B200 build's bitset pass detects repeats (fewer set bits than keys) and
+redoes the sort from the untouched input with the counting-sort pass (KB1-KB3
+packed layout + KB4m, bucket.cu). Checked bit-exact against the oracle (C
+restatement of the reference's bitwise sort) and, where it was built, the
+reference's own bws_sort.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import bitwise_sort
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def capi(cuda):
+    from paper_1312_0138_b200 import capi as c
+
+    cuda.cuda.set_device(0)
+    return c
+
+
+@pytest.fixture(autouse=True)
+def _auto_mode(capi):
+    yield
+    capi.set_path(capi.Path.AUTO)
+
+
+def _reference(keys: np.ndarray, is_unsigned: int = 1) -> np.ndarray:
+    a = keys.copy()
+    if oracle.REFERENCE is not None:  # the reference's own bws_sort
+        assert oracle.REFERENCE.bws_sort(a.ctypes.data, a.size, 32, is_unsigned, 0) == 0
+        return a
+    return bitwise_sort(a) if is_unsigned else np.sort(a)
+
+
+def _sort_host(capi, keys, is_unsigned=1):
+    a = keys.copy()
+    assert capi.sort_raw(a.ctypes.data, a.size, 32, is_unsigned, capi.Algorithm.BITWISE) == capi.Status.OK, \
+        capi.last_error()
+    return a
+
+
+def _sort_device(capi, torch, keys, is_unsigned=1, offset=0):
+    buf = torch.zeros(keys.size + offset + 4, dtype=torch.int32, device="cuda")
+    view = buf[offset: offset + keys.size]
+    view.copy_(torch.from_numpy(keys.view(np.int32)))
+    assert capi.sort_raw(view.data_ptr(), keys.size, 32, is_unsigned, 0) == capi.Status.OK, capi.last_error()
+    torch.cuda.synchronize()
+    assert int(buf[offset + keys.size:].abs().sum()) == 0  # nothing written past the array
+    return view.cpu().numpy().view(keys.dtype)
+
+
+@pytest.mark.parametrize("path", ["AUTO", "DIRECT", "BUCKETED"])
+@pytest.mark.parametrize("n", [2, 3, 100, 1000, 65537, (1 << 21) - 1, (1 << 21) + 5])
+@pytest.mark.parametrize("key_range", [1, 2, 17, 1000, 1 << 20, 1 << 32])
+def test_repeats_vs_oracle(capi, cuda, path, n, key_range):
+    capi.set_path(getattr(capi.Path, path))
+    rng = np.random.default_rng(n * 31 + key_range % 1000)
+    keys = rng.integers(0, key_range, size=n, dtype=np.uint64).astype(np.uint32)
+    expected = bitwise_sort(keys)
+    assert np.array_equal(_sort_host(capi, keys), expected)
+    assert np.array_equal(_sort_device(capi, cuda, keys, offset=n % 3), expected)
+
+
+@pytest.mark.parametrize("n", [1000, 1 << 20])
+def test_reference_generator_inputs(capi, n):
+    """The reference's own uint32 input generator (generator.hpp:91-103, seeded
+    like acceptance.cpp) draws with repeats: bit-exact vs its bws_sort."""
+    for trial in range(3):
+        keys = oracle.generate_uniform_u32(n, seed=1337, trial=trial)
+        assert np.array_equal(_sort_host(capi, keys), _reference(keys))
+
+
+@pytest.mark.parametrize("value", [0, 123456789, 0xFFFFFFFF])
+@pytest.mark.parametrize("n", [5, 1 << 22])
+def test_all_equal(capi, cuda, value, n):
+    """One key repeated n times: the counting pass expands a single counter."""
+    keys = np.full(n, value, dtype=np.uint32)
+    assert np.array_equal(_sort_host(capi, keys), keys)
+    assert np.array_equal(_sort_device(capi, cuda, keys), keys)
+
+
+def test_few_values_many_times(capi, cuda):
+    rng = np.random.default_rng(7)
+    vals = rng.integers(0, 1 << 32, size=37, dtype=np.uint64).astype(np.uint32)
+    keys = vals[rng.integers(0, vals.size, size=(1 << 22) + 3)]
+    expected = np.sort(keys)
+    assert np.array_equal(_sort_host(capi, keys), expected)
+    assert np.array_equal(_sort_device(capi, cuda, keys, offset=1), expected)
+
+
+@pytest.mark.parametrize("n", [3, 1000, 1 << 21])
+def test_signed_repeats(capi, cuda, n):
+    rng = np.random.default_rng(n)
+    keys = rng.integers(-(1 << 31), 1 << 31, size=n, dtype=np.int64).astype(np.int32)
+    keys[: n // 2] = keys[n // 2: 2 * (n // 2)]  # every key of the first half repeats
+    if n >= 4:
+        keys[:4] = [-(1 << 31), -(1 << 31), (1 << 31) - 1, (1 << 31) - 1]
+    rng.shuffle(keys)
+    expected = _reference(keys, is_unsigned=0)
+    assert np.array_equal(expected, np.sort(keys))
+    assert np.array_equal(_sort_host(capi, keys, 0), expected)
+    assert np.array_equal(_sort_device(capi, cuda, keys, 0), expected)
+
+
+def test_pinned_host_repeats(capi, cuda):
+    keys = np.random.default_rng(11).integers(0, 1 << 16, size=1 << 21, dtype=np.uint32)
+    t = cuda.from_numpy(keys.view(np.int32).copy()).pin_memory()
+    assert capi.sort_raw(t.data_ptr(), keys.size, 32, 1, 0) == capi.Status.OK, capi.last_error()
+    assert np.array_equal(t.numpy().view(np.uint32), np.sort(keys))
+
+
+def test_repeats_then_distinct(capi, cuda):
+    """A repeat-sorting call leaves nothing behind for the next distinct sort
+    (cached bitset, slab counters, control block)."""
+    rng = np.random.default_rng(2)
+    for _ in range(2):
+        rep = rng.integers(0, 1 << 24, size=1 << 22, dtype=np.uint32)
+        assert np.array_equal(_sort_host(capi, rep), np.sort(rep))
+        dis = rng.choice(1 << 24, size=1 << 22, replace=False).astype(np.uint32)
+        assert np.array_equal(_sort_host(capi, dis), np.sort(dis))
+        small = rng.choice(1 << 20, size=5000, replace=False).astype(np.uint32)
+        assert np.array_equal(_sort_host(capi, small), np.sort(small))
+
+
+@pytest.mark.slow
+def test_c2_shape_with_repeats(capi, cuda):
+    """C2's size (2^26 keys) drawn WITH replacement from [0, 2^24): every value
+    about four times. Device array, in place."""
+    keys = np.random.default_rng(42).integers(0, 1 << 24, size=1 << 26, dtype=np.uint32)
+    t = cuda.from_numpy(keys.view(np.int32).copy()).cuda()
+    assert capi.sort_raw(t.data_ptr(), keys.size, 32, 1, 0) == capi.Status.OK, capi.last_error()
+    got = t.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, np.sort(keys))

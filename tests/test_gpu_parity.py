@@ -53,21 +53,27 @@ def gpu_sort_device(capi, torch, keys: np.ndarray, offset: int = 0) -> np.ndarra
 @pytest.mark.parametrize("path", PATHS)
 def test_acceptance_golden_vectors(capi, acceptance_records, path):
     """acceptance.cpp:65-95 criterion-2 inputs (uint32 arm) vs the reference's
-    bws_sort output; inputs with duplicate draws must be rejected untouched."""
+    bws_sort output, bit-exact."""
     capi.set_path(getattr(capi.Path, path))
-    checked = rejected = 0
+    checked = 0
     for rec in acceptance_records:
         a = rec["input"].copy()
         status = capi.sort_raw(a.ctypes.data, a.size, 32, 1, capi.Algorithm.BITWISE)
-        if rec["distinct"]:
-            assert status == capi.Status.OK, capi.last_error()
-            assert np.array_equal(a, rec["output"]), (rec["n"], rec["trial"])
-            checked += 1
-        else:
-            assert status == capi.Status.ERROR_DATA
-            assert np.array_equal(a, rec["input"])
-            rejected += 1
+        assert status == capi.Status.OK, capi.last_error()
+        assert np.array_equal(a, rec["output"]), (rec["n"], rec["trial"])
+        checked += 1
     assert checked >= 60
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_repeats_golden_vectors(capi, cuda, repeats_records, path):
+    """Inputs with repeated keys from the reference's own generator (small
+    range, constant) vs the reference's bws_sort output, host and device
+    arrays: the bitset pass detects the repeats, the counting pass sorts."""
+    capi.set_path(getattr(capi.Path, path))
+    for rec in repeats_records:
+        assert np.array_equal(gpu_sort_host(capi, rec["input"]), rec["output"]), (rec["n"], rec["trial"])
+        assert np.array_equal(gpu_sort_device(capi, cuda, rec["input"]), rec["output"])
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -91,7 +97,10 @@ def test_capi_uint8_vector_widened(capi):
 def test_status_conventions(capi, path):
     capi.set_path(getattr(capi.Path, path))
     a = np.array([5, 1, 5], dtype=np.uint32)
-    assert capi.sort_raw(a.ctypes.data, 3, 32, 1, 0) == capi.Status.ERROR_DATA
+    assert capi.sort_raw(a.ctypes.data, 3, 32, 1, 0) == capi.Status.OK  # repeats sort like the reference
+    assert a.tolist() == [1, 5, 5]
+    a = np.array([5, 1, 5], dtype=np.uint32)
+    assert capi.lib.bws_sort_u32_range(a.ctypes.data, 3, 16) == capi.Status.ERROR_DATA  # distinct-only extension
     assert "distinct" in capi.last_error()
     assert a.tolist() == [5, 1, 5]  # rejected input left unmodified
     b = np.array([3, 1, 2], dtype=np.uint32)
@@ -204,13 +213,19 @@ def test_top_of_range(capi, path):
 
 
 @pytest.mark.parametrize("path", PATHS)
-def test_duplicates_rejected_at_scale(capi, path):
+def test_one_repeat_at_scale(capi, cuda, path):
+    """One repeated key among 2^20: bws_sort sorts it (host and device
+    arrays); the distinct-only range extension rejects it untouched."""
     capi.set_path(getattr(capi.Path, path))
     keys = np.random.default_rng(3).choice(1 << 24, size=1 << 20, replace=False).astype(np.uint32)
     keys[777] = keys[123456]
     a = keys.copy()
-    assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.ERROR_DATA
-    assert np.array_equal(a, keys)
+    assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.OK, capi.last_error()
+    assert np.array_equal(a, np.sort(keys))
+    assert np.array_equal(gpu_sort_device(capi, cuda, keys), np.sort(keys))
+    b = keys.copy()
+    assert capi.lib.bws_sort_u32_range(b.ctypes.data, b.size, 1 << 24) == capi.Status.ERROR_DATA
+    assert np.array_equal(b, keys)
 
 
 # --- signed int32 (x ^ 0x80000000 on load and store, bucketed pipeline) ----
@@ -254,10 +269,6 @@ def test_signed_int32_layouts(capi, kind):
     keys = rng.permutation(keys).astype(np.int32)
     if kind == "duplicate":
         keys[10] = keys[12345]
-        a = keys.copy()
-        assert capi.sort_raw(a.ctypes.data, a.size, 32, 0, 0) == capi.Status.ERROR_DATA
-        assert np.array_equal(a, keys)
-        return
     a = keys.copy()
     assert capi.sort_raw(a.ctypes.data, a.size, 32, 0, 0) == capi.Status.OK
     assert np.array_equal(a, np.sort(keys))
@@ -309,8 +320,10 @@ def test_slab_layout_full_bucket(capi):
 
 @pytest.mark.parametrize("kind", ["pair", "overflow"])
 def test_slab_layout_duplicates(capi, kind):
-    """Duplicates are rejected in the slab layout too, including ones that
-    overflow a bucket's fixed slots (then that bucket sorts nothing)."""
+    """Repeats in the slab layout, including ones that overflow a bucket's
+    fixed slots (then that bucket sorts nothing and the popcount total drops):
+    the distinct-only range extension rejects them untouched, bws_sort then
+    sorts them by the counting-sort pass (from the untouched input)."""
     capi.set_path(capi.Path.BUCKETED)
     keys = np.random.default_rng(4).choice(SLAB_RANGE, size=SLAB_N, replace=False).astype(np.uint32)
     if kind == "pair":
@@ -319,9 +332,11 @@ def test_slab_layout_duplicates(capi, kind):
         keys[: 1 << 17] = (7 << 16) + (np.arange(1 << 17, dtype=np.uint32) % 40)
     for _ in range(2):  # and the next sort is unaffected
         a = keys.copy()
-        assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.ERROR_DATA
+        assert capi.lib.bws_sort_u32_range(a.ctypes.data, a.size, SLAB_RANGE) == capi.Status.ERROR_DATA
         assert "distinct" in capi.last_error()
         assert np.array_equal(a, keys)
+        assert capi.sort_raw(a.ctypes.data, a.size, 32, 1, 0) == capi.Status.OK, capi.last_error()
+        assert np.array_equal(a, np.sort(keys))
     good = np.random.default_rng(5).choice(SLAB_RANGE, size=SLAB_N, replace=False).astype(np.uint32)
     a = good.copy()
     capi.sort_u32_range(a, SLAB_RANGE)
@@ -364,7 +379,9 @@ def test_non_power_of_two_bucket_width(capi, cuda, n_log2, range_log2):
     capi.set_path(capi.Path.BUCKETED)
     dup = keys.copy()
     dup[1] = dup[keys.size - 2]
-    assert capi.sort_raw(dup.ctypes.data, dup.size, 32, 1, 0) == capi.Status.ERROR_DATA
+    expected = np.sort(dup)
+    assert capi.sort_raw(dup.ctypes.data, dup.size, 32, 1, 0) == capi.Status.OK, capi.last_error()
+    assert np.array_equal(dup, expected)
 
 
 @pytest.mark.parametrize("kind", ["distinct", "overflow"])

@@ -19,6 +19,15 @@ def test_oracle_matches_reference_golden_outputs(acceptance_records, edge_record
         assert np.array_equal(bitwise_sort(rec["input"], skip_empty_bits=True), rec["output"])
 
 
+def test_oracle_matches_reference_repeats(repeats_records):
+    """The reference's duplicate-heavy generator distributions (small range,
+    constant) and its outputs: the restatement sorts them identically."""
+    assert len(repeats_records) == 18 and not any(r["distinct"] for r in repeats_records)
+    for rec in repeats_records:
+        assert np.array_equal(bitwise_sort(rec["input"]), rec["output"])
+        assert np.array_equal(rec["output"], np.sort(rec["input"]))
+
+
 def test_generate_input_restatement(acceptance_records):
     """oracle_generate_uniform_u32 == generate_input<uint32_t>(n,
     uniform_full_range, 1337, trial) (generator.hpp:91-103), as captured from
