@@ -20,12 +20,16 @@
  * handle (:101-143) entry points are not on the sort path and are not part of
  * this library.
  *
- * Domain of the GPU bws_sort: width 32, unsigned or signed (int32 keys are
- * mapped onto the unsigned order by x ^ 0x80000000 on load and store),
- * BWS_ALG_BITWISE (or its BWS_ALG_BITWISE_SKIP_EMPTY variant), DISTINCT keys.
- * Other (width, algorithm) combinations return BWS_ERROR_CONFIG; duplicate keys
- * return BWS_ERROR_DATA and leave a host array unmodified. There is no CPU
- * fallback. Additive GPU extensions live in bitsort_gpu.h.
+ * Domain of the GPU bws_sort: BWS_ALG_BITWISE (or its BWS_ALG_BITWISE_SKIP_EMPTY
+ * variant), unsigned or signed keys (mapped onto the unsigned order by flipping
+ * the sign bit on load and store), naturally aligned:
+ *   width 32  the bitset sort (the hot path); repeated keys are detected and
+ *             sorted by a GPU counting-sort pass, as the reference sorts them;
+ *   width 8/16  a GPU counting sort over the type's range;
+ *   width 64  keys whose span max - min is below 2^32 (narrowed to the 32-bit
+ *             path); wider spans return BWS_ERROR_CONFIG.
+ * Other algorithms return BWS_ERROR_CONFIG. There is no CPU fallback.
+ * Additive GPU extensions live in bitsort_gpu.h.
  */
 
 #include <stddef.h>

@@ -194,6 +194,9 @@ struct DeviceCtx {
     uint32_t* parted = nullptr;         // bucketed path: keys grouped by bucket
     size_t parted_cap = 0;
     void* bucket_scratch = nullptr;     // bucketed path: histograms, totals, bases
+    void* wide = nullptr;               // staging for host arrays of 8/16/64-bit keys
+    size_t wide_cap = 0;
+    void* width_scratch = nullptr;      // 8/16-bit histogram + prefix, 64-bit min/max
     size_t last_count = 0;        // count of the last async device sort (bws_gpu_sort_check)
     uint64_t last_range = 0;      // its key range (0 = derived)
     void* bounce[2] = {nullptr, nullptr};  // pinned staging for pageable host arrays
@@ -213,6 +216,7 @@ struct DeviceCtx {
         cuda_check(bws_gpu::query_geometry(dev, &geo), "occupancy query");
         cuda_check(bws_gpu::configure_bucket_kernels(dev, &geo), "bucket kernel configuration");
         cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
+        cuda_check(bws_gpu::configure_width_kernels(dev, &geo), "width kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes), "cudaMalloc(control block)");
         cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
@@ -268,6 +272,19 @@ struct DeviceCtx {
         return parted_cap;
     }
 
+    void* ensure_wide(size_t bytes) {
+        if (bytes > wide_cap) {
+            if (wide) cuda_check(cudaFree(wide), "cudaFree(wide keys)");
+            wide = nullptr;
+            wide_cap = 0;
+            cuda_check(cudaMalloc(&wide, bytes), "cudaMalloc(wide keys)");
+            wide_cap = bytes;
+        }
+        if (!width_scratch)
+            cuda_check(cudaMalloc(&width_scratch, bws_gpu::width_scratch_bytes()), "cudaMalloc(width scratch)");
+        return wide;
+    }
+
     void ensure_bounce() {
         if (bounce[0]) return;
         for (int i = 0; i < 2; ++i) {
@@ -291,6 +308,11 @@ struct DeviceCtx {
         if (keys) cudaFree(keys);
         if (parted) cudaFree(parted);
         if (bucket_scratch) cudaFree(bucket_scratch);
+        if (wide) cudaFree(wide);
+        if (width_scratch) cudaFree(width_scratch);
+        wide = nullptr;
+        wide_cap = 0;
+        width_scratch = nullptr;
         parted = nullptr;
         parted_cap = 0;
         bucket_scratch = nullptr;
@@ -708,6 +730,100 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     }
 }
 
+// 8-, 16- and 64-bit keys (the reference's with_width arms, dispatch.hpp:17-40),
+// on the GPU: 8/16-bit keys by a counting sort over the type's range
+// (widths.cu KW1-KW3, repeats included); 64-bit keys whose biased span
+// max - min is below 2^32 narrowed to u32 offsets, sorted by the 32-bit
+// pipeline (repeats redone by the counting pass) and widened back. Wider
+// 64-bit spans are BWS_ERROR_CONFIG (no CPU fallback).
+void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned) {
+    if (count == 0) return;
+    visible_devices();
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, data) != cudaSuccess) {
+        cudaGetLastError();
+        attr.type = cudaMemoryTypeUnregistered;
+    }
+    const bool on_device = attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+    int device = 0;
+    if (on_device)
+        device = attr.device;
+    else
+        cuda_check(cudaGetDevice(&device), "cudaGetDevice");
+    DeviceCtx& ctx = context_for(device);
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    int prev = 0;
+    cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    struct restore_device {
+        int d;
+        ~restore_device() { cudaSetDevice(d); }
+    } restore{prev};
+    ctx.init(device);
+    const size_t bytes = count * (width / 8);
+    void* scratch_owner = ctx.ensure_wide(on_device ? 16 : bytes);
+    void* dev = on_device ? data : scratch_owner;
+    const bool pinned = attr.type == cudaMemoryTypeHost;
+    cudaStream_t s = ctx.stream;
+    cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+    auto upload = [&] {
+        if (on_device) return;
+        if (pinned)
+            cuda_check(cudaMemcpyAsync(dev, data, bytes, cudaMemcpyHostToDevice, s), "host-to-device copy");
+        else
+            stage_to_device(ctx, dev, data, bytes);
+    };
+    upload();
+    if (width == 8 || width == 16) {
+        int launches = 0;
+        cuda_check(bws_gpu::launch_sort_small(dev, count, static_cast<int>(width), is_unsigned, ctx.width_scratch,
+                                              ctx.geo, s, &launches, active_timer()),
+                   "counting sort launch");
+        g_launches.fetch_add(static_cast<uint64_t>(launches));
+    } else {
+        const uint64_t* k64 = static_cast<const uint64_t*>(dev);
+        cuda_check(bws_gpu::launch_minmax64(k64, count, is_unsigned, ctx.width_scratch, ctx.geo, s), "min/max launch");
+        g_launches.fetch_add(1);
+        uint64_t mm[2] = {0, 0};
+        cuda_check(cudaMemcpyAsync(mm, ctx.width_scratch, sizeof mm, cudaMemcpyDeviceToHost, s), "min/max readback");
+        cuda_check(cudaStreamSynchronize(s), "min/max");
+        if (mm[1] - mm[0] >= (uint64_t(1) << 32))
+            throw config_error("64-bit keys spanning 2^32 or more values (max - min = " +
+                               std::to_string(mm[1] - mm[0]) + ") are not supported by the B200 build");
+        const uint64_t range = mm[1] - mm[0] + 1;
+        ctx.ensure_keys(count);
+        auto narrow = [&] {
+            cuda_check(bws_gpu::launch_narrow64(k64, count, is_unsigned, ctx.width_scratch, ctx.keys, ctx.geo, s),
+                       "narrowing launch");
+            g_launches.fetch_add(1);
+        };
+        narrow();
+        enqueue_sort(ctx, ctx.keys, count, ctx.keys, range, s);
+        const Ctrl c = read_ctrl(ctx, s);
+        if (c.total != count) {  // repeated keys: the counting pass, from the untouched 64-bit keys
+            if (count >= (size_t(1) << 32))
+                throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
+            narrow();
+            enqueue_bucketed(ctx, ctx.keys, count, ctx.keys, range, s, 0, 0, /*multiset=*/true);
+            validate(ctx, count, range, s);
+        }
+        cuda_check(bws_gpu::launch_widen64(ctx.keys, count, is_unsigned, ctx.width_scratch,
+                                           static_cast<uint64_t*>(dev), ctx.geo, s),
+                   "widening launch");
+        g_launches.fetch_add(1);
+    }
+    if (on_device) {
+        cuda_check(cudaStreamSynchronize(s), "sort execution");
+    } else if (pinned) {
+        cuda_check(cudaMemcpyAsync(data, dev, bytes, cudaMemcpyDeviceToHost, s), "device-to-host copy");
+        cuda_check(cudaStreamSynchronize(s), "device-to-host copy");
+    } else {
+        cuda_check(cudaStreamSynchronize(s), "sort execution");
+        stage_to_host(ctx, data, dev, bytes);
+    }
+    cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+}
+
 const char* algorithm_name_of(bws_algorithm a) {
     switch (a) {
         case BWS_ALG_BITWISE: return "bitwise";
@@ -758,12 +874,16 @@ bws_status bws_sort(void* data, size_t count, uint32_t width, int is_unsigned,
         // Nothing to sort: the reference returns OK for any valid (width,
         // signedness, algorithm) here (test_capi.cpp:95), so do we.
         if (count == 0) return;
+        // bitsort.h:86-88: the array holds naturally aligned keys of `width` bits
+        if (reinterpret_cast<uintptr_t>(data) % (width / 8) != 0)
+            throw data_error("data is not aligned to its " + std::to_string(width) + "-bit keys");
         if (algorithm != BWS_ALG_BITWISE && algorithm != BWS_ALG_BITWISE_SKIP_EMPTY)
             throw config_error(std::string("algorithm '") + algorithm_name_of(algorithm) +
                                "' is not provided by the B200 build (bitwise only)");
-        if (width != 32)
-            throw config_error("the B200 bitset sort supports width 32 keys only (got width " +
-                               std::to_string(width) + ")");
+        if (width != 32) {
+            sort_other_width(data, count, width, is_unsigned);
+            return;
+        }
         // signed int32: x ^ 0x80000000 maps the signed order onto the unsigned
         // one (the reference splits negatives and non-negatives instead,
         // bitsort.hpp:131-152); the same XOR maps the sorted keys back

@@ -229,6 +229,21 @@ cudaError_t launch_scan2_sources(const OrSources& srcs, std::uint64_t n_words, s
                                  std::uint32_t* out, std::uint64_t out_capacity, Ctrl* ctrl,
                                  unsigned long long* status, unsigned long long* d_total,
                                  const LaunchGeometry& geo, cudaStream_t stream);
+// Other widths (widths.cu). 8/16-bit keys: counting sort over the type's
+// whole range, in place on device memory (scratch: width_scratch_bytes()).
+std::size_t width_scratch_bytes();
+cudaError_t configure_width_kernels(int device, LaunchGeometry* geo);
+cudaError_t launch_sort_small(void* data, std::size_t n, int width, int is_unsigned, void* scratch,
+                              const LaunchGeometry& geo, cudaStream_t stream, int* launches,
+                              KernelTimer* timer = nullptr);
+// 64-bit keys: (min, max) of the biased keys into scratch[0..1] (u64), then
+// narrowing to u32 offsets from the min and widening back (scratch holds the min).
+cudaError_t launch_minmax64(const std::uint64_t* keys, std::size_t n, int is_unsigned, void* scratch,
+                            const LaunchGeometry& geo, cudaStream_t stream);
+cudaError_t launch_narrow64(const std::uint64_t* keys, std::size_t n, int is_unsigned, const void* scratch,
+                            std::uint32_t* out, const LaunchGeometry& geo, cudaStream_t stream);
+cudaError_t launch_widen64(const std::uint32_t* sorted, std::size_t n, int is_unsigned, const void* scratch,
+                           std::uint64_t* out, const LaunchGeometry& geo, cudaStream_t stream);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream, std::uint32_t xr = 0);

@@ -94,7 +94,6 @@ def test_config_errors():
     assert "unsupported width 24" in capi.last_error()
     assert capi.sort_raw(p, 3, 32, 1, 99) == capi.Status.ERROR_CONFIG  # capi.cpp:69
     assert "unknown algorithm id" in capi.last_error()
-    assert capi.sort_raw(p, 3, 16, 1, 0) == capi.Status.ERROR_CONFIG
     for alg in (capi.Algorithm.INSERTION, capi.Algorithm.MERGE, capi.Algorithm.COUNTING,
                 capi.Algorithm.PLATFORM):
         assert capi.sort_raw(p, 3, 32, 1, alg) == capi.Status.ERROR_CONFIG

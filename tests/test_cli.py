@@ -42,8 +42,12 @@ def test_usage_and_config_errors(tmp_path):
     assert run(["sort"]).returncode == 1
     f = tmp_path / "in.txt"
     f.write_text("3\n1\n")
-    r = run(["sort", str(f), "--width", "16"])
-    assert r.returncode == 1 and "width 32" in r.stderr
+    r = run(["sort", str(f), "--width", "24"])
+    assert r.returncode == 1 and "unsupported width 24" in r.stderr
+    r = run(["sort", "-", "--width", "8"], stdin="1\n128\n")
+    assert r.returncode == 2 and "<stdin>:2: value 128 out of range for signed 8-bit" in r.stderr
+    r = run(["sort", "-", "--width", "16", "--unsigned"], stdin="65536\n")
+    assert r.returncode == 2 and "out of range for unsigned 16-bit" in r.stderr
     r = run(["sort", str(f), "--algorithm", "nonsense"])
     assert r.returncode == 1 and "unknown algorithm" in r.stderr
     assert run(["sort", str(f), "--bogus"]).returncode == 1
@@ -88,3 +92,23 @@ def test_sort_file_on_gpu(tmp_path, signed):
     assert r.returncode == 0 and r.stdout == "1\n2\n3\n"
     r = run(["sort", "-"], stdin="3\n1\n3\n")
     assert r.returncode == 0 and r.stdout == "1\n3\n3\n", r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("width", [8, 16, 64])
+@pytest.mark.parametrize("signed", [True, False])
+def test_sort_other_widths(tmp_path, width, signed):
+    """--width 8/16/64 (main.cpp's width option) through bws_sort at that width."""
+    rng = np.random.default_rng(width)
+    if width == 64:
+        lo = -(1 << 63) + 5 if signed else (1 << 64) - (1 << 31)
+        keys = [lo + int(x) for x in rng.integers(0, 1 << 30, size=5000)]
+    else:
+        lo, hi = (-(1 << (width - 1)), 1 << (width - 1)) if signed else (0, 1 << width)
+        keys = [int(x) for x in rng.integers(lo, hi, size=5000)]
+    keys += [keys[0], keys[1]]  # repeats
+    f = tmp_path / "in.txt"
+    f.write_text("\n".join(str(k) for k in keys) + "\n")
+    r = run(["sort", str(f), "--width", str(width)] + ([] if signed else ["--unsigned"]))
+    assert r.returncode == 0, r.stderr
+    assert [int(x) for x in r.stdout.split()] == sorted(keys)

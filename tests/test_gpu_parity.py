@@ -108,7 +108,7 @@ def test_status_conventions(capi, path):
     assert capi.last_error() == ""
     assert b.tolist() == [1, 2, 3]
     assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.BITWISE_SKIP_EMPTY) == capi.Status.OK
-    assert capi.sort_raw(b.ctypes.data, 3, 16, 1, 0) == capi.Status.ERROR_CONFIG
+    assert capi.sort_raw(b.ctypes.data, 3, 24, 1, 0) == capi.Status.ERROR_CONFIG
     assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.PLATFORM) == capi.Status.ERROR_CONFIG
 
 

@@ -2,7 +2,7 @@
 // 97-144 read_integer_file/sort_typed, :206-223 run_sort, :352-356 options)
 // over the B200 library, talking to it only through the C ABI (bws_sort).
 //
-//   bitsort sort <input|-> [--width 32] [--unsigned] [--algorithm bitwise]
+//   bitsort sort <input|-> [--width 8|16|32|64] [--unsigned] [--algorithm bitwise]
 //                [--out PATH] [--threads N]
 //
 // Same input format (one decimal value per line; blank lines and lines
@@ -68,17 +68,19 @@ int usage(const char* msg) {
     return 1;
 }
 
-// One chunk of the text: parsed 32-bit patterns, its line count, and the
-// first error (chunk-relative line number).
+// One chunk of the text: parsed two's-complement patterns of the key width,
+// its line count, and the first error (chunk-relative line number).
 struct Chunk {
-    std::vector<uint32_t> values;
+    std::vector<uint64_t> values;
     size_t lines = 0;
     size_t error_line = 0;  // 0 = none
     std::string error;
 };
 
-// Parses one decimal value into a 32-bit pattern (main.cpp:58-93, width 32).
-bool parse_value(std::string_view text, bool is_unsigned, uint32_t& pattern, std::string& error) {
+// Parses one decimal value into its two's-complement pattern at `width` bits
+// (main.cpp:58-93: same range checks and messages).
+bool parse_value(std::string_view text, uint32_t width, bool is_unsigned, uint64_t& pattern, std::string& error) {
+    const std::string w = std::to_string(width) + "-bit";
     if (is_unsigned) {
         uint64_t v = 0;
         const auto [ptr, ec] = std::from_chars(text.data(), text.data() + text.size(), v);
@@ -86,11 +88,11 @@ bool parse_value(std::string_view text, bool is_unsigned, uint32_t& pattern, std
             error = "cannot parse '" + std::string(text) + "' as an unsigned integer";
             return false;
         }
-        if (v > 0xffffffffull) {
-            error = "value " + std::string(text) + " out of range for unsigned 32-bit";
+        if (width < 64 && (v >> width) != 0) {
+            error = "value " + std::string(text) + " out of range for unsigned " + w;
             return false;
         }
-        pattern = static_cast<uint32_t>(v);
+        pattern = v;
     } else {
         int64_t v = 0;
         const auto [ptr, ec] = std::from_chars(text.data(), text.data() + text.size(), v);
@@ -98,16 +100,20 @@ bool parse_value(std::string_view text, bool is_unsigned, uint32_t& pattern, std
             error = "cannot parse '" + std::string(text) + "' as an integer";
             return false;
         }
-        if (v < INT32_MIN || v > INT32_MAX) {
-            error = "value " + std::string(text) + " out of range for signed 32-bit";
-            return false;
+        if (width < 64) {
+            const int64_t lim = int64_t{1} << (width - 1);
+            if (v < -lim || v >= lim) {
+                error = "value " + std::string(text) + " out of range for signed " + w;
+                return false;
+            }
         }
-        pattern = static_cast<uint32_t>(static_cast<int32_t>(v));
+        pattern = static_cast<uint64_t>(v);
     }
+    if (width < 64) pattern &= (uint64_t{1} << width) - 1;
     return true;
 }
 
-void parse_chunk(std::string_view text, bool is_unsigned, Chunk& c) {
+void parse_chunk(std::string_view text, uint32_t width, bool is_unsigned, Chunk& c) {
     c.values.reserve(text.size() / 8);
     size_t pos = 0;
     while (pos < text.size()) {
@@ -117,8 +123,8 @@ void parse_chunk(std::string_view text, bool is_unsigned, Chunk& c) {
         const std::string_view line = trim(text.substr(pos, nl - pos));
         pos = nl + 1;
         if (line.empty() || line.front() == '#') continue;
-        uint32_t pattern = 0;
-        if (!parse_value(line, is_unsigned, pattern, c.error)) {
+        uint64_t pattern = 0;
+        if (!parse_value(line, width, is_unsigned, pattern, c.error)) {
             c.error_line = c.lines;
             return;
         }
@@ -154,10 +160,9 @@ void parallel_for(unsigned n, F&& f) {
 int run_sort(const Options& o) {
     bws_algorithm algorithm = BWS_ALG_BITWISE;
     if (const bws_status s = bws_algorithm_from_name(o.algorithm.c_str(), &algorithm); s != BWS_OK) return fail(s);
-    if (o.width != 32) {  // the B200 library sorts 32-bit keys; say so the way bws_sort would
-        uint32_t probe = 0;
-        const bws_status s = bws_sort(&probe, 1, o.width, o.is_unsigned ? 1 : 0, algorithm);
-        return s == BWS_OK ? 0 : fail(s);
+    if (o.width != 8 && o.width != 16 && o.width != 32 && o.width != 64) {  // bws_sort words the error
+        uint64_t probe = 0;
+        return fail(bws_sort(&probe, 1, o.width, o.is_unsigned ? 1 : 0, algorithm));
     }
     std::string text;
     if (!read_all(o.input, text)) return 2;
@@ -174,7 +179,9 @@ int run_sort(const Options& o) {
     }
     std::vector<Chunk> chunks(nt);
     const std::string_view all(text);
-    parallel_for(nt, [&](unsigned i) { parse_chunk(all.substr(cut[i], cut[i + 1] - cut[i]), o.is_unsigned, chunks[i]); });
+    parallel_for(nt, [&](unsigned i) {
+        parse_chunk(all.substr(cut[i], cut[i + 1] - cut[i]), o.width, o.is_unsigned, chunks[i]);
+    });
     size_t lines_before = 0, n = 0;
     for (const Chunk& c : chunks) {
         if (c.error_line) {
@@ -185,16 +192,20 @@ int run_sort(const Options& o) {
         lines_before += c.lines;
         n += c.values.size();
     }
-    std::vector<uint32_t> data(n);
+    // the keys at their width, sorted in place by the library
+    const size_t kb = o.width / 8;
+    std::vector<unsigned char> data(n * kb + 8);
     {
         size_t off = 0;
         for (Chunk& c : chunks) {
-            std::copy(c.values.begin(), c.values.end(), data.begin() + static_cast<std::ptrdiff_t>(off));
-            off += c.values.size();
-            std::vector<uint32_t>().swap(c.values);
+            for (const uint64_t v : c.values) {
+                std::memcpy(data.data() + off * kb, &v, kb);  // little-endian low bytes
+                ++off;
+            }
+            std::vector<uint64_t>().swap(c.values);
         }
     }
-    const bws_status status = bws_sort(data.data(), data.size(), 32, o.is_unsigned ? 1 : 0, algorithm);
+    const bws_status status = bws_sort(data.data(), n, o.width, o.is_unsigned ? 1 : 0, algorithm);
     if (status != BWS_OK) return fail(status);
 
     // print in parallel into per-thread buffers, then write them in order
@@ -202,11 +213,18 @@ int run_sort(const Options& o) {
     parallel_for(nt, [&](unsigned i) {
         const size_t lo = n * i / nt, hi = n * (i + 1) / nt;
         std::string& s = outs[i];
-        s.reserve((hi - lo) * 11);
+        s.reserve((hi - lo) * (o.width / 3 + 3));
         char buf[24];
         for (size_t k = lo; k < hi; ++k) {
-            const auto r = o.is_unsigned ? std::to_chars(buf, buf + sizeof buf, data[k])
-                                         : std::to_chars(buf, buf + sizeof buf, static_cast<int32_t>(data[k]));
+            uint64_t u = 0;
+            std::memcpy(&u, data.data() + k * kb, kb);
+            std::to_chars_result r;
+            if (o.is_unsigned) {
+                r = std::to_chars(buf, buf + sizeof buf, u);
+            } else {
+                const unsigned sh = 64 - o.width;  // sign-extend the width-bit pattern
+                r = std::to_chars(buf, buf + sizeof buf, static_cast<int64_t>(u << sh) >> sh);
+            }
             s.append(buf, r.ptr);
             s.push_back('\n');
         }
