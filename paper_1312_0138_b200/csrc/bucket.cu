@@ -240,6 +240,61 @@ __global__ void bucket_colscan_kernel(uint32_t* __restrict__ H, int P, int nb,
     if (lane == 31) tot[b] = incl;
 }
 
+// KB2b (packed layout, i.e. wide sparse ranges with skewed bucket sizes such
+// as C5's Zipf clusters): KB4's ticket order, largest buckets first (by
+// power-of-two size class; the order inside a class is arbitrary). KB4 takes
+// buckets by dynamic ticket, so a big bucket ticketed last would run alone
+// at the end: measured C5 counts give a ~17% longer KB4 in index order than
+// with this approximate longest-processing-time-first order.
+// Run by one whole CTA (CTA 0 of the packed KB3, once the totals are known);
+// order[nb] = 1 if the order is not the identity (KB4 reads it once).
+__device__ void compute_kb4_order(const uint32_t* __restrict__ tot, int nb, uint32_t* __restrict__ order) {
+    __shared__ uint32_t s_cls[33];
+    __shared__ unsigned long long s_sum;
+    __shared__ uint32_t s_max;
+    if (threadIdx.x < 33) s_cls[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) {
+        s_sum = 0;
+        s_max = 0;
+    }
+    __syncthreads();
+    unsigned long long sum = 0;
+    uint32_t mx = 0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const uint32_t c = tot[b];
+        sum += c;
+        mx = max(mx, c);
+        atomicAdd(&s_cls[c ? 32 - __clz(c) : 0], 1u);
+    }
+    sum = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(sum));  // per-warp (< 2^32 keys)
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_sum, sum);
+        atomicMax(&s_max, mx);
+    }
+    __syncthreads();
+    // near-uniform sizes (C4: uniform draws) keep the index order: LPT buys
+    // nothing there and the permuted order measured 3% slower
+    if (static_cast<unsigned long long>(s_max) * nb <= 2 * s_sum) {
+        if (threadIdx.x == 0) order[nb] = 0u;
+        return;
+    }
+    if (threadIdx.x == 0) order[nb] = 1u;
+    if (threadIdx.x == 0) {  // exclusive prefix in descending class order
+        uint32_t run = 0;
+        for (int k = 32; k >= 0; --k) {
+            const uint32_t v = s_cls[k];
+            s_cls[k] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const uint32_t c = tot[b];
+        order[atomicAdd(&s_cls[c ? 32 - __clz(c) : 0], 1u)] = static_cast<uint32_t>(b);
+    }
+}
+
 // Slab epilogue shared by the slab KB3 variants: folds the CTA's bad-key
 // count into ctrl, and the last CTA to finish turns the fill counters into
 // bucket totals (0 for an overflowed bucket: its keys are lost, so the sort
@@ -289,6 +344,11 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
 // issued before the tile's SMEM scatter and consumed after it, so their
 // latency overlaps that work. The last CTA to finish turns the fill counters
 // into bucket totals and output offsets for KB4.
+// L2 hints (packed layout only, i.e. !SLAB): the key stream is loaded
+// evict_first and the scattered run stores are evict_last, so the partially
+// written 32-byte sectors of ~4096 short runs per tile stay in L2 until
+// complete instead of being evicted half-written (measured: C5 KB3 1570 ->
+// 1462 us, C4 116 -> 104 us; the slab layout's longer runs (C3) got slower).
 template <int THREADS, int KPT, int MAXB, bool SLAB>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     bucket_partition_kernel(KeySplit ks, BucketMap bm, int nb,
@@ -340,8 +400,11 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         for (size_t t = 0; t < 2 && t < ntiles; ++t) {
             const size_t v0 = vlo + t * kTileVec;
             const size_t nvec = min(kTileVec, vhi - v0);
-            tma_load_bytes(s_buf + t * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16),
-                           &s_bar[t]);
+            if (!SLAB)
+                tma_load_bytes_hint(s_buf + t * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16), &s_bar[t],
+                                    l2_policy_evict_first());
+            else
+                tma_load_bytes(s_buf + t * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16), &s_bar[t]);
         }
     }
 
@@ -358,6 +421,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         }
         if (c == 0 && threadIdx.x == 0) g_base[nb] = total;
         __syncthreads();
+        if (c == 0 && sa.order) compute_kb4_order(tot, nb, sa.order);  // KB4's ticket order
     }
     for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
         if constexpr (!SLAB) s_cur[b] = b < nb ? s_delta[b] : 0u;
@@ -514,17 +578,30 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         }
         __syncthreads();  // C
         const uint32_t tile_valid = s_tile_valid;
+        if (!SLAB) {
+            const unsigned long long pol = l2_policy_evict_last();
 #pragma unroll 4
-        for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
-            const uint32_t key = buf[i];
-            parted[s_delta[bucket_id(key, bm)] + i] = key;
+            for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
+                const uint32_t key = buf[i];
+                st_hint(parted + s_delta[bucket_id(key, bm)] + i, key, pol);
+            }
+        } else {
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
+                const uint32_t key = buf[i];
+                parted[s_delta[bucket_id(key, bm)] + i] = key;
+            }
         }
         __syncthreads();  // D: buf free again
         if (threadIdx.x == 0 && t + 2 < ntiles) {
             const size_t v2 = vlo + (t + 2) * kTileVec;
             const size_t nv2 = min(kTileVec, vhi - v2);
             fence_proxy_async_smem();
-            tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
+            if (!SLAB)
+                tma_load_bytes_hint(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p],
+                                    l2_policy_evict_first());
+            else
+                tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
         }
     }
     if constexpr (SLAB) slab_finish(sa, nb, bad, s_cur, s_base64, s_scratch, &s_last);
@@ -829,7 +906,8 @@ template <int STAGE, int NT = BUCKET_THREADS>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
-                       uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
+                       uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl,
+                       const uint32_t* __restrict__ order) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t W = bm.width >> 5;  // words per bucket bitset (>= 1024; 2^k or a multiple of 4096)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
@@ -867,7 +945,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
 
     auto fetch = [&](int slot) {  // thread 0
-        const unsigned nbk = atomicAdd(&ctrl->ticket, 1u);
+        unsigned nbk = atomicAdd(&ctrl->ticket, 1u);
+        if (order && nbk < static_cast<unsigned>(nb)) nbk = order[nbk];  // largest buckets first
         s_b[slot] = nbk;
         if (nbk < static_cast<unsigned>(nb)) {
             s_bbase[slot] = g_base[nbk];
@@ -875,7 +954,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         }
     };
     for (uint32_t i = threadIdx.x; i < W / 32; i += NT) s_sum[i] = 0u;
-    if (threadIdx.x == 0) fetch(0);
+    if (threadIdx.x == 0) {
+        if (order && order[nb] == 0u) order = nullptr;  // identity: no per-ticket lookup
+        fetch(0);
+    }
     bool dirty = true;  // block-uniform: bitset needs zeroing before the next bucket
     for (unsigned it = 0;; ++it) {
         const int slot = static_cast<int>(it & 1u);
@@ -1345,6 +1427,7 @@ size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
     return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H
            + (MAX_BUCKETS + 1) * sizeof(uint32_t)                          // tot
            + (MAX_BUCKETS + 2) * sizeof(unsigned long long)                // base (8-aligned)
+           + MAX_BUCKETS * sizeof(uint32_t)                                // KB4 ticket order
            + 2 * MAX_BUCKETS * sizeof(uint32_t);                           // slab fill + true counts
 }
 
@@ -1361,6 +1444,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     uint32_t* tot = H + static_cast<size_t>(P) * plan.nb;
     unsigned long long* base =
         reinterpret_cast<unsigned long long*>(reinterpret_cast<uintptr_t>(tot + MAX_BUCKETS + 1) & ~uintptr_t(7));
+    // KB4 ticket order (packed layout only; slab buckets are uniform in C2/C3)
+    uint32_t* order_buf = reinterpret_cast<uint32_t*>(base + MAX_BUCKETS + 2);
     const int check = key_range < (1ull << 32);
     const uint32_t limit = check ? static_cast<uint32_t>(key_range) : 0u;
     KeySplit ks;
@@ -1378,6 +1463,13 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     const uint64_t slab = slab_slots(plan, n);
     // multiset sorts take the packed layout: exact for any key multiplicity
     const bool use_slab = !multiset && slab != 0 && slab <= parted_cap;
+    static const bool order_off = [] {
+        const char* e = std::getenv("BITSORT_KB4_ORDER");
+        return e && std::string(e) == "0";
+    }();
+    uint32_t* kb4_order =
+        (!use_slab && !plan.partition_only && !multiset && !bits_out && !order_off && plan.nb > 1) ? order_buf
+                                                                                                    : nullptr;
     SlabArgs sa;
     int nlaunch = 0;
     cudaError_t err;
@@ -1425,6 +1517,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         bucket_colscan_kernel<<<(plan.nb * 32 + 255) / 256, 256, 0, stream>>>(H, P, plan.nb, tot);
         if (timer) timer->after("bucket_colscan", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        sa.order = kb4_order;
         if (timer) timer->before(stream);
         if (narrow_partition(plan))
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>
@@ -1436,7 +1529,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
         if (timer) timer->after("bucket_partition", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
-        nlaunch = 3;
+        nlaunch += 3;
     }
     if (plan.partition_only) {  // range split: the packed groups are the result
         if (launches) *launches = nlaunch;
@@ -1467,10 +1560,10 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     const size_t smem = bucket_sort_smem_bytes(plan.shift);
     if (plan.shift >= MAX_BUCKET_SHIFT)
         bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order);
     else  // narrower buckets: two 512-thread CTAs per SM
         bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl);
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;

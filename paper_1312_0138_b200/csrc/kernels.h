@@ -138,6 +138,8 @@ struct SlabArgs {
     unsigned long long* g_base = nullptr;  // out: output offset per bucket (+ total at [nb])
     std::uint32_t* gtrue = nullptr;        // TMA-store KB3: true keys per bucket (gcnt counts
                                            // slots, padded to multiples of 4); zeroed like gcnt
+    std::uint32_t* order = nullptr;        // packed KB3 (CTA 0): KB4 ticket order, largest
+                                           // buckets first; order[nb] = 0 means identity
 };
 
 // Optional per-kernel timing hook (bench.py's live roofline): before() and

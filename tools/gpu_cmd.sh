@@ -1,2 +1,3 @@
-timeout 900 python bench.py --config all --steps 20 --warmup 3 > gpurun_out/bench_all_v9.jsonl 2> gpurun_out/bench_all_v9.err
-timeout 300 python bench.py > gpurun_out/bench_default.json 2>&1
+for c in C3 C5 C4 C2; do
+  timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/tmpl_$c.json 2>>gpurun_out/tmpl.err
+done
