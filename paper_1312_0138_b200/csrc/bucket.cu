@@ -661,7 +661,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         const size_t v0 = vlo + t * kTileVec;
         const size_t nvec = min(kTileVec, vhi - v0);
         fence_proxy_async_smem();
-        tma_load_bytes(s_ring + p * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16), &s_bar[p]);
+        // the key stream is read once: evict_first keeps L2 for the runs KB4
+        // reads next (measured C2 KB4 146.6 -> 144.2 us)
+        tma_load_bytes_hint(s_ring + p * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16), &s_bar[p],
+                            l2_policy_evict_first());
     };
 
     if (threadIdx.x == 0) {
