@@ -26,8 +26,8 @@
  *   width 32  the bitset sort (the hot path); repeated keys are detected and
  *             sorted by a GPU counting-sort pass, as the reference sorts them;
  *   width 8/16  a GPU counting sort over the type's range;
- *   width 64  keys whose span max - min is below 2^32 (narrowed to the 32-bit
- *             path); wider spans return BWS_ERROR_CONFIG.
+ *   width 64  keys whose span max - min is below 2^32 narrowed to the 32-bit
+ *             path; wider spans by a stable LSD radix sort (8-bit digits).
  * Other algorithms return BWS_ERROR_CONFIG. There is no CPU fallback.
  * Additive GPU extensions live in bitsort_gpu.h.
  */

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
@@ -761,8 +762,12 @@ void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned)
     } restore{prev};
     ctx.init(device);
     const size_t bytes = count * (width / 8);
-    void* scratch_owner = ctx.ensure_wide(on_device ? 16 : bytes);
+    // host arrays: keys at wide[0, bytes); every 64-bit sort also gets a
+    // second array of `bytes` (the radix sort's ping-pong partner)
+    const size_t partner = width == 64 ? bytes : 0;
+    void* scratch_owner = ctx.ensure_wide((on_device ? 0 : bytes) + partner + 16);
     void* dev = on_device ? data : scratch_owner;
+    void* other = static_cast<unsigned char*>(scratch_owner) + (on_device ? 0 : bytes);
     const bool pinned = attr.type == cudaMemoryTypeHost;
     cudaStream_t s = ctx.stream;
     cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
@@ -787,30 +792,60 @@ void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned)
         uint64_t mm[2] = {0, 0};
         cuda_check(cudaMemcpyAsync(mm, ctx.width_scratch, sizeof mm, cudaMemcpyDeviceToHost, s), "min/max readback");
         cuda_check(cudaStreamSynchronize(s), "min/max");
-        if (mm[1] - mm[0] >= (uint64_t(1) << 32))
-            throw config_error("64-bit keys spanning 2^32 or more values (max - min = " +
-                               std::to_string(mm[1] - mm[0]) + ") are not supported by the B200 build");
-        const uint64_t range = mm[1] - mm[0] + 1;
-        ctx.ensure_keys(count);
-        auto narrow = [&] {
-            cuda_check(bws_gpu::launch_narrow64(k64, count, is_unsigned, ctx.width_scratch, ctx.keys, ctx.geo, s),
-                       "narrowing launch");
+        if (mm[1] - mm[0] >= (uint64_t(1) << 32)) {
+            // a span beyond the bitset sort's 2^32: stable LSD radix passes over
+            // the 8-bit digits on which the keys differ
+            if (count >= (size_t(1) << 32)) throw std::out_of_range("64-bit radix sorts take fewer than 2^32 keys");
+            if (bws_gpu::radix64_scratch_bytes(ctx.geo) > bws_gpu::width_scratch_bytes())
+                throw std::runtime_error("radix scratch too small");
+            cuda_check(bws_gpu::launch_radix64_hist(k64, count, is_unsigned, ctx.width_scratch, ctx.geo, s),
+                       "radix histogram launch");
             g_launches.fetch_add(1);
-        };
-        narrow();
-        enqueue_sort(ctx, ctx.keys, count, ctx.keys, range, s);
-        const Ctrl c = read_ctrl(ctx, s);
-        if (c.total != count) {  // repeated keys: the counting pass, from the untouched 64-bit keys
-            if (count >= (size_t(1) << 32))
-                throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
+            std::vector<uint64_t> hist(8 * 256);
+            cuda_check(cudaMemcpyAsync(hist.data(), ctx.width_scratch, hist.size() * sizeof(uint64_t),
+                                       cudaMemcpyDeviceToHost, s),
+                       "radix histogram readback");
+            cuda_check(cudaStreamSynchronize(s), "radix histogram");
+            std::vector<int> digits;
+            for (int d = 0; d < 8; ++d)
+                if (*std::max_element(hist.begin() + 256 * d, hist.begin() + 256 * (d + 1)) != count)
+                    digits.push_back(d);
+            const uint64_t bias = is_unsigned ? 0 : (uint64_t(1) << 63);
+            uint64_t* cur = static_cast<uint64_t*>(dev);
+            uint64_t* nxt = static_cast<uint64_t*>(other);
+            for (size_t j = 0; j < digits.size(); ++j) {
+                cuda_check(bws_gpu::launch_radix64_pass(cur, nxt, count, digits[j], j == 0 ? bias : 0,
+                                                        j + 1 == digits.size() ? bias : 0, ctx.width_scratch,
+                                                        ctx.geo, s),
+                           "radix pass launch");
+                g_launches.fetch_add(3);
+                std::swap(cur, nxt);
+            }
+            if (cur != dev)
+                cuda_check(cudaMemcpyAsync(dev, cur, bytes, cudaMemcpyDeviceToDevice, s), "radix result copy");
+        } else {
+            const uint64_t range = mm[1] - mm[0] + 1;
+            ctx.ensure_keys(count);
+            auto narrow = [&] {
+                cuda_check(bws_gpu::launch_narrow64(k64, count, is_unsigned, ctx.width_scratch, ctx.keys, ctx.geo, s),
+                           "narrowing launch");
+                g_launches.fetch_add(1);
+            };
             narrow();
-            enqueue_bucketed(ctx, ctx.keys, count, ctx.keys, range, s, 0, 0, /*multiset=*/true);
-            validate(ctx, count, range, s);
+            enqueue_sort(ctx, ctx.keys, count, ctx.keys, range, s);
+            const Ctrl c = read_ctrl(ctx, s);
+            if (c.total != count) {  // repeated keys: the counting pass, from the untouched 64-bit keys
+                if (count >= (size_t(1) << 32))
+                    throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
+                narrow();
+                enqueue_bucketed(ctx, ctx.keys, count, ctx.keys, range, s, 0, 0, /*multiset=*/true);
+                validate(ctx, count, range, s);
+            }
+            cuda_check(bws_gpu::launch_widen64(ctx.keys, count, is_unsigned, ctx.width_scratch,
+                                               static_cast<uint64_t*>(dev), ctx.geo, s),
+                       "widening launch");
+            g_launches.fetch_add(1);
         }
-        cuda_check(bws_gpu::launch_widen64(ctx.keys, count, is_unsigned, ctx.width_scratch,
-                                           static_cast<uint64_t*>(dev), ctx.geo, s),
-                   "widening launch");
-        g_launches.fetch_add(1);
     }
     if (on_device) {
         cuda_check(cudaStreamSynchronize(s), "sort execution");

@@ -246,6 +246,17 @@ cudaError_t launch_narrow64(const std::uint64_t* keys, std::size_t n, int is_uns
                             std::uint32_t* out, const LaunchGeometry& geo, cudaStream_t stream);
 cudaError_t launch_widen64(const std::uint32_t* sorted, std::size_t n, int is_unsigned, const void* scratch,
                            std::uint64_t* out, const LaunchGeometry& geo, cudaStream_t stream);
+// 64-bit keys of any span: stable LSD radix sort with 8-bit digits. hist:
+// scratch[0 .. 8*256) u64 = global histogram of every digit of the biased
+// keys (the host skips digits on which all keys agree); pass: one stable
+// scatter by digit `digit` from in to out (keys XORed with xin on load and
+// xout on store, n < 2^32).
+std::size_t radix64_scratch_bytes(const LaunchGeometry& geo);
+cudaError_t launch_radix64_hist(const std::uint64_t* keys, std::size_t n, int is_unsigned, void* scratch,
+                                const LaunchGeometry& geo, cudaStream_t stream);
+cudaError_t launch_radix64_pass(const std::uint64_t* in, std::uint64_t* out, std::size_t n, int digit,
+                                std::uint64_t xin, std::uint64_t xout, void* scratch, const LaunchGeometry& geo,
+                                cudaStream_t stream);
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream, std::uint32_t xr = 0);

@@ -15,7 +15,8 @@
 //
 // 64-bit keys whose span max - min is below 2^32 are narrowed on the GPU to
 // u32 offsets from the minimum, sorted by the 32-bit pipeline (repeats
-// included) and widened back; the bias 2^63 maps signed order onto unsigned.
+// included) and widened back; wider spans take a stable LSD radix sort with
+// 8-bit digits (KR0-KR3 below). The bias 2^63 maps signed order onto unsigned.
 #include "kernels.h"
 #include "device_util.cuh"
 
@@ -221,6 +222,128 @@ cudaError_t launch_small(T* data, size_t n, int is_unsigned, unsigned long long*
     return cudaGetLastError();
 }
 
+
+// ---- 64-bit keys of any span: stable LSD radix sort, 8-bit digits ----------
+// (the reference's own algorithm family: bitsort.hpp:84-129 is an LSD radix
+// sort with 1-bit digits and stable partitions; here 8-bit digits, and digits
+// on which every key agrees are skipped, like skip_empty_bits.)
+//   KR0 rx_hist_all  global histogram of all 8 digits in one read (host then
+//                    skips the constant digits)
+//   per remaining digit:
+//   KR1 rx_hist      per-CTA digit histogram of its contiguous chunk
+//   KR2 rx_offsets   one CTA: exclusive prefix in (digit, CTA) order
+//   KR3 rx_scatter   stable scatter: the chunk in rounds of 256 keys (thread t
+//                    takes key r*256 + t); rank inside a warp from match.any,
+//                    across the 8 warps from a per-round digit x warp count
+//                    table (double-buffered: 2 barriers per round)
+constexpr int RX_THREADS = 256;
+constexpr int RX_WARPS = RX_THREADS / 32;
+
+__device__ __forceinline__ void rx_chunk(size_t n, size_t& c0, size_t& c1) {
+    const size_t per = (n + gridDim.x - 1) / gridDim.x;
+    c0 = min(n, per * blockIdx.x);
+    c1 = min(n, c0 + per);
+}
+
+__global__ void __launch_bounds__(RX_THREADS)
+    rx_hist_all_kernel(const unsigned long long* __restrict__ in, size_t n, unsigned long long bias,
+                       unsigned long long* __restrict__ hist /* [8][256] */) {
+    __shared__ uint32_t s_h[8 * 256];
+    for (int i = threadIdx.x; i < 8 * 256; i += RX_THREADS) s_h[i] = 0u;
+    __syncthreads();
+    for (size_t i = blockIdx.x * static_cast<size_t>(RX_THREADS) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * RX_THREADS) {
+        const unsigned long long k = __ldcs(in + i) ^ bias;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) atomicAdd(&s_h[d * 256 + ((k >> (8 * d)) & 255u)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += RX_THREADS)
+        if (s_h[i]) atomicAdd(hist + i, static_cast<unsigned long long>(s_h[i]));
+}
+
+__global__ void __launch_bounds__(RX_THREADS)
+    rx_hist_kernel(const unsigned long long* __restrict__ in, size_t n, unsigned long long xin, int shift,
+                   uint32_t* __restrict__ H /* [256][P] */) {
+    __shared__ uint32_t s_h[256];
+    s_h[threadIdx.x] = 0u;
+    __syncthreads();
+    size_t c0, c1;
+    rx_chunk(n, c0, c1);
+    for (size_t i = c0 + threadIdx.x; i < c1; i += RX_THREADS)
+        atomicAdd(&s_h[((__ldcs(in + i) ^ xin) >> shift) & 255u], 1u);
+    __syncthreads();
+    H[static_cast<size_t>(threadIdx.x) * gridDim.x + blockIdx.x] = s_h[threadIdx.x];
+}
+
+// One CTA: H[i] <- sum of H[< i] (i over 256 * P entries, digit-major).
+__global__ void __launch_bounds__(1024) rx_offsets_kernel(uint32_t* __restrict__ H, int total) {
+    __shared__ uint32_t s_w[32];
+    const int per = (total + 1023) / 1024;
+    const int b0 = threadIdx.x * per;
+    uint32_t local = 0;
+    for (int i = 0; i < per; ++i)
+        if (b0 + i < total) local += H[b0 + i];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t incl = warp_incl_scan(local, lane);
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_w[lane];
+        s_w[lane] = warp_incl_scan(w, lane) - w;
+    }
+    __syncthreads();
+    uint32_t run = s_w[warp] + incl - local;
+    for (int i = 0; i < per; ++i) {
+        if (b0 + i < total) {
+            const uint32_t v = H[b0 + i];
+            H[b0 + i] = run;
+            run += v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RX_THREADS)
+    rx_scatter_kernel(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out, size_t n,
+                      unsigned long long xin, unsigned long long xout, int shift,
+                      const uint32_t* __restrict__ H) {
+    __shared__ uint32_t s_base[256];                // next output slot per digit
+    __shared__ uint32_t s_w[2][RX_WARPS][256];      // per round: warp x digit counts -> slots
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned t = threadIdx.x;                 // also: the digit this thread scans
+    s_base[t] = H[static_cast<size_t>(t) * gridDim.x + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < RX_WARPS; ++w) s_w[0][w][t] = s_w[1][w][t] = 0u;
+    __syncthreads();
+    size_t c0, c1;
+    rx_chunk(n, c0, c1);
+    const unsigned lt = lanemask_lt();
+    int buf = 0;
+    for (size_t r0 = c0; r0 < c1; r0 += RX_THREADS, buf ^= 1) {
+        const size_t i = r0 + t;
+        const bool in_range = i < c1;
+        const unsigned long long k = in_range ? (__ldcs(in + i) ^ xin) : 0ull;
+        const uint32_t d = in_range ? static_cast<uint32_t>((k >> shift) & 255u) : 256u;
+        const unsigned peers = __match_any_sync(kFull, d);
+        const uint32_t rank = __popc(peers & lt);
+        if (in_range && rank == 0) s_w[buf][warp][d] = __popc(peers);
+        __syncthreads();
+        {  // digit t: exclusive prefix over the warps, offset by the digit's running base
+            uint32_t run = s_base[t];
+#pragma unroll
+            for (int w = 0; w < RX_WARPS; ++w) {
+                const uint32_t c = s_w[buf][w][t];
+                s_w[buf][w][t] = run;
+                run += c;
+                s_w[buf ^ 1][w][t] = 0u;  // next round's table (its readers finished last round)
+            }
+            s_base[t] = run;
+        }
+        __syncthreads();
+        if (in_range) __stcs(out + s_w[buf][warp][d] + rank, k ^ xout);
+    }
+}
+
 }  // namespace
 
 std::size_t width_scratch_bytes() { return 2 * (std::size_t(1) << 16) * sizeof(unsigned long long) + 64; }
@@ -266,6 +389,41 @@ cudaError_t launch_widen64(const std::uint32_t* sorted, std::size_t n, int is_un
     widen64_kernel<<<geo.fill_blocks, 256, 0, stream>>>(sorted, n, is_unsigned ? 0ull : (1ull << 63),
                                                          static_cast<const unsigned long long*>(scratch),
                                                          reinterpret_cast<unsigned long long*>(out));
+    return cudaGetLastError();
+}
+
+}  // namespace bws_gpu
+
+namespace bws_gpu {
+
+std::size_t radix64_scratch_bytes(const LaunchGeometry& geo) {
+    return 8 * 256 * sizeof(unsigned long long) + static_cast<std::size_t>(256) * (geo.multiset_blocks * 4) * 4 + 64;
+}
+
+cudaError_t launch_radix64_hist(const std::uint64_t* keys, std::size_t n, int is_unsigned, void* scratch,
+                                const LaunchGeometry& geo, cudaStream_t stream) {
+    auto* hist = static_cast<unsigned long long*>(scratch);
+    cudaError_t err = cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(unsigned long long), stream);
+    if (err != cudaSuccess) return err;
+    rx_hist_all_kernel<<<geo.multiset_blocks * 4, RX_THREADS, 0, stream>>>(
+        reinterpret_cast<const unsigned long long*>(keys), n, is_unsigned ? 0ull : (1ull << 63), hist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_radix64_pass(const std::uint64_t* in, std::uint64_t* out, std::size_t n, int digit,
+                                std::uint64_t xin, std::uint64_t xout, void* scratch, const LaunchGeometry& geo,
+                                cudaStream_t stream) {
+    const int P = geo.multiset_blocks * 4;
+    uint32_t* H = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(scratch) +
+                                              8 * 256 * sizeof(unsigned long long));
+    const auto* i64 = reinterpret_cast<const unsigned long long*>(in);
+    rx_hist_kernel<<<P, RX_THREADS, 0, stream>>>(i64, n, xin, 8 * digit, H);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    rx_offsets_kernel<<<1, 1024, 0, stream>>>(H, 256 * P);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    rx_scatter_kernel<<<P, RX_THREADS, 0, stream>>>(i64, reinterpret_cast<unsigned long long*>(out), n, xin, xout,
+                                                    8 * digit, H);
     return cudaGetLastError();
 }
 

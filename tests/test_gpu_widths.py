@@ -115,18 +115,40 @@ def test_64bit_narrow_span(capi, cuda, signed, n, span_log2):
     assert np.array_equal(_device(capi, cuda, keys, offset=8), expected)
 
 
-def test_64bit_wide_span_rejected(capi):
-    keys = np.array([5, 1 << 40, 3], dtype=np.uint64)
-    a = keys.copy()
-    assert capi.sort_raw(a.ctypes.data, 3, 64, 1, 0) == capi.Status.ERROR_CONFIG
-    assert "2^32" in capi.last_error()
-    assert np.array_equal(a, keys)
-    b = np.array([-(1 << 40), 7], dtype=np.int64)
-    assert capi.sort_raw(b.ctypes.data, 2, 64, 0, 0) == capi.Status.ERROR_CONFIG
+@pytest.mark.parametrize("signed", [False, True])
+@pytest.mark.parametrize("n", [2, 3, 255, 1000, 65537, (1 << 20) + 7])
+@pytest.mark.parametrize("kind", ["full_range", "high_bits", "repeats"])
+def test_64bit_wide_span_radix(capi, cuda, signed, n, kind):
+    """Spans of 2^32 values or more: the stable LSD radix path (8-bit digits,
+    constant digits skipped)."""
+    rng = np.random.default_rng(n * 3 + len(kind))
+    dt = np.int64 if signed else np.uint64
+    info = np.iinfo(dt)
+    if kind == "full_range":
+        keys = rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+    elif kind == "high_bits":  # only bits 40-47 and 0-3 vary: most digits are skipped
+        keys = ((rng.integers(0, 256, size=n).astype(np.uint64) << np.uint64(40)) |
+                rng.integers(0, 16, size=n).astype(np.uint64)).astype(dt)
+    else:
+        vals = rng.integers(info.min, info.max, size=max(2, n // 50), dtype=dt, endpoint=True)
+        keys = vals[rng.integers(0, vals.size, size=n)]
+    keys[0], keys[-1] = info.min, info.max
+    expected = _expected(keys)
+    assert np.array_equal(expected, np.sort(keys))
+    assert np.array_equal(_host(capi, keys), expected)
+    assert np.array_equal(_device(capi, cuda, keys, offset=1), expected)
+
+
+def test_64bit_edges(capi):
     c = np.array([np.iinfo(np.int64).min, np.iinfo(np.int64).min + 5, np.iinfo(np.int64).min], dtype=np.int64)
     assert capi.sort_raw(c.ctypes.data, 3, 64, 0, 0) == capi.Status.OK, capi.last_error()
-    assert np.array_equal(c, np.sort(np.array([np.iinfo(np.int64).min, np.iinfo(np.int64).min + 5,
-                                               np.iinfo(np.int64).min], dtype=np.int64)))
+    assert c.tolist() == sorted(c.tolist())
+    d = np.full(1000, 1 << 63, dtype=np.uint64)  # all equal: no radix pass at all
+    assert capi.sort_raw(d.ctypes.data, d.size, 64, 1, 0) == capi.Status.OK
+    assert bool((d == np.uint64(1 << 63)).all())
+    e = np.array([5, 1 << 40, 3], dtype=np.uint64)  # 3 keys, span > 2^32
+    assert capi.sort_raw(e.ctypes.data, 3, 64, 1, 0) == capi.Status.OK
+    assert e.tolist() == [3, 5, 1 << 40]
 
 
 def test_misaligned_data_rejected(capi):
