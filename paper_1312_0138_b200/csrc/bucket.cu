@@ -570,7 +570,10 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 if (ccnt[q]) {
                     const uint32_t b = sb + q;
                     // a claim past the bucket's capacity (only duplicates can cause
-                    // one) lands in the dump tile instead
+                    // one) is aimed at the dump tile, whose stores are then skipped
+                    // (a bucket that overflowed sorts nothing; repeated keys can
+                    // overflow every tile's run, and concurrent stores to one dump
+                    // tile measured 3 ms on 2^26 keys)
                     const uint32_t dst = claim[q] + ccnt[q] <= sa.cap ? b * sa.cap + claim[q] : sa.dump;
                     s_delta[b] = dst - s_start[b];
                 }
@@ -589,7 +592,8 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
                 const uint32_t key = buf[i];
-                parted[s_delta[bucket_id(key, bm)] + i] = key;
+                const uint32_t pos = s_delta[bucket_id(key, bm)] + i;
+                if (pos < sa.dump) parted[pos] = key;  // dump-tile runs are dropped
             }
         }
         __syncthreads();  // D: buf free again
@@ -819,13 +823,16 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
                 const uint32_t st = s_start[b];
                 for (uint32_t i = cb; i < pc; ++i) s_sorted[st + i] = s_sorted[st];  // pad with a repeat
                 fence_proxy_async_smem();
-                // a claim past the bucket's capacity (only duplicates cause one) goes to the dump tile
-                uint32_t* dst = parted + (claim[q] + pc <= sa.cap ? static_cast<size_t>(b) * sa.cap + claim[q]
-                                                                  : static_cast<size_t>(sa.dump));
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                             "r"(smem_u32(s_sorted + st)), "r"(pc * 4)
-                             : "memory");
-                stores_pending = true;
+                // a claim past the bucket's capacity (only duplicates cause one) is
+                // dropped: that bucket then sorts nothing and the popcount total
+                // reports the repeats
+                if (claim[q] + pc <= sa.cap) {
+                    uint32_t* dst = parted + static_cast<size_t>(b) * sa.cap + claim[q];
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                                 "r"(smem_u32(s_sorted + st)), "r"(pc * 4)
+                                 : "memory");
+                    stores_pending = true;
+                }
             }
         }
         if (stores_pending) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -1134,25 +1141,31 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
 
 // KB4m (multiset sorts, bws_sort on input with repeated keys): the counting
 // sort of a bucket (baselines.hpp:99-122's counting_sort with the bucket as its
-// span) in shared memory. The bucket's width is covered by windows of
-// 2^MS_WIN_SHIFT values; per window: 32-bit SMEM counters (atomicAdd per key
-// of the window), a block-wide inclusive prefix of the counters, and the
-// expansion — output slot i of the window takes the value whose prefix first
-// exceeds i (binary search), so a value repeated 2^26 times is written by all
-// threads, coalesced. Windows with no keys are skipped (per-window counts from
-// a first pass). The output range of a bucket is the prefix of the bucket
+// span) in shared memory. The bucket's width is covered by windows of values
+// with SMEM counters — 16-bit counters over 2^16 values when the bucket holds
+// fewer than 2^16 keys (no counter can overflow), else 32-bit counters over
+// 2^15 values. Per window: one counting pass over the bucket's keys (staged in
+// SMEM once when they fit, else 16-byte-batched loads), a block-wide
+// inclusive prefix of the counters (lane-rotated LDS.128, conflict-free) and
+// the expansion — output slot i of the window takes the value whose prefix
+// first exceeds i (binary search), so a value repeated 2^26 times is written by
+// all threads, coalesced. Windows with no keys are skipped (per-window counts
+// from a first pass). The output range of a bucket is the prefix of the bucket
 // totals (packed layout: the same slots the bucket occupies in `parted`).
 // Adds every key it writes to ctrl->total.
 constexpr int MS_THREADS = 1024;
-constexpr int MS_WIN_SHIFT = 15;  // 32768 counters = 128 KB
-constexpr int MS_WIN = 1 << MS_WIN_SHIFT;
-constexpr int MS_MAX_WIN = (1 << MAX_BUCKET_SHIFT) / MS_WIN;  // 32
+constexpr int MS_CNT_BYTES = 128 << 10;          // counter area
+constexpr int MS_STAGE_KEYS = 16384;             // keys staged in SMEM (64 KB)
+constexpr int MS_MAX_WIN = (1 << MAX_BUCKET_SHIFT) / (1 << 15);  // 32
+constexpr std::size_t ms_smem_bytes() { return MS_CNT_BYTES + MS_STAGE_KEYS * 4; }
 __global__ void __launch_bounds__(MS_THREADS, 1)
     bucket_multiset_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                            const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                            uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw);  // MS_WIN counters, then inclusive prefix
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw);  // counters, then inclusive prefix
+    uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(smem_raw);
+    uint32_t* s_keys = reinterpret_cast<uint32_t*>(smem_raw + MS_CNT_BYTES);
     __shared__ uint32_t s_wc[MS_MAX_WIN];                     // keys per window of the bucket
     __shared__ uint32_t s_warp[MS_THREADS / 32];
     __shared__ unsigned s_b;
@@ -1168,14 +1181,44 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
         const unsigned long long base = g_base[b];
         const uint32_t* src = parted + base;
         const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
-        const uint32_t nwin = (bm.width + MS_WIN - 1) >> MS_WIN_SHIFT;
+        const bool c16 = cnt < 65536u;           // block-uniform
+        const int wshift = c16 ? 16 : 15;
+        const uint32_t win = 1u << wshift;
+        const uint32_t nwin = (bm.width + win - 1) >> wshift;
+        const bool staged = cnt <= static_cast<uint32_t>(MS_STAGE_KEYS);
+        if (staged)
+            for (uint32_t i = threadIdx.x; i < cnt; i += MS_THREADS) s_keys[i] = src[i] - key_lo;
+        // visits every key of the bucket (offset from key_lo) in batches of
+        // four independent loads per thread
+        auto for_keys = [&](auto&& f) {
+            if (staged) {
+                for (uint32_t i = threadIdx.x; i < cnt; i += MS_THREADS) f(s_keys[i], true);
+                return;
+            }
+            uint32_t i0 = 0;
+            for (; i0 + 4 * MS_THREADS <= cnt; i0 += 4 * MS_THREADS) {
+                uint32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + i0 + u * MS_THREADS + threadIdx.x);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) f(v[u] - key_lo, true);
+            }
+            for (uint32_t i = i0 + threadIdx.x; i < cnt; i += MS_THREADS) f(src[i] - key_lo, true);
+        };
+        __syncthreads();
         // pass 0: keys per window (warp-aggregated: one SMEM atomic per window per warp step)
-        for (uint32_t i0 = 0; i0 < cnt; i0 += MS_THREADS) {
-            const uint32_t i = i0 + threadIdx.x;
-            const uint32_t w = i < cnt ? (src[i] - key_lo) >> MS_WIN_SHIFT : 0xffffffffu;
-            const unsigned peers = __match_any_sync(kFull, w);
-            if (w != 0xffffffffu && lane == static_cast<unsigned>(__ffs(peers) - 1))
-                atomicAdd(&s_wc[w], static_cast<uint32_t>(__popc(peers)));
+        if (nwin == 1) {
+            if (threadIdx.x == 0) s_wc[0] = cnt;
+        } else {
+            const uint32_t rounds = (cnt + MS_THREADS - 1) / MS_THREADS;  // every lane takes part in the match
+            for (uint32_t r = 0; r < rounds; ++r) {
+                const uint32_t i = r * MS_THREADS + threadIdx.x;
+                const uint32_t x = i < cnt ? (staged ? s_keys[i] : src[i] - key_lo) : 0u;
+                const uint32_t w = i < cnt ? x >> wshift : 0xffffffffu;
+                const unsigned peers = __match_any_sync(kFull, w);
+                if (w != 0xffffffffu && lane == static_cast<unsigned>(__ffs(peers) - 1))
+                    atomicAdd(&s_wc[w], static_cast<uint32_t>(__popc(peers)));
+            }
         }
         __syncthreads();
         unsigned long long o = base;
@@ -1183,53 +1226,60 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
             const uint32_t wk = s_wc[w];  // block-uniform
             if (wk == 0) continue;
             uint4* c4 = reinterpret_cast<uint4*>(s_cnt);
-            for (uint32_t i = threadIdx.x; i < MS_WIN / 4; i += MS_THREADS) c4[i] = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = threadIdx.x; i < MS_CNT_BYTES / 16; i += MS_THREADS) c4[i] = make_uint4(0, 0, 0, 0);
             __syncthreads();
-            const uint32_t wlo = w << MS_WIN_SHIFT;
-            for (uint32_t i = threadIdx.x; i < cnt; i += MS_THREADS) {
-                const uint32_t x = src[i] - key_lo - wlo;
-                if (x < static_cast<uint32_t>(MS_WIN)) atomicAdd(s_cnt + x, 1u);
+            const uint32_t wlo = w << wshift;
+            if (c16) {
+                for_keys([&](uint32_t x, bool) {
+                    x -= wlo;
+                    if (x < win) atomicAdd(s_cnt + (x >> 1), 1u << ((x & 1u) << 4));
+                });
+            } else {
+                for_keys([&](uint32_t x, bool) {
+                    x -= wlo;
+                    if (x < win) atomicAdd(s_cnt + x, 1u);
+                });
             }
             __syncthreads();
-            // inclusive prefix of the counters: thread t owns [32t, 32t + 32),
-            // read and written as 8 lane-rotated uint4 (bank-conflict free)
-            constexpr int kPer = MS_WIN / MS_THREADS;  // 32
-            uint32_t v[kPer];
-#pragma unroll
-            for (int q = 0; q < kPer / 4; ++q) {
-                const int qq = (q + static_cast<int>(lane)) & (kPer / 4 - 1);
-                const uint4 t = c4[threadIdx.x * (kPer / 4) + qq];
-                v[4 * qq] = t.x;
-                v[4 * qq + 1] = t.y;
-                v[4 * qq + 2] = t.z;
-                v[4 * qq + 3] = t.w;
+            // inclusive prefix of the counters: warp w owns words [1024w, 1024w + 1024),
+            // lane l the words 1024w + 32j + l (conflict-free); pass A: warp
+            // totals; pass B: row-by-row warp scans carrying the running sum
+            const uint32_t* wrow = s_cnt + warp * 1024 + lane;
+            uint32_t part = 0;
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t x = wrow[32 * j];
+                part += c16 ? (x & 0xffffu) + (x >> 16) : x;
             }
-#pragma unroll
-            for (int j = 1; j < kPer; ++j) v[j] += v[j - 1];
-            const uint32_t incl = warp_incl_scan(v[kPer - 1], lane);
-            if (lane == 31) s_warp[warp] = incl;
+            part = __reduce_add_sync(kFull, part);
+            if (lane == 0) s_warp[warp] = part;
             __syncthreads();
             if (warp == 0) {
                 const uint32_t x = s_warp[lane];
                 s_warp[lane] = warp_incl_scan(x, lane) - x;
             }
             __syncthreads();
-            const uint32_t add = s_warp[warp] + incl - v[kPer - 1];
-#pragma unroll
-            for (int q = 0; q < kPer / 4; ++q) {
-                const int qq = (q + static_cast<int>(lane)) & (kPer / 4 - 1);
-                c4[threadIdx.x * (kPer / 4) + qq] =
-                    make_uint4(v[4 * qq] + add, v[4 * qq + 1] + add, v[4 * qq + 2] + add, v[4 * qq + 3] + add);
+            uint32_t carry = s_warp[warp];
+            uint32_t* wrow_w = s_cnt + warp * 1024 + lane;
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t x = wrow_w[32 * j];
+                const uint32_t sum = c16 ? (x & 0xffffu) + (x >> 16) : x;
+                const uint32_t incl = warp_incl_scan(sum, lane);
+                const uint32_t excl = carry + incl - sum;
+                wrow_w[32 * j] = c16 ? ((excl + (x & 0xffffu)) | ((excl + sum) << 16)) : excl + sum;
+                carry += __shfl_sync(kFull, incl, 31);
             }
             __syncthreads();
             // expansion: slot i holds the smallest value whose inclusive prefix exceeds i
             const uint32_t kbase = key_lo + wlo;
             for (uint32_t i = threadIdx.x; i < wk; i += MS_THREADS) {
-                uint32_t lo = 0, len = MS_WIN;
+                uint32_t lo = 0, len = win;
 #pragma unroll 1
                 while (len > 1) {
                     const uint32_t half = len >> 1;
-                    if (s_cnt[lo + half - 1] <= i) lo += half;
+                    const uint32_t pv = c16 ? s_cnt16[lo + half - 1] : s_cnt[lo + half - 1];
+                    if (pv <= i) lo += half;
                     len -= half;
                 }
                 __stcs(out + o + i, (kbase + lo) ^ bm.xr);
@@ -1241,7 +1291,6 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
     }
     if (threadIdx.x == 0 && written) atomicAdd(&ctrl->total, written);
 }
-
 
 // KB4b (multi-GPU per-rank build): like KB4, but instead of extracting keys
 // each bucket's SMEM bitset is written to the global bitset, coalesced and
@@ -1286,8 +1335,26 @@ __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl
                                uint32_t xr) {
     uint32_t mx = 0;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
-        mx = max(mx, __ldcs(keys + i) ^ xr);
+    const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    // 16-byte loads over the aligned body, four in flight per thread
+    size_t head = ((16 - (reinterpret_cast<uintptr_t>(keys) & 15)) & 15) / 4;
+    if (head > n) head = n;
+    const uint4* v4 = reinterpret_cast<const uint4*>(keys + head);
+    const size_t nv = (n - head) / 4;
+    size_t i = tid;
+    for (; i + 3 * stride < nv; i += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(v4 + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mx = max(mx, max(max(v[u].x ^ xr, v[u].y ^ xr), max(v[u].z ^ xr, v[u].w ^ xr)));
+    }
+    for (; i < nv; i += stride) {
+        const uint4 v = __ldcs(v4 + i);
+        mx = max(mx, max(max(v.x ^ xr, v.y ^ xr), max(v.z ^ xr, v.w ^ xr)));
+    }
+    if (tid < head) mx = max(mx, keys[tid] ^ xr);
+    for (size_t j = head + 4 * nv + tid; j < n; j += stride) mx = max(mx, keys[j] ^ xr);
     mx = __reduce_max_sync(kFull, mx);
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(&ctrl->max_key, mx);
 }
@@ -1361,6 +1428,24 @@ BucketPlan plan_buckets(uint64_t key_range, int kb4_ctas) {
             }
         }
     }
+    return p;
+}
+
+BucketPlan plan_multiset(uint64_t key_range) {
+    // KB4m covers a bucket in 2^15-value windows, one pass over the bucket's
+    // keys per window: the narrowest buckets KB3 allows (<= MAX_BUCKETS) keep
+    // that at one or two passes below 2^28 values, and give KB4m more
+    // buckets than SMs
+    int log2m = 0;
+    while ((1ull << log2m) < key_range) ++log2m;
+    int shift = log2m - 12;
+    if (shift < MIN_BUCKET_SHIFT) shift = MIN_BUCKET_SHIFT;
+    if (shift > MAX_BUCKET_SHIFT) shift = MAX_BUCKET_SHIFT;
+    BucketPlan p;
+    p.shift = shift;
+    p.map = pow2_map(shift);
+    const uint64_t nb = (key_range + (1ull << shift) - 1) >> shift;
+    p.nb = static_cast<int>(nb < 1 ? 1 : nb);
     return p;
 }
 
@@ -1552,7 +1637,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     }
     if (multiset) {
         if (timer) timer->before(stream);
-        bucket_multiset_kernel<<<geo.multiset_blocks, MS_THREADS, MS_WIN * sizeof(uint32_t), stream>>>(
+        bucket_multiset_kernel<<<geo.multiset_blocks, MS_THREADS, ms_smem_bytes(), stream>>>(
             parted, tot, base, plan.map, plan.nb, out, ctrl);
         if (timer) timer->after("bucket_multiset", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
@@ -1604,7 +1689,7 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
                                1 << (MAX_BUCKET_SHIFT - 3));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_multiset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(MS_WIN * sizeof(uint32_t)));
+                               static_cast<int>(ms_smem_bytes()));
     if (err != cudaSuccess) return err;
     geo->multiset_blocks = sms;
     err = cudaFuncSetAttribute(bucket_sort_kernel<BUCKET_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -521,7 +521,8 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
     // signed sorts keep power-of-two bucket widths (the output XOR then
     // commutes with the in-bucket offsets)
     bws_gpu::BucketPlan plan =
-        bws_gpu::plan_buckets(key_range, xr ? 0 : ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
+        multiset ? bws_gpu::plan_multiset(key_range)
+                 : bws_gpu::plan_buckets(key_range, xr ? 0 : ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
     plan.map.lo = key_lo;
     plan.map.xr = xr;
     const size_t parted_cap = ctx.ensure_parted(count, plan);

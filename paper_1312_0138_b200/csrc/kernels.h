@@ -193,6 +193,9 @@ BucketPlan plan_range_split(std::uint64_t key_range, int parts);
 const std::uint32_t* bucket_totals(const void* scratch, const BucketPlan& plan, const LaunchGeometry& geo);
 // kb4_ctas: resident KB4 CTAs (0: power-of-two widths only).
 BucketPlan plan_buckets(std::uint64_t key_range, int kb4_ctas);
+// Bucket plan of the multiset (repeated keys) pass: the narrowest power-of-two
+// buckets with at most MAX_BUCKETS of them.
+BucketPlan plan_multiset(std::uint64_t key_range);
 // Bucket-buffer slots the slab layout needs for n keys (0: use the packed
 // histogram layout: the slab would exceed 4n slots or 2^32).
 std::uint64_t slab_slots(const BucketPlan& plan, std::size_t n);

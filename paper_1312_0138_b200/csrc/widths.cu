@@ -276,71 +276,128 @@ __global__ void __launch_bounds__(RX_THREADS)
     H[static_cast<size_t>(threadIdx.x) * gridDim.x + blockIdx.x] = s_h[threadIdx.x];
 }
 
-// One CTA: H[i] <- sum of H[< i] (i over 256 * P entries, digit-major).
-__global__ void __launch_bounds__(1024) rx_offsets_kernel(uint32_t* __restrict__ H, int total) {
+// One CTA: H[d][c] <- (keys of digits < d) + (keys of digit d in CTAs < c),
+// i.e. the exclusive prefix of H in digit-major order. Warp-per-row passes
+// (coalesced): row totals, their prefix, then row scans carrying it.
+__global__ void __launch_bounds__(1024) rx_offsets_kernel(uint32_t* __restrict__ H, int P) {
+    __shared__ uint32_t s_tot[256];
     __shared__ uint32_t s_w[32];
-    const int per = (total + 1023) / 1024;
-    const int b0 = threadIdx.x * per;
-    uint32_t local = 0;
-    for (int i = 0; i < per; ++i)
-        if (b0 + i < total) local += H[b0 + i];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t incl = warp_incl_scan(local, lane);
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t w = s_w[lane];
-        s_w[lane] = warp_incl_scan(w, lane) - w;
+    for (int d = warp; d < 256; d += 32) {
+        uint32_t sum = 0;
+        for (int c = lane; c < P; c += 32) sum += H[static_cast<size_t>(d) * P + c];
+        sum = __reduce_add_sync(kFull, sum);
+        if (lane == 0) s_tot[d] = sum;
     }
     __syncthreads();
-    uint32_t run = s_w[warp] + incl - local;
-    for (int i = 0; i < per; ++i) {
-        if (b0 + i < total) {
-            const uint32_t v = H[b0 + i];
-            H[b0 + i] = run;
-            run += v;
+    if (threadIdx.x < 256) {  // exclusive prefix of the 256 row totals
+        const uint32_t x = s_tot[threadIdx.x];
+        const uint32_t incl = warp_incl_scan(x, lane);
+        if (lane == 31) s_w[warp] = incl;
+        __syncwarp();
+        s_tot[threadIdx.x] = incl - x;  // warp-local for now
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        uint32_t run = 0;
+        for (int w = 0; w < static_cast<int>(threadIdx.x); ++w) run += s_w[w];
+        s_w[8 + threadIdx.x] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) s_tot[threadIdx.x] += s_w[8 + warp];
+    __syncthreads();
+    for (int d = warp; d < 256; d += 32) {
+        uint32_t carry = s_tot[d];
+        for (int c0 = 0; c0 < P; c0 += 32) {
+            const int c = c0 + static_cast<int>(lane);
+            const uint32_t x = c < P ? H[static_cast<size_t>(d) * P + c] : 0u;
+            const uint32_t incl = warp_incl_scan(x, lane);
+            if (c < P) H[static_cast<size_t>(d) * P + c] = carry + incl - x;
+            carry += __shfl_sync(kFull, incl, 31);
         }
     }
 }
 
+constexpr int RX_KPT = 16;                         // keys per thread per round
+constexpr int RX_ROUND = RX_KPT * RX_THREADS;      // 4096 keys per round
 __global__ void __launch_bounds__(RX_THREADS)
     rx_scatter_kernel(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out, size_t n,
                       unsigned long long xin, unsigned long long xout, int shift,
                       const uint32_t* __restrict__ H) {
-    __shared__ uint32_t s_base[256];                // next output slot per digit
-    __shared__ uint32_t s_w[2][RX_WARPS][256];      // per round: warp x digit counts -> slots
+    // Round r covers keys [r0, r0 + 4096) of the CTA's chunk; warp w takes
+    // [r0 + 512w, r0 + 512(w+1)), 32 consecutive keys per step j. Stable rank:
+    // per-warp running digit counts (match.any per step, warp-synchronous),
+    // their prefix over the warps, and the digit's run start in the round.
+    // The round is counting-sorted into SMEM and written run by run, so the
+    // stores of a digit's run are consecutive (coalesced) instead of scattered.
+    __shared__ uint32_t s_wcnt[RX_WARPS][256];             // warp x digit counts -> offsets
+    __shared__ unsigned long long s_stage[RX_ROUND];
+    __shared__ uint32_t s_base[256];                       // next output slot per digit
+    __shared__ uint32_t s_dstart[256];                     // digit run start in the round
+    __shared__ uint32_t s_w[RX_WARPS];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned t = threadIdx.x;                 // also: the digit this thread scans
+    const unsigned t = threadIdx.x;                        // also: the digit this thread scans
     s_base[t] = H[static_cast<size_t>(t) * gridDim.x + blockIdx.x];
-#pragma unroll
-    for (int w = 0; w < RX_WARPS; ++w) s_w[0][w][t] = s_w[1][w][t] = 0u;
-    __syncthreads();
     size_t c0, c1;
     rx_chunk(n, c0, c1);
     const unsigned lt = lanemask_lt();
-    int buf = 0;
-    for (size_t r0 = c0; r0 < c1; r0 += RX_THREADS, buf ^= 1) {
-        const size_t i = r0 + t;
-        const bool in_range = i < c1;
-        const unsigned long long k = in_range ? (__ldcs(in + i) ^ xin) : 0ull;
-        const uint32_t d = in_range ? static_cast<uint32_t>((k >> shift) & 255u) : 256u;
-        const unsigned peers = __match_any_sync(kFull, d);
-        const uint32_t rank = __popc(peers & lt);
-        if (in_range && rank == 0) s_w[buf][warp][d] = __popc(peers);
-        __syncthreads();
-        {  // digit t: exclusive prefix over the warps, offset by the digit's running base
-            uint32_t run = s_base[t];
+    for (size_t r0 = c0; r0 < c1; r0 += RX_ROUND) {
+        const uint32_t round_n = static_cast<uint32_t>(min(static_cast<size_t>(RX_ROUND), c1 - r0));
 #pragma unroll
-            for (int w = 0; w < RX_WARPS; ++w) {
-                const uint32_t c = s_w[buf][w][t];
-                s_w[buf][w][t] = run;
-                run += c;
-                s_w[buf ^ 1][w][t] = 0u;  // next round's table (its readers finished last round)
+        for (int q = 0; q < 256 / 32; ++q) s_wcnt[warp][q * 32 + lane] = 0u;
+        __syncwarp();
+        unsigned long long k[RX_KPT];
+        uint32_t dr[RX_KPT];  // digit << 16 | rank among the warp's keys of that digit (256: none)
+#pragma unroll
+        for (int j = 0; j < RX_KPT; ++j) {
+            const uint32_t li = warp * (RX_KPT * 32) + j * 32 + lane;
+            const bool ok = li < round_n;
+            k[j] = ok ? (__ldcs(in + r0 + li) ^ xin) : 0ull;
+            const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 255u) : 256u;
+            const unsigned peers = __match_any_sync(kFull, d);
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (ok && static_cast<int>(lane) == leader) {
+                old = s_wcnt[warp][d];
+                s_wcnt[warp][d] = old + __popc(peers);
             }
-            s_base[t] = run;
+            old = __shfl_sync(kFull, old, leader);
+            dr[j] = (d << 16) | (old + __popc(peers & lt));
+            __syncwarp();
         }
         __syncthreads();
-        if (in_range) __stcs(out + s_w[buf][warp][d] + rank, k ^ xout);
+        uint32_t total;
+        {  // digit t: exclusive prefix over the warps, then over the digits
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < RX_WARPS; ++w) {
+                const uint32_t c = s_wcnt[w][t];
+                s_wcnt[w][t] = run;
+                run += c;
+            }
+            total = run;
+            const uint32_t incl = warp_incl_scan(total, lane);
+            if (lane == 31) s_w[warp] = incl;
+            __syncthreads();
+            uint32_t wbase = 0;
+#pragma unroll
+            for (int w = 0; w < RX_WARPS; ++w) wbase += w < static_cast<int>(warp) ? s_w[w] : 0u;
+            s_dstart[t] = wbase + incl - total;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < RX_KPT; ++j) {
+            const uint32_t d = dr[j] >> 16;
+            if (d < 256u) s_stage[s_dstart[d] + s_wcnt[warp][d] + (dr[j] & 0xffffu)] = k[j];
+        }
+        __syncthreads();
+        for (uint32_t i = t; i < round_n; i += RX_THREADS) {
+            const unsigned long long key = s_stage[i];
+            const uint32_t d = static_cast<uint32_t>((key >> shift) & 255u);
+            __stcs(out + s_base[d] + (i - s_dstart[d]), key ^ xout);
+        }
+        __syncthreads();
+        s_base[t] += total;
     }
 }
 
@@ -413,14 +470,14 @@ cudaError_t launch_radix64_hist(const std::uint64_t* keys, std::size_t n, int is
 cudaError_t launch_radix64_pass(const std::uint64_t* in, std::uint64_t* out, std::size_t n, int digit,
                                 std::uint64_t xin, std::uint64_t xout, void* scratch, const LaunchGeometry& geo,
                                 cudaStream_t stream) {
-    const int P = geo.multiset_blocks * 4;
+    const int P = geo.multiset_blocks * 3;  // rx_scatter: 3 resident CTAs per SM (78 registers, 43 KB)
     uint32_t* H = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(scratch) +
                                               8 * 256 * sizeof(unsigned long long));
     const auto* i64 = reinterpret_cast<const unsigned long long*>(in);
     rx_hist_kernel<<<P, RX_THREADS, 0, stream>>>(i64, n, xin, 8 * digit, H);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
-    rx_offsets_kernel<<<1, 1024, 0, stream>>>(H, 256 * P);
+    rx_offsets_kernel<<<1, 1024, 0, stream>>>(H, P);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     rx_scatter_kernel<<<P, RX_THREADS, 0, stream>>>(i64, reinterpret_cast<unsigned long long*>(out), n, xin, xout,
                                                     8 * digit, H);
