@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(1024) rx_offsets_kernel(uint32_t* __restrict__
 
 constexpr int RX_KPT = 16;                         // keys per thread per round
 constexpr int RX_ROUND = RX_KPT * RX_THREADS;      // 4096 keys per round
-__global__ void __launch_bounds__(RX_THREADS)
+__global__ void __launch_bounds__(RX_THREADS, 4)
     rx_scatter_kernel(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out, size_t n,
                       unsigned long long xin, unsigned long long xout, int shift,
                       const uint32_t* __restrict__ H) {
@@ -348,11 +348,14 @@ __global__ void __launch_bounds__(RX_THREADS)
         __syncwarp();
         unsigned long long k[RX_KPT];
         uint32_t dr[RX_KPT];  // digit << 16 | rank among the warp's keys of that digit (256: none)
+        const uint32_t wfirst = warp * (RX_KPT * 32) + lane;
+#pragma unroll
+        for (int j = 0; j < RX_KPT; ++j)  // every load in flight before the first rank
+            k[j] = wfirst + j * 32 < round_n ? __ldcs(in + r0 + wfirst + j * 32) : 0ull;
 #pragma unroll
         for (int j = 0; j < RX_KPT; ++j) {
-            const uint32_t li = warp * (RX_KPT * 32) + j * 32 + lane;
-            const bool ok = li < round_n;
-            k[j] = ok ? (__ldcs(in + r0 + li) ^ xin) : 0ull;
+            const bool ok = wfirst + j * 32 < round_n;
+            k[j] ^= xin;
             const uint32_t d = ok ? static_cast<uint32_t>((k[j] >> shift) & 255u) : 256u;
             const unsigned peers = __match_any_sync(kFull, d);
             const int leader = __ffs(peers) - 1;
@@ -470,7 +473,7 @@ cudaError_t launch_radix64_hist(const std::uint64_t* keys, std::size_t n, int is
 cudaError_t launch_radix64_pass(const std::uint64_t* in, std::uint64_t* out, std::size_t n, int digit,
                                 std::uint64_t xin, std::uint64_t xout, void* scratch, const LaunchGeometry& geo,
                                 cudaStream_t stream) {
-    const int P = geo.multiset_blocks * 3;  // rx_scatter: 3 resident CTAs per SM (78 registers, 43 KB)
+    const int P = geo.multiset_blocks * 4;  // rx_scatter: 4 resident CTAs per SM (64 registers, 43 KB)
     uint32_t* H = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(scratch) +
                                               8 * 256 * sizeof(unsigned long long));
     const auto* i64 = reinterpret_cast<const unsigned long long*>(in);
