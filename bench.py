@@ -56,7 +56,9 @@ def parse_args():
     ap.add_argument("--a2a", action="store_true",
                     help="multi-GPU key all-to-all variant (range split + NCCL all-to-all + range sort)")
     ap.add_argument("--p2p", action="store_true",
-                    help="multi-GPU peer-to-peer variant (CUDA IPC OR-gather instead of the NCCL reduce-scatter)")
+                    help="multi-GPU peer-to-peer variant (the exchange fused into the scan over CUDA IPC)")
+    ap.add_argument("--push", action="store_true",
+                    help="multi-GPU push variant (the exchange fused into the build: bulk ORs into peers' slices)")
     return ap.parse_args()
 
 
@@ -98,8 +100,10 @@ def kernel_alg_bytes(kernel: str, n: int, key_range: int, world: int = 1) -> int
         "bucket_partition": 8 * n,            # read keys, write bucketed keys
         "bucket_sort": 8 * n,                 # read bucketed keys, write sorted keys
         "bucket_bitset": 4 * n + words_bytes,  # read bucketed keys, write the bitset (multi-GPU)
+        "bucket_push": 4 * n + words_bytes,    # read bucketed keys, OR the bitset into the slices
         "bitset_scatter": 4 * n + words_bytes,          # read keys, write bitset
         "bitset_scan": words_bytes // world + 4 * n,    # read (slice of) bitset, write keys
+        "bitset_scan_sources": words_bytes + 4 * n,     # read the slice of every rank's bitset, write keys
     }.get(kernel, 0)
 
 
@@ -261,7 +265,7 @@ def run_ours(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    use_dist = world > 1 or args.dist or args.a2a or args.p2p
+    use_dist = world > 1 or args.dist or args.a2a or args.p2p or args.push
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
@@ -277,8 +281,10 @@ def run_ours(args, cfg):
         from paper_1312_0138_b200.dist import distributed_sort as dist_rs
         from paper_1312_0138_b200.dist import distributed_sort_a2a as dist_a2a
         from paper_1312_0138_b200.dist import distributed_sort_p2p as dist_p2p
+        from paper_1312_0138_b200.dist import distributed_sort_push as dist_push
 
-        distributed_sort = dist_a2a if args.a2a else (dist_p2p if args.p2p else dist_rs)
+        distributed_sort = (dist_a2a if args.a2a else dist_p2p if args.p2p else
+                            dist_push if args.push else dist_rs)
 
         lo, hi = shard_bounds(n_total, rank, world)
         shard_h = keys_h[lo:hi]
@@ -461,8 +467,9 @@ def run_ours(args, cfg):
                    "path": args.path,
                    "parallelism": (f"key shards x{world} + " + ("NCCL all-to-all of range-split keys"
                                                                   if args.a2a else
-                                                                  "CUDA IPC OR-gather" if args.p2p else
-                                                                  "NCCL reduce-scatter"))
+                                                                  "scan fused with CUDA IPC peer reads" if args.p2p else
+                                                                  "build fused with bulk-OR pushes to peers' slices"
+                                                                  if args.push else "NCCL reduce-scatter"))
                    if use_dist else "single GPU"},
         "step_ms": {"median": round(statistics.median(step_ms), 4), "best": round(min(step_ms), 4),
                     "worst": round(max(step_ms), 4)},

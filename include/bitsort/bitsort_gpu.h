@@ -96,6 +96,19 @@ BITSORT_API bws_status bws_gpu_bitset_scan_sources(const uint32_t* const* srcs, 
                                                    uint64_t n_words, uint32_t key_base,
                                                    uint32_t* out, uint64_t out_capacity,
                                                    uint64_t* d_total, void* stream);
+/* The exchange fused into the build (push variant): builds the bitset of
+ * `count` keys in [0, key_range) bucket by bucket in shared memory and ORs
+ * each finished bucket straight into the owner's slice with bulk
+ * OR-reductions: slices[r] (device pointer, local or a peer's opened through
+ * CUDA IPC, 16-byte aligned, zeroed by its owner beforehand) holds words
+ * [r * slice_words, (r + 1) * slice_words) of the global bitset; slice_words
+ * a multiple of 4 and nslices * slice_words >= ceil(key_range / 32). Every
+ * rank pushes into every slice; after a cross-rank barrier each owner scans
+ * its slice with bws_gpu_bitset_scan. No full bitset is materialised on any
+ * rank and no separate collective runs. */
+BITSORT_API bws_status bws_gpu_bitset_push(const uint32_t* keys, size_t count, uint64_t key_range,
+                                           uint32_t* const* slices, int nslices, uint64_t slice_words,
+                                           void* stream);
 /* handle_out: BWS_GPU_IPC_HANDLE_BYTES bytes naming dev_ptr's allocation;
  * *offset_out: dev_ptr's byte offset in it (add it to the pointer
  * bws_gpu_ipc_open returns in the peer process). */

@@ -91,6 +91,7 @@ def _load() -> ctypes.CDLL:
         "bws_gpu_range_split": (i32, [vp, sz, u64, i32, vp, vp, ctypes.POINTER(u64), vp]),
         "bws_gpu_bitset_or_gather": (i32, [ctypes.POINTER(vp), i32, u64, vp, vp]),
         "bws_gpu_bitset_scan_sources": (i32, [ctypes.POINTER(vp), i32, u64, u32, vp, u64, vp, vp]),
+        "bws_gpu_bitset_push": (i32, [vp, sz, u64, ctypes.POINTER(vp), i32, u64, vp]),
         "bws_gpu_ipc_get_handle": (i32, [vp, vp, ctypes.POINTER(u64)]),
         "bws_gpu_ipc_open": (i32, [vp, ctypes.POINTER(vp)]),
         "bws_gpu_ipc_close": (i32, [vp]),
@@ -117,7 +118,7 @@ EXPORTED = (
     "bws_version", "bws_last_error", "bws_algorithm_name", "bws_algorithm_from_name",
     "bws_sort", "bws_sort_u32_range", "bws_gpu_sort_device_async", "bws_gpu_sort_check",
     "bws_gpu_sort_range_device_async", "bws_gpu_range_split",
-    "bws_gpu_bitset_or_gather", "bws_gpu_bitset_scan_sources", "bws_gpu_ipc_get_handle", "bws_gpu_ipc_open", "bws_gpu_ipc_close",
+    "bws_gpu_bitset_or_gather", "bws_gpu_bitset_scan_sources", "bws_gpu_bitset_push", "bws_gpu_ipc_get_handle", "bws_gpu_ipc_open", "bws_gpu_ipc_close",
     "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode", "bws_gpu_set_path",
     "bws_gpu_launch_count",
     "bws_gpu_set_kernel_timing", "bws_gpu_kernel_timings",
@@ -231,6 +232,12 @@ def bitset_scan_sources(src_ptrs, n_words: int, key_base: int, out_ptr: int, out
     arr = (ctypes.c_void_p * len(src_ptrs))(*src_ptrs)
     _check(lib.bws_gpu_bitset_scan_sources(arr, len(src_ptrs), n_words, key_base, out_ptr,
                                            out_capacity, d_total_ptr, stream or None))
+
+
+def bitset_push(keys_ptr: int, count: int, key_range: int, slice_ptrs, slice_words: int, stream: int = 0) -> None:
+    """OR the bitset of the keys into the owners' slices (bws_gpu_bitset_push)."""
+    arr = (ctypes.c_void_p * len(slice_ptrs))(*slice_ptrs)
+    _check(lib.bws_gpu_bitset_push(keys_ptr, count, key_range, arr, len(slice_ptrs), slice_words, stream or None))
 
 
 def ipc_get_handle(dev_ptr: int) -> tuple[bytes, int]:

@@ -1330,6 +1330,70 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
     }
 }
 
+
+// KB4p (multi-GPU push build, the exchange fused into the build): like KB4b,
+// but each bucket's finished SMEM bitset leaves with one bulk OR-reduction
+// per destination slice (cp.reduce.async.bulk ... .or.b32) straight into the
+// owner rank's slice buffer — peer memory over NVLink/NVSwitch through CUDA
+// IPC, or local memory for the rank's own slice. The L2 of the owner applies
+// the OR, so pushes from all ranks into one slice need no other
+// synchronisation; distinct keys set disjoint bits, so OR is exact, and
+// repeats only lose bits (the popcount total reports them). Slice r covers
+// words [r * slice_words, (r + 1) * slice_words) (slice_words a multiple of
+// 4: bulk operations move 16-byte units).
+__global__ void __launch_bounds__(BUCKET_THREADS, 1)
+    bucket_push_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
+                       const unsigned long long* __restrict__ g_base, BucketMap bm, int nb, uint32_t src_cap,
+                       OrSources slices, unsigned long long slice_words, unsigned long long n_words,
+                       uint32_t last_mask, Ctrl* __restrict__ ctrl) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t W = bm.width >> 5;
+    uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
+    __shared__ unsigned s_b;
+    uint4* s4 = reinterpret_cast<uint4*>(s_bits);
+    const unsigned long long total_words = slice_words * static_cast<unsigned long long>(slices.n);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            // the previous bucket's bulk reductions must have read s_bits
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            s_b = atomicAdd(&ctrl->ticket, 1u);
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < W / 4; i += BUCKET_THREADS) s4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        const unsigned b = s_b;
+        if (b >= static_cast<unsigned>(nb)) break;
+        scatter_bucket_keys<false>(parted + (src_cap ? static_cast<size_t>(b) * src_cap : g_base[b]), tot[b],
+                                   bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, nullptr);
+        __syncthreads();
+        const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
+        if (threadIdx.x == 0 && n_words - 1 >= w0 && n_words - 1 < w0 + W) s_bits[n_words - 1 - w0] &= last_mask;
+        fence_proxy_async_smem();  // generic-proxy SMEM writes -> visible to the bulk reductions
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // one bulk OR per slice the bucket's words [w0, w0 + W) overlap
+            const unsigned long long end = min(w0 + W, total_words);
+            unsigned long long w = w0;
+#pragma unroll 1
+            while (w < end) {
+                const int r = static_cast<int>(w / slice_words);
+                const unsigned long long seg_end = min(end, static_cast<unsigned long long>(r + 1) * slice_words);
+                uint32_t* dst = const_cast<uint32_t*>(slices.p[r]) + (w - static_cast<unsigned long long>(r) * slice_words);
+                const uint32_t bytes = static_cast<uint32_t>(seg_end - w) * 4u;
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b32 [%0], [%1], %2;" ::"l"(dst),
+                             "r"(smem_u32(s_bits + (w - w0))), "r"(bytes)
+                             : "memory");
+                w = seg_end;
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // reductions performed
+        __threadfence_system();
+    }
+}
+
 // K0: max key (only when no key-range hint is given).
 __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl* __restrict__ ctrl,
                                uint32_t xr) {
@@ -1523,7 +1587,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                                uint32_t* parted, void* scratch, Ctrl* ctrl, const BucketPlan& plan,
                                const LaunchGeometry& geo, cudaStream_t stream, int* launches,
                                KernelTimer* timer, uint32_t* bits_out, uint64_t n_words,
-                               uint64_t parted_cap, bool multiset) {
+                               uint64_t parted_cap, bool multiset, const OrSources* push,
+                               uint64_t push_slice_words) {
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     // scratch: slab fill counters (fixed place: they persist across sorts), then H, tot, base
@@ -1556,7 +1621,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         return e && std::string(e) == "0";
     }();
     uint32_t* kb4_order =
-        (!use_slab && !plan.partition_only && !multiset && !bits_out && !order_off && plan.nb > 1) ? order_buf
+        (!use_slab && !plan.partition_only && !multiset && !bits_out && !push && !order_off && plan.nb > 1) ? order_buf
                                                                                                     : nullptr;
     SlabArgs sa;
     int nlaunch = 0;
@@ -1624,6 +1689,17 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         return cudaSuccess;
     }
     const uint32_t src_cap = use_slab ? sa.cap : 0u;
+    if (push) {  // multi-GPU push build: bucket bitsets ORed into the owners' slices
+        if (timer) timer->before(stream);
+        bucket_push_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, std::size_t(1) << (plan.shift - 3),
+                             stream>>>(parted, tot, base, plan.map, plan.nb, src_cap, *push, push_slice_words,
+                                       n_words, (key_range & 31) ? (1u << (key_range & 31)) - 1u : 0xffffffffu,
+                                       ctrl);
+        if (timer) timer->after("bucket_push", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (launches) *launches = nlaunch + 1;
+        return cudaSuccess;
+    }
     if (bits_out) {  // multi-GPU per-rank build: write the bitset instead of sorted keys
         if (timer) timer->before(stream);
         bucket_bitset_kernel<<<geo.bucket_blocks[plan.shift], BUCKET_THREADS,
@@ -1658,6 +1734,14 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     return cudaSuccess;
 }
 
+cudaError_t launch_bucket_push(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* parted, void* scratch,
+                               Ctrl* ctrl, const BucketPlan& plan, const LaunchGeometry& geo, cudaStream_t stream,
+                               int* launches, const OrSources& slices, uint64_t slice_words, uint64_t parted_cap,
+                               KernelTimer* timer) {
+    return launch_bucket_sort(keys, n, key_range, nullptr, parted, scratch, ctrl, plan, geo, stream, launches, timer,
+                              nullptr, (key_range + 31) / 32, parted_cap, false, &slices, slice_words);
+}
+
 cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     int sms = 0;
     cudaError_t err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1686,6 +1770,9 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
                                static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_bitset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               1 << (MAX_BUCKET_SHIFT - 3));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_push_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                1 << (MAX_BUCKET_SHIFT - 3));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_multiset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

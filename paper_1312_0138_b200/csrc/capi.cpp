@@ -1143,6 +1143,45 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
     });
 }
 
+bws_status bws_gpu_bitset_push(const uint32_t* keys, size_t count, uint64_t key_range, uint32_t* const* slices,
+                               int nslices, uint64_t slice_words, void* stream) {
+    return wrap([&] {
+        if (nslices < 1 || nslices > bws_gpu::MAX_OR_SOURCES) throw std::out_of_range("nslices must be in [1, 8]");
+        check_range(key_range);
+        if (key_range == 0) throw std::out_of_range("bitset_push needs a key range");
+        if (slice_words % 4 != 0) throw std::out_of_range("slice_words must be a multiple of 4");
+        if (slice_words * static_cast<uint64_t>(nslices) < (key_range + 31) / 32)
+            throw std::out_of_range("the slices do not cover the key range");
+        if (count > 0 && keys == nullptr) throw data_error("null device pointer");
+        if (count >= (size_t(1) << 32)) throw std::out_of_range("bitset_push takes fewer than 2^32 keys");
+        bws_gpu::OrSources os{};
+        os.n = nslices;
+        for (int i = 0; i < nslices; ++i) {
+            if (slices == nullptr || slices[i] == nullptr) throw data_error("null slice pointer");
+            if (!bws_gpu::scan2_supported(slices[i])) throw data_error("slices must be 16-byte aligned");
+            os.p[i] = slices[i];
+        }
+        if (count == 0) return;
+        const int dev = current_device();
+        DeviceCtx& ctx = context_for(dev);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        ctx.init(dev);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
+        const bws_gpu::BucketPlan plan =
+            bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
+        const size_t parted_cap = ctx.ensure_parted(count, plan);
+        int launches = 0;
+        cuda_check(bws_gpu::launch_bucket_push(keys, count, key_range, ctx.parted, ctx.bucket_scratch, ctx.ctrl(),
+                                               plan, ctx.geo, s, &launches, os, slice_words, parted_cap,
+                                               active_timer()),
+                   "bitset push launch");
+        g_launches.fetch_add(static_cast<uint64_t>(launches));
+        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+    });
+}
+
 bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t key_base,
                                uint32_t* out, uint64_t out_capacity, uint64_t* d_total,
                                void* stream) {

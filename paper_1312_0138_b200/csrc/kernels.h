@@ -215,7 +215,8 @@ cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::ui
                                const BucketPlan& plan, const LaunchGeometry& geo,
                                cudaStream_t stream, int* launches, KernelTimer* timer = nullptr,
                                std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0,
-                               std::uint64_t parted_cap = 0, bool multiset = false);
+                               std::uint64_t parted_cap = 0, bool multiset = false,
+                               const struct OrSources* push = nullptr, std::uint64_t push_slice_words = 0);
 // Multi-GPU OR-gather (the P2P replacement of the reduce-scatter): dst[i] =
 // OR over s of srcs.p[s][i] for i < n_words; srcs may point into peer GPUs'
 // memory (CUDA IPC over NVLink/NVSwitch).
@@ -226,6 +227,16 @@ struct OrSources {
 };
 cudaError_t launch_or_gather(const OrSources& srcs, std::uint32_t* dst, std::uint64_t n_words,
                              const LaunchGeometry& geo, cudaStream_t stream);
+// Multi-GPU push build (the exchange fused into the build): KB1-KB3, then
+// KB4p ORs every bucket's SMEM bitset straight into the owner rank's slice
+// (slices.p[r] covers words [r * slice_words, (r + 1) * slice_words), 16-byte
+// aligned, zeroed by the owner beforehand; slice_words a multiple of 4) with
+// bulk OR-reductions; peers' slices are CUDA IPC pointers over NVLink.
+cudaError_t launch_bucket_push(const std::uint32_t* keys, std::size_t n, std::uint64_t key_range,
+                               std::uint32_t* parted, void* scratch, Ctrl* ctrl, const BucketPlan& plan,
+                               const LaunchGeometry& geo, cudaStream_t stream, int* launches,
+                               const OrSources& slices, std::uint64_t slice_words, std::uint64_t parted_cap,
+                               KernelTimer* timer = nullptr);
 // K3 v2 over the OR of srcs (the fused P2P exchange + scan): same contract as
 // launch_scan2 (lookback variant, no clearing) on the virtual bitset
 // OR_s srcs.p[s][0, n_words); every source 16-byte aligned (scan2_supported).

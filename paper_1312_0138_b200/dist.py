@@ -19,6 +19,14 @@ out of their memory over NVLink (bws_gpu_bitset_scan_sources): no gathered
 slice is written to HBM or read back. OR is exact on distinct keys and only
 loses bits on duplicates.
 
+Push variant (``distributed_sort_push``, NVLink/NVSwitch node): steps 1 and 2
+become ONE kernel — every rank allocates its (zeroed) slice and exports it
+through CUDA IPC; each rank then builds its shard's bitset bucket by bucket in
+shared memory and ORs every finished bucket straight into the owner ranks'
+slices with bulk OR-reductions over NVLink (bws_gpu_bitset_push). No rank
+materialises a full bitset and no separate collective runs; after a barrier
+each owner scans its slice.
+
 Key all-to-all variant (``distributed_sort_a2a``): rank r
 splits its shard by destination key range (range split, C ABI), the ranks
 exchange the groups with one all-to-all (4n/G bytes per rank instead of the
@@ -70,6 +78,19 @@ class RankOps(Protocol):
         """bitset_scan of or_gather(sources, word_lo, n_words) in one step
         (the CUDA build fuses the peer reads into the scan kernel)."""
 
+    def alloc_slice(self, n_words: int) -> torch.Tensor:
+        """A zeroed slice this rank owns (push variant)."""
+
+    def export_slice(self, slice_: torch.Tensor):
+        """A picklable handle through which other ranks write ``slice_``."""
+
+    def import_slice(self, rank: int, handle):
+        """Writable target for bitset_push behind another rank's handle."""
+
+    def bitset_push(self, keys: torch.Tensor, key_range: int, targets, slice_words: int) -> None:
+        """OR the bitset of ``keys`` into the slices: targets[r] holds words
+        [r * slice_words, (r + 1) * slice_words)."""
+
 
 @dataclass
 class SliceResult:
@@ -79,6 +100,14 @@ class SliceResult:
     total: int              # keys over all ranks
     key_lo: int             # this rank's key range [key_lo, key_hi)
     key_hi: int
+
+
+def push_slice_words(key_range: int, world: int) -> int:
+    """Words per rank of the push variant: whole 16-byte units (bulk
+    reductions move 16 bytes at a time)."""
+    words = (key_range + 31) // 32
+    per = (words + world - 1) // world
+    return (per + 3) // 4 * 4
 
 
 def slice_words(key_range: int, world: int) -> tuple[int, int]:
@@ -188,6 +217,19 @@ class CudaRankOps:
         self._capi.bitset_scan_sources(ptrs, n_words, key_base, self._out.data_ptr(), capacity,
                                        self._total.data_ptr(), self._stream())
         return self._out, self._total
+
+    def alloc_slice(self, n_words: int) -> torch.Tensor:
+        return torch.zeros(max(n_words, 4), dtype=torch.int32, device=self.device)[:n_words]
+
+    def export_slice(self, slice_: torch.Tensor):
+        return self.export_bitset(slice_)
+
+    def import_slice(self, rank: int, handle):
+        return self.import_peer(rank, handle)
+
+    def bitset_push(self, keys: torch.Tensor, key_range: int, targets, slice_words: int) -> None:
+        ptrs = [t.data_ptr() if isinstance(t, torch.Tensor) else int(t) for t in targets]
+        self._capi.bitset_push(keys.data_ptr(), keys.numel(), key_range, ptrs, slice_words, self._stream())
 
     def bitset_scan(self, bits: torch.Tensor, key_base: int, capacity: int):
         if self._out is None or self._out.numel() < capacity:
@@ -326,6 +368,54 @@ def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[i
         dist.all_reduce(fence, group=group)
     out, count_t = ops.or_scan(sources, rank * per, per, key_lo, capacity)
     # the counts' all-gather doubles as the "peers are done reading" barrier
+    counts = [torch.empty_like(count_t) for _ in range(world)]
+    dist.all_gather(counts, count_t, group=group)
+    counts_h = [int(c.item()) for c in counts]
+    total = sum(counts_h)
+    if total != n_total:
+        raise _data_error(f"keys are not distinct or out of range: {n_total} keys, {total} distinct")
+    count = counts_h[rank]
+    return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
+                       key_lo=key_lo, key_hi=key_hi)
+
+
+def distributed_sort_push(keys: torch.Tensor, key_range: int, n_total: Optional[int] = None,
+                          ops: Optional[RankOps] = None, group=None) -> SliceResult:
+    """:func:`distributed_sort` with the bitset build and the reduce-scatter
+    fused: every rank ORs its bucket bitsets straight into the owners' slices
+    (bws_gpu_bitset_push over CUDA IPC); each owner then scans its slice.
+    Slices hold :func:`push_slice_words` words (a multiple of 4)."""
+    if not 0 < key_range <= 1 << 32:
+        raise ValueError("key_range must be in [1, 2^32]")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ops = ops or CudaRankOps(keys.device)
+    dev = keys.device
+    per = push_slice_words(key_range, world)
+    if n_total is None:
+        t = torch.tensor([keys.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, group=group)
+        n_total = int(t.item())
+
+    own = ops.alloc_slice(per)
+    fence = torch.zeros(1, dtype=torch.int32, device=dev)
+    if world == 1:
+        targets = [own]
+    else:
+        handles = [None] * world
+        dist.all_gather_object(handles, ops.export_slice(own), group=group)
+        targets = [own if r == rank else ops.import_slice(r, h) for r, h in enumerate(handles)]
+        # every slice is zeroed (stream-ordered before this collective) before anyone pushes
+        dist.all_reduce(fence, group=group)
+    if keys.numel():
+        ops.bitset_push(keys, key_range, targets, per)
+    if world > 1:
+        dist.all_reduce(fence, group=group)  # every rank's pushes have landed
+
+    key_lo = rank * per * 32
+    key_hi = min((rank + 1) * per * 32, key_range)
+    capacity = max(0, min(n_total, key_hi - key_lo))
+    out, count_t = ops.bitset_scan(own, key_lo, capacity)
     counts = [torch.empty_like(count_t) for _ in range(world)]
     dist.all_gather(counts, count_t, group=group)
     counts_h = [int(c.item()) for c in counts]

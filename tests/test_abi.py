@@ -143,6 +143,8 @@ def test_extension_argument_checks():
     assert capi.lib.bws_gpu_bitset_or_gather(None, 9, 0, None, None) == capi.Status.ERROR_RANGE
     assert capi.lib.bws_gpu_bitset_scan_sources(None, 0, 0, 0, None, 0, None, None) == capi.Status.ERROR_RANGE
     assert capi.lib.bws_gpu_bitset_scan_sources(None, 9, 0, 0, None, 0, None, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_bitset_push(None, 0, 1 << 10, None, 0, 32, None) == capi.Status.ERROR_RANGE
+    assert capi.lib.bws_gpu_bitset_push(None, 0, 1 << 10, None, 1, 30, None) == capi.Status.ERROR_RANGE
     assert capi.lib.bws_gpu_ipc_get_handle(None, None, None) == capi.Status.ERROR_DATA
 
 

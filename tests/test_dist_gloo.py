@@ -18,7 +18,8 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_1312_0138_b200.dist import (distributed_sort, distributed_sort_a2a, distributed_sort_p2p,
-                                       part_width, shard_bounds, slice_words)
+                                       distributed_sort_push, part_width, push_slice_words, shard_bounds,
+                                       slice_words)
 
 
 class OracleRankOps:
@@ -64,6 +65,38 @@ class OracleRankOps:
             acc |= src.numpy().view(np.uint32)[word_lo:word_lo + n_words]
         return torch.from_numpy(acc.view(np.int32))
 
+    # push variant: slices are shared files every rank maps writable; the OR
+    # into a slice holds the file's lock (the GPU's bulk OR is atomic in L2)
+    def alloc_slice(self, n_words):
+        import tempfile
+
+        fd, path = tempfile.mkstemp(prefix="bws_push_", suffix=".u32")
+        os.close(fd)
+        np.zeros(max(n_words, 1), dtype=np.uint32).tofile(path)
+        self.__dict__.setdefault("_slice_path", {})[n_words] = path
+        return torch.from_numpy(np.memmap(path, dtype=np.uint32, mode="r+", shape=(n_words,)).view(np.int32))
+
+    def export_slice(self, slice_):
+        return self._slice_path[slice_.numel()]
+
+    def import_slice(self, rank, handle):
+        return handle
+
+    def bitset_push(self, keys, key_range, targets, slice_words):
+        import fcntl
+
+        bits, _ = oracle.bitset_build(keys.numpy().view(np.uint32), key_range)
+        for r, tgt in enumerate(targets):
+            path = tgt if isinstance(tgt, str) else self._slice_path[tgt.numel()]
+            part = bits[r * slice_words:(r + 1) * slice_words]
+            with open(path, "r+b") as fh:
+                fcntl.flock(fh, fcntl.LOCK_EX)
+                m = np.memmap(path, dtype=np.uint32, mode="r+", shape=(slice_words,))
+                m[: part.size] |= part
+                m.flush()
+                del m
+                fcntl.flock(fh, fcntl.LOCK_UN)
+
     def or_scan(self, sources, word_lo, n_words, key_base, capacity):
         return self.bitset_scan(self.or_gather(sources, word_lo, n_words), key_base, capacity)
 
@@ -91,7 +124,8 @@ def _worker(rank, world, port, keys, key_range, q, variant="rs"):
         lo, hi = shard_bounds(keys.size, rank, world)
         shard = torch.from_numpy(keys[lo:hi].view(np.int32).copy())
         try:
-            sorter = {"a2a": distributed_sort_a2a, "p2p": distributed_sort_p2p}.get(variant, distributed_sort)
+            sorter = {"a2a": distributed_sort_a2a, "p2p": distributed_sort_p2p,
+                      "push": distributed_sort_push}.get(variant, distributed_sort)
             r = sorter(shard, key_range, ops=OracleRankOps())
             q.put((rank, "ok", r.keys.numpy().view(np.uint32).copy(), r.offset, r.total, r.key_lo, r.key_hi))
         except Exception as e:  # noqa: BLE001
@@ -220,5 +254,30 @@ def test_distributed_p2p_duplicates_rejected():
     keys = np.arange(0, 2000, 2, dtype=np.uint32)
     keys[-1] = keys[0]
     res = run_ranks(keys, 1 << 12, 2, "p2p")
+    for rank, status, code, msg, *_ in res:
+        assert status == "BitsortError" and int(code) == 2
+
+
+@pytest.mark.parametrize("world,key_range,n", [(2, 1 << 20, 100_000), (3, 1000, 1000), (3, (1 << 16) + 5, 3000)])
+def test_distributed_sort_push_gloo(world, key_range, n):
+    """Push variant: slice handles (all_gather_object), the zeroed-slices
+    fence, every rank ORing its bitset into every owner's slice, the
+    pushes-landed fence, the owners' scans and the offsets."""
+    keys = np.random.default_rng(world * 43 + n).choice(key_range, size=n, replace=False).astype(np.uint32)
+    res = run_ranks(keys, key_range, world, "push")
+    per = push_slice_words(key_range, world)
+    assert per % 4 == 0 and per * world * 32 >= key_range
+    parts = []
+    for rank, status, out, offset, total, lo, hi in res:
+        assert status == "ok", (status, out)
+        assert total == n and lo == rank * per * 32 and offset == sum(p.size for p in parts)
+        parts.append(out)
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+
+
+def test_distributed_push_duplicates_rejected():
+    keys = np.arange(0, 2000, 2, dtype=np.uint32)
+    keys[-1] = keys[0]
+    res = run_ranks(keys, 1 << 12, 2, "push")
     for rank, status, code, msg, *_ in res:
         assert status == "BitsortError" and int(code) == 2

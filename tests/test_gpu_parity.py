@@ -661,6 +661,52 @@ def test_scan_sources_vs_numpy(capi, cuda, nsrc, n_words, offset):
     assert bool((out[expected.size:] == -1).all())
 
 
+@pytest.mark.parametrize("world,key_range,n", [(2, (1 << 22) - 7, 200_000), (8, 1 << 26, 1 << 22),
+                                             (3, 1 << 32, 1 << 21), (8, 1 << 28, 1 << 24), (1, 5000, 3000)])
+def test_push_build_emulated(capi, cuda, world, key_range, n):
+    """dist.distributed_sort_push's per-rank calls on one GPU: every emulated
+    rank ORs its shard's bucket bitsets into ALL ranks' slices
+    (bws_gpu_bitset_push, local pointers here instead of IPC-opened peer
+    pointers), then each slice is scanned; the concatenation is the sort."""
+    from paper_1312_0138_b200.dist import CudaRankOps, push_slice_words, shard_bounds
+
+    keys = np.random.default_rng(world + 11).choice(key_range, size=n, replace=False).astype(np.uint32)
+    per = push_slice_words(key_range, world)
+    ops = CudaRankOps()
+    slices = [ops.alloc_slice(per) for _ in range(world)]
+    for r in range(world):
+        lo, hi = shard_bounds(n, r, world)
+        shard = cuda.from_numpy(keys[lo:hi].view(np.int32)).cuda()
+        ops.bitset_push(shard, key_range, slices, per)
+    cuda.cuda.synchronize()
+    parts = []
+    for r in range(world):
+        out, cnt = ops.bitset_scan(slices[r], r * per * 32, n)
+        parts.append(out[: int(cnt.item())].cpu().numpy().view(np.uint32).copy())
+    assert np.array_equal(np.concatenate(parts), np.sort(keys))
+    # the full bitset is the OR of the slices: equal to the direct build
+    full = cuda.cat(slices)[: (key_range + 31) // 32]
+    ref = cuda.full(((key_range + 31) // 32,), -1, dtype=cuda.int32, device="cuda")
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    capi.bitset_build(t.data_ptr(), t.numel(), ref.data_ptr(), key_range)
+    cuda.cuda.synchronize()
+    assert cuda.equal(full, ref)
+
+
+def test_push_argument_checks(capi, cuda):
+    s = cuda.zeros(8, dtype=cuda.int32, device="cuda")
+    k = cuda.zeros(4, dtype=cuda.int32, device="cuda")
+    with pytest.raises(capi.BitsortError) as e:
+        capi.bitset_push(k.data_ptr(), 4, 1 << 10, [s.data_ptr()], 6)  # not a multiple of 4
+    assert e.value.status == capi.Status.ERROR_RANGE
+    with pytest.raises(capi.BitsortError) as e:
+        capi.bitset_push(k.data_ptr(), 4, 1 << 10, [s.data_ptr()], 4)  # 4 words cover 128 keys only
+    assert e.value.status == capi.Status.ERROR_RANGE
+    with pytest.raises(capi.BitsortError) as e:
+        capi.bitset_push(k.data_ptr(), 4, 1 << 7, [s.data_ptr() + 4], 4)  # misaligned slice
+    assert e.value.status == capi.Status.ERROR_DATA
+
+
 def test_ipc_handle_offsets(capi, cuda):
     t = cuda.empty(1 << 20, dtype=cuda.int32, device="cuda")
     h0, off0 = capi.ipc_get_handle(t.data_ptr())
@@ -668,7 +714,7 @@ def test_ipc_handle_offsets(capi, cuda):
     assert len(h0) == capi.IPC_HANDLE_BYTES and h0 == h1 and off1 == off0 + 4000
 
 
-@pytest.mark.parametrize("variant", ["reduce_scatter", "all_to_all", "p2p"])
+@pytest.mark.parametrize("variant", ["reduce_scatter", "all_to_all", "p2p", "push"])
 def test_distributed_sort_nccl_single_rank(capi, cuda, variant):
     """dist.distributed_sort (bitset build, NCCL reduce-scatter, all-gather,
     K3 on the slice) and dist.distributed_sort_a2a (range split, NCCL
@@ -680,8 +726,9 @@ def test_distributed_sort_nccl_single_rank(capi, cuda, variant):
     from paper_1312_0138_b200.dist import distributed_sort as rs
     from paper_1312_0138_b200.dist import distributed_sort_a2a as a2a
     from paper_1312_0138_b200.dist import distributed_sort_p2p as p2p
+    from paper_1312_0138_b200.dist import distributed_sort_push as push
 
-    distributed_sort = {"all_to_all": a2a, "p2p": p2p}.get(variant, rs)
+    distributed_sort = {"all_to_all": a2a, "p2p": p2p, "push": push}.get(variant, rs)
 
     store = dist.HashStore()
     dist.init_process_group("nccl", store=store, rank=0, world_size=1,

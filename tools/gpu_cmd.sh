@@ -1,5 +1,3 @@
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_requests_op_red.sum,lts__t_sectors_op_red.sum,lts__t_sector_hit_rate.pct,lts__t_sector_op_red_hit_rate.pct,l1tex__t_requests_pipe_lsu_mem_global_op_red.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors.sum
-for c in C2 C4; do
-  timeout 600 ncu --metrics $M --clock-control none -k regex:"scatter|scan" -c 4 --csv --log-file gpurun_out/ncu_direct_$c.csv \
-      python tools/run_one.py --config $c --path DIRECT --iters 2 > gpurun_out/ncu_direct_$c.log 2>&1
-done
+timeout 600 python tools/push_bench.py > gpurun_out/push_bench.jsonl 2> gpurun_out/push_bench.err
+timeout 300 python bench.py --config C2 --push --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c2_push_1rank.json 2> gpurun_out/bench_push.err
+timeout 300 python bench.py --config C2 --dist --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c2_rs_1rank.json 2>> gpurun_out/bench_push.err
