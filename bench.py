@@ -39,6 +39,27 @@ NOMINAL_HBM_GBS = 8000.0  # B200 HBM3e nominal (SURVEY.md §8(d) reports both fr
 FALLBACK_HBM_GBPS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
+# The JSON lines go to the process's original stdout; everything else written
+# to fd 1 by native code (e.g. NCCL's "NCCL version ..." banner when NCCL_DEBUG
+# is set in the environment) is sent to stderr, so stdout carries exactly the
+# result lines the driver parses.
+_RESULT_OUT = None
+
+
+def isolate_stdout() -> None:
+    global _RESULT_OUT
+    if _RESULT_OUT is None:
+        sys.stdout.flush()
+        _RESULT_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    out = _RESULT_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def parse_args():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -239,7 +260,7 @@ def run_reference(args, cfg):
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -476,12 +497,13 @@ def run_ours(args, cfg):
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
         "step_roofline": step_roofline, "kernels": kernels, "cpu_baseline": cpu, "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
 def main():
     args = parse_args()
+    isolate_stdout()
     from paper_1312_0138_b200.configs import CONFIGS
 
     names = list(CONFIGS) if args.config == "all" else [args.config]

@@ -71,8 +71,8 @@ def main():
             slices.zero_()
 
         t_build = timed(build, flush, a.iters)
-        t_push = timed(push, flush, a.iters)
         t_zero = timed(zero_only, flush, a.iters)
+        t_push = timed(push, flush, a.iters)
         torch.cuda.synchronize()
         assert torch.equal(slices[:words], full), "push != build"
         print(json.dumps({"config": name, "world": a.world, "shard_keys": int(shard.numel()), "key_range": M,
