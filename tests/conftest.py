@@ -51,6 +51,35 @@ def edge_records():
     return read_records(GOLDEN / "edge_u32.bin")
 
 
+WIDTH_DTYPES = {(8, 0): np.int8, (8, 1): np.uint8, (16, 0): np.int16, (16, 1): np.uint16,
+                (32, 0): np.int32, (32, 1): np.uint32, (64, 0): np.int64, (64, 1): np.uint64}
+
+
+def read_width_records(path: Path):
+    """tests/golden/widths.bin (gen_golden.cpp write_width_records)."""
+    buf = path.read_bytes()
+    magic, ver, count = struct.unpack_from("<III", buf, 0)
+    assert magic == 0x57535742 and ver == 1
+    off = 12
+    recs = []
+    for _ in range(count):
+        width, uns, n, dist = struct.unpack_from("<IIII", buf, off)
+        off += 16
+        dt = np.dtype(WIDTH_DTYPES[(width, uns)]).newbyteorder("<")
+        inp = np.frombuffer(buf, dtype=dt, count=n, offset=off).astype(dt.newbyteorder("="))
+        off += n * dt.itemsize
+        out = np.frombuffer(buf, dtype=dt, count=n, offset=off).astype(dt.newbyteorder("="))
+        off += n * dt.itemsize
+        recs.append({"width": width, "unsigned": uns, "n": n, "dist": dist, "input": inp, "output": out})
+    assert off == len(buf)
+    return recs
+
+
+@pytest.fixture(scope="session")
+def width_records():
+    return read_width_records(GOLDEN / "widths.bin")
+
+
 @pytest.fixture(scope="session")
 def repeats_records():
     return read_records(GOLDEN / "repeats_u32.bin")

@@ -17,6 +17,14 @@
 //                       generator (generator.hpp:91-130: uniform_small_range
 //                       with spans 16 and 1024, constant), n in {100, 1000,
 //                       3000}, trials 0-1, seed 1337, with the reference output
+//   widths.bin          every other (width, signedness) bws_sort arm: the
+//                       reference generator's five distributions
+//                       (generator.hpp:91-130; small range with span 100)
+//                       for int8/uint8/int16/uint16/int32/int64/uint64,
+//                       n in {17, 1000}, seed 1337, with the reference output
+//                       (format: "BWSW" u32 version=1 u32 count, then per
+//                       record u32 width, is_unsigned, n, distribution index,
+//                       then n keys in, n keys out, little endian)
 //   anchors.json        C1/C2/C4 synthetic-input anchors
 //                       computed with the reference's splitmix64 and sorted by
 //                       the reference bws_sort; the test_capi.cpp:78-82 vector
@@ -32,6 +40,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <unordered_set>
 #include <vector>
 
@@ -137,6 +146,52 @@ void anchor(FILE* f, const char* name, const std::vector<uint32_t>& in, bool las
                  fnv1a64(in), fnv1a64(out), *mn, *mx, last ? "" : ",");
 }
 
+template <class T>
+void width_records(FILE* f, uint32_t& count) {
+    constexpr uint32_t width = sizeof(T) * 8;
+    const uint32_t is_unsigned = std::is_unsigned_v<T> ? 1u : 0u;
+    const char* names[] = {"uniform_full_range", "uniform_small_range:100", "sorted", "reverse_sorted",
+                           "constant"};
+    for (uint32_t di = 0; di < 5; ++di) {
+        const bws::distribution_spec d = bws::distribution_spec::parse(names[di]);
+        for (const size_t n : {size_t{17}, size_t{1000}}) {
+            std::vector<T> in = bws::generate_input<T>(n, d, 1337, 0);
+            std::vector<T> out = in;
+            if (bws_sort(out.data(), out.size(), width, static_cast<int>(is_unsigned), BWS_ALG_BITWISE) != BWS_OK) {
+                std::fprintf(stderr, "reference bws_sort failed: %s\n", bws_last_error());
+                std::exit(1);
+            }
+            const uint32_t h[4] = {width, is_unsigned, static_cast<uint32_t>(n), di};
+            std::fwrite(h, sizeof h, 1, f);
+            std::fwrite(in.data(), sizeof(T), n, f);
+            std::fwrite(out.data(), sizeof(T), n, f);
+            ++count;
+        }
+    }
+}
+
+void write_width_records(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) {
+        std::perror(path.c_str());
+        std::exit(1);
+    }
+    uint32_t hdr[3] = {0x57535742u /* "BWSW" */, 1u, 0u};
+    std::fwrite(hdr, sizeof hdr, 1, f);
+    uint32_t count = 0;
+    width_records<int8_t>(f, count);
+    width_records<uint8_t>(f, count);
+    width_records<int16_t>(f, count);
+    width_records<uint16_t>(f, count);
+    width_records<int32_t>(f, count);
+    width_records<int64_t>(f, count);
+    width_records<uint64_t>(f, count);
+    hdr[2] = count;
+    std::fseek(f, 0, SEEK_SET);
+    std::fwrite(hdr, sizeof hdr, 1, f);
+    std::fclose(f);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -159,6 +214,8 @@ int main(int argc, char** argv) {
                 rep.push_back(make_record(bws::generate_input<uint32_t>(n, d, 1337, trial), trial));
     }
     write_records(dir + "/repeats_u32.bin", rep);
+
+    write_width_records(dir + "/widths.bin");
 
     // distinct-key edge cases at the 32-bit boundaries
     std::vector<std::vector<uint32_t>> edges = {

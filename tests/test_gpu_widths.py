@@ -56,6 +56,18 @@ def _device(capi, torch, keys, offset=0):
     return view.cpu().numpy().view(keys.dtype).copy()
 
 
+@pytest.mark.parametrize("width", [8, 16, 32, 64])
+def test_width_golden_vectors(capi, cuda, width_records, width):
+    """The reference's own bws_sort outputs for its generator's distributions
+    at this width, signed and unsigned (tests/golden/widths.bin): bit-exact,
+    host and device arrays."""
+    recs = [r for r in width_records if r["width"] == width]
+    assert recs
+    for rec in recs:
+        assert np.array_equal(_host(capi, rec["input"]), rec["output"]), (rec["unsigned"], rec["dist"], rec["n"])
+        assert np.array_equal(_device(capi, cuda, rec["input"], offset=1), rec["output"])
+
+
 def test_capi_uint8_vector(capi):
     """test_capi.cpp:78-82 exactly as the reference tests it: width 8, unsigned."""
     a = np.array([200, 3, 255, 0], dtype=np.uint8)

@@ -28,6 +28,17 @@ def test_oracle_matches_reference_repeats(repeats_records):
         assert np.array_equal(rec["output"], np.sort(rec["input"]))
 
 
+def test_oracle_matches_reference_widths(width_records):
+    """Every (width, signedness) arm of the reference's bws_sort on its own
+    generator's five distributions: unsigned arms equal the restatement's
+    sort, and every arm equals the ascending order of its input."""
+    assert len(width_records) == 70
+    for rec in width_records:
+        assert np.array_equal(rec["output"], np.sort(rec["input"])), (rec["width"], rec["unsigned"], rec["dist"])
+        if rec["unsigned"]:
+            assert np.array_equal(bitwise_sort(rec["input"]), rec["output"])
+
+
 def test_generate_input_restatement(acceptance_records):
     """oracle_generate_uniform_u32 == generate_input<uint32_t>(n,
     uniform_full_range, 1337, trial) (generator.hpp:91-103), as captured from
