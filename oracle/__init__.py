@@ -23,7 +23,7 @@ def _load_oracle():
         raise ImportError(f"{ORACLE_PATH} missing; run `make -C oracle`")
     lib = ctypes.CDLL(str(ORACLE_PATH))
     vp, sz, u64, u32, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
-    for w in ("u8", "u16", "u32", "u64"):
+    for w in ("u8", "u16", "u32", "u64", "s8", "s16", "s32", "s64"):
         f = getattr(lib, f"oracle_bitwise_sort_{w}")
         f.restype, f.argtypes = i32, [vp, sz, i32]
     lib.oracle_splitmix64_next.restype, lib.oracle_splitmix64_next.argtypes = u64, [ctypes.POINTER(u64)]
@@ -49,11 +49,13 @@ def _load_reference():
 ORACLE = _load_oracle()
 REFERENCE = _load_reference()
 
-_DT = {np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.uint64): "u64"}
+_DT = {np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.uint64): "u64",
+       np.dtype(np.int8): "s8", np.dtype(np.int16): "s16", np.dtype(np.int32): "s32", np.dtype(np.int64): "s64"}
 
 
 def bitwise_sort(a: np.ndarray, skip_empty_bits: bool = False) -> np.ndarray:
-    """Sorted copy via the C restatement of bitsort.hpp:84-136 (unsigned)."""
+    """Sorted copy via the C restatement of bitsort.hpp:84-151 (unsigned, or
+    signed with the reference's sign split)."""
     out = np.ascontiguousarray(a).copy()
     rc = getattr(ORACLE, f"oracle_bitwise_sort_{_DT[out.dtype]}")(out.ctypes.data, out.size, int(skip_empty_bits))
     if rc != 0:

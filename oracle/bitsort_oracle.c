@@ -17,6 +17,14 @@
  *        (unsigned: no sign split)
  *     pass_count<unsigned T> = t            proj/src/bitsort.hpp:46-47
  *
+ *   oracle_bitwise_sort_s{8,16,32,64}
+ *     <- bws::detail::bitwise_sort_impl     proj/src/bitsort.hpp:137-151
+ *        (signed: stable split into negatives and non-negatives, each group
+ *        sorted by the same-sign passes on its two's-complement bits, then
+ *        negatives written back first)
+ *     pass_count<signed T> = t - 1          proj/src/bitsort.hpp:46-47
+ *        (the sign bit is constant inside a group and never inspected)
+ *
  *   oracle_splitmix64_next / oracle_generate_uniform_u32
  *     <- bws::splitmix64                    proj/src/generator.hpp:21-30
  *     <- bws::mix64                         proj/src/generator.hpp:32-36
@@ -79,6 +87,67 @@ DEFINE_BITWISE_SORT(u8, uint8_t, 8)
 DEFINE_BITWISE_SORT(u16, uint16_t, 16)
 DEFINE_BITWISE_SORT(u32, uint32_t, 32)
 DEFINE_BITWISE_SORT(u64, uint64_t, 64)
+
+/* Same-sign passes over bits 0 .. BITS-2 of the unsigned patterns (the sign
+ * split already made the top bit constant), reusing the unsigned routine's
+ * pass on a group (bitsort.hpp:111-129 with pass_count = t - 1). */
+#define DEFINE_SIGNED_SORT(SUFFIX, ST, UT, BITS)                                          \
+    static void same_sign_##SUFFIX(UT* g, size_t n, UT* zeros, UT* ones, int skip) {       \
+        UT set_bits = (UT)~(UT)0;                                                          \
+        if (skip) {                                                                        \
+            set_bits = 0;                                                                  \
+            for (size_t i = 0; i < n; ++i) set_bits |= g[i];                               \
+        }                                                                                  \
+        for (unsigned k = 0; k + 1 < (BITS); ++k) {                                        \
+            if (skip && ((set_bits >> k) & 1u) == 0) continue;                             \
+            size_t zc = 0, oc = 0;                                                         \
+            for (size_t i = 0; i < n; ++i) {                                               \
+                if ((g[i] >> k) & 1u)                                                      \
+                    ones[oc++] = g[i];                                                     \
+                else                                                                       \
+                    zeros[zc++] = g[i];                                                    \
+            }                                                                              \
+            size_t j = 0;                                                                  \
+            for (size_t z = 0; z < zc; ++z) g[j++] = zeros[z];                             \
+            for (size_t o = 0; o < oc; ++o) g[j++] = ones[o];                              \
+        }                                                                                  \
+    }                                                                                      \
+    ORACLE_API int oracle_bitwise_sort_##SUFFIX(ST* a, size_t n, int skip_empty_bits) {    \
+        if (n == 0) return 0;                                                              \
+        UT* neg = (UT*)calloc(n, sizeof(UT));                                              \
+        UT* pos = (UT*)calloc(n, sizeof(UT));                                              \
+        UT* zeros = (UT*)calloc(n, sizeof(UT));                                            \
+        UT* ones = (UT*)calloc(n, sizeof(UT));                                             \
+        if (!neg || !pos || !zeros || !ones) {                                             \
+            free(neg);                                                                     \
+            free(pos);                                                                     \
+            free(zeros);                                                                   \
+            free(ones);                                                                    \
+            return -1;                                                                     \
+        }                                                                                  \
+        size_t nn = 0, np = 0;                                                             \
+        for (size_t i = 0; i < n; ++i) {                                                   \
+            if (a[i] < 0)                                                                  \
+                neg[nn++] = (UT)a[i];                                                      \
+            else                                                                           \
+                pos[np++] = (UT)a[i];                                                      \
+        }                                                                                  \
+        same_sign_##SUFFIX(neg, nn, zeros, ones, skip_empty_bits);                         \
+        same_sign_##SUFFIX(pos, np, zeros, ones, skip_empty_bits);                         \
+        size_t j = 0;                                                                      \
+        for (size_t i = 0; i < nn; ++i) a[j++] = (ST)neg[i];                               \
+        for (size_t i = 0; i < np; ++i) a[j++] = (ST)pos[i];                               \
+        free(neg);                                                                         \
+        free(pos);                                                                         \
+        free(zeros);                                                                       \
+        free(ones);                                                                        \
+        return 0;                                                                          \
+    }
+
+DEFINE_SIGNED_SORT(s8, int8_t, uint8_t, 8)
+DEFINE_SIGNED_SORT(s16, int16_t, uint16_t, 16)
+DEFINE_SIGNED_SORT(s32, int32_t, uint32_t, 32)
+DEFINE_SIGNED_SORT(s64, int64_t, uint64_t, 64)
 
 /* splitmix64 step (generator.hpp:24-29). `state` is advanced in place. */
 ORACLE_API uint64_t oracle_splitmix64_next(uint64_t* state) {

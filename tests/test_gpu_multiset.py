@@ -38,7 +38,7 @@ def _reference(keys: np.ndarray, is_unsigned: int = 1) -> np.ndarray:
     if oracle.REFERENCE is not None:  # the reference's own bws_sort
         assert oracle.REFERENCE.bws_sort(a.ctypes.data, a.size, 32, is_unsigned, 0) == 0
         return a
-    return bitwise_sort(a) if is_unsigned else np.sort(a)
+    return bitwise_sort(a)  # the oracle's restatement (signed split included)
 
 
 def _sort_host(capi, keys, is_unsigned=1):

@@ -33,7 +33,7 @@ def _expected(keys: np.ndarray) -> np.ndarray:
     if oracle.REFERENCE is not None:  # the reference's own bws_sort at this width
         assert oracle.REFERENCE.bws_sort(a.ctypes.data, a.size, WIDTH[a.dtype], int(unsigned), 0) == 0
         return a
-    return bitwise_sort(a) if unsigned else np.sort(a)
+    return bitwise_sort(a)  # the oracle's restatement (signed split included)
 
 
 def _host(capi, keys):

@@ -35,8 +35,8 @@ def test_oracle_matches_reference_widths(width_records):
     assert len(width_records) == 70
     for rec in width_records:
         assert np.array_equal(rec["output"], np.sort(rec["input"])), (rec["width"], rec["unsigned"], rec["dist"])
-        if rec["unsigned"]:
-            assert np.array_equal(bitwise_sort(rec["input"]), rec["output"])
+        assert np.array_equal(bitwise_sort(rec["input"]), rec["output"])
+        assert np.array_equal(bitwise_sort(rec["input"], skip_empty_bits=True), rec["output"])
 
 
 def test_generate_input_restatement(acceptance_records):
@@ -105,6 +105,24 @@ def test_oracle_vs_compiled_reference_random():
     for n in (1, 5, 64, 1000, 100_000):
         a = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
         assert np.array_equal(bitwise_sort(a), oracle.reference_sort_u32(a))
+
+
+@needs_ref
+@pytest.mark.parametrize("dtype", [np.int8, np.uint8, np.int16, np.uint16, np.int32, np.int64, np.uint64])
+def test_oracle_vs_compiled_reference_widths(dtype):
+    """The restatement (including the signed split) against the reference's own
+    bws_sort at every width, on random inputs with and without repeats."""
+    rng = np.random.default_rng(7)
+    info = np.iinfo(dtype)
+    for n in (1, 7, 300, 20_000):
+        for span in (None, 50):
+            if span is None:
+                a = rng.integers(info.min, info.max, size=n, dtype=dtype, endpoint=True)
+            else:
+                a = (rng.integers(0, span, size=n) + (info.min // 2)).astype(dtype)
+            ref = a.copy()
+            assert oracle.REFERENCE.bws_sort(ref.ctypes.data, ref.size, info.bits, int(info.min == 0), 0) == 0
+            assert np.array_equal(bitwise_sort(a), ref)
 
 
 @needs_ref
