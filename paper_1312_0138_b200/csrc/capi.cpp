@@ -33,11 +33,23 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges are no-ops unless a tool attaches
+
 #include "bitsort/bitsort.h"
 #include "bitsort/bitsort_gpu.h"
 #include "kernels.h"
 
 namespace {
+
+// NVTX range over a host-side phase (enqueue of a pipeline, staging copies,
+// entry points), visible in nsys / ncu timelines as "bitsort:<name>".
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 using bws_gpu::Ctrl;
 
@@ -465,6 +477,7 @@ int current_device() {
 // folds the max key; K3 scans (max >> 5) + 1 words).
 void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
                     uint64_t key_range, cudaStream_t stream) {
+    NvtxRange nvtx_range("bitsort:direct K2+K3");
     const bool derived = key_range == 0;
     const uint64_t words = derived ? 0 : (key_range + 31) / 32;
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
@@ -507,6 +520,7 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
 void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
                       uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0,
                       bool multiset = false) {
+    NvtxRange nvtx_range("bitsort:bucketed KB1-KB4");
     cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
     cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
     if (key_range == 0) {
@@ -584,6 +598,7 @@ void check_range(uint64_t key_range) {
 // buffers; the multi-threaded host copy of chunk i+1 overlaps the DMA of
 // chunk i (the driver's own pageable path measured 4x slower than pinned).
 void stage_to_device(DeviceCtx& ctx, void* dev, const void* host, size_t bytes) {
+    NvtxRange nvtx_range("bitsort:host-to-device");
     ctx.ensure_bounce();
     for (size_t off = 0, i = 0; off < bytes; off += kStageChunk, ++i) {
         const int b = static_cast<int>(i & 1);
@@ -600,6 +615,7 @@ void stage_to_device(DeviceCtx& ctx, void* dev, const void* host, size_t bytes) 
 // Device -> pageable host array, the mirror image (DMA of chunk i+1 overlaps
 // the host copy of chunk i).
 void stage_to_host(DeviceCtx& ctx, void* host, const void* dev, size_t bytes) {
+    NvtxRange nvtx_range("bitsort:device-to-host");
     ctx.ensure_bounce();
     const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
     auto issue = [&](size_t i) {
@@ -634,6 +650,7 @@ void stage_to_host(DeviceCtx& ctx, void* host, const void* dev, size_t bytes) {
 // the original survives the detection. Without multiset (the key-range
 // extension) repeated keys are BWS_ERROR_DATA.
 void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, bool multiset = false) {
+    NvtxRange nvtx_range("bitsort:bws_sort u32");
     check_range(key_range);
     if (count == 0) return;
     visible_devices();
@@ -739,6 +756,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
 // pipeline (repeats redone by the counting pass) and widened back. Wider
 // 64-bit spans are BWS_ERROR_CONFIG (no CPU fallback).
 void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned) {
+    NvtxRange nvtx_range("bitsort:bws_sort other width");
     if (count == 0) return;
     visible_devices();
     cudaPointerAttributes attr{};

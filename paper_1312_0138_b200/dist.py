@@ -46,6 +46,7 @@ from typing import Optional, Protocol
 
 import torch
 import torch.distributed as dist
+from torch.cuda import nvtx  # ranges around the exchange steps (no-ops unless a profiler attaches)
 
 
 class RankOps(Protocol):
@@ -256,7 +257,8 @@ def distributed_sort(keys: torch.Tensor, key_range: int, n_total: Optional[int] 
 
     bits = ops.bitset_build(keys, key_range, words)
     slice_ = torch.empty(per, dtype=torch.int32, device=bits.device)
-    dist.reduce_scatter_tensor(slice_, bits, op=dist.ReduceOp.SUM, group=group)
+    with nvtx.range("bitsort:NCCL reduce-scatter"):
+        dist.reduce_scatter_tensor(slice_, bits, op=dist.ReduceOp.SUM, group=group)
 
     key_lo = rank * per * 32
     key_hi = min((rank + 1) * per * 32, key_range)
@@ -314,8 +316,9 @@ def distributed_sort_a2a(keys: torch.Tensor, key_range: int, n_total: Optional[i
     sc = [int(c) for c in counts.tolist()]
     rc = [int(c) for c in recv_counts.tolist()]
     recv = torch.empty(sum(rc), dtype=torch.int32, device=dev)
-    dist.all_to_all_single(recv, grouped[:sum(sc)], output_split_sizes=rc, input_split_sizes=sc,
-                           group=group)
+    with nvtx.range("bitsort:NCCL all-to-all"):
+        dist.all_to_all_single(recv, grouped[:sum(sc)], output_split_sizes=rc, input_split_sizes=sc,
+                               group=group)
 
     key_lo = min(rank * width, key_range)
     key_hi = min((rank + 1) * width, key_range)
@@ -366,7 +369,8 @@ def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[i
         # every rank's build (enqueued before its collective) has finished
         fence = torch.zeros(1, dtype=torch.int32, device=dev)
         dist.all_reduce(fence, group=group)
-    out, count_t = ops.or_scan(sources, rank * per, per, key_lo, capacity)
+    with nvtx.range("bitsort:p2p scan over peer bitsets"):
+        out, count_t = ops.or_scan(sources, rank * per, per, key_lo, capacity)
     # the counts' all-gather doubles as the "peers are done reading" barrier
     counts = [torch.empty_like(count_t) for _ in range(world)]
     dist.all_gather(counts, count_t, group=group)
@@ -408,7 +412,8 @@ def distributed_sort_push(keys: torch.Tensor, key_range: int, n_total: Optional[
         # every slice is zeroed (stream-ordered before this collective) before anyone pushes
         dist.all_reduce(fence, group=group)
     if keys.numel():
-        ops.bitset_push(keys, key_range, targets, per)
+        with nvtx.range("bitsort:push build into owners' slices"):
+            ops.bitset_push(keys, key_range, targets, per)
     if world > 1:
         dist.all_reduce(fence, group=group)  # every rank's pushes have landed
 
