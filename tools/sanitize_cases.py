@@ -1,5 +1,6 @@
-"""Small sorts that launch every kernel of the library once or more, for
-compute-sanitizer (memcheck / racecheck / synccheck) runs:
+"""Small sorts that launch every kernel of the library once or more, each
+checked against numpy. Plain runs work everywhere; where compute-sanitizer is
+allowed (it is closed on this build's GPU pool) the same driver serves:
 
   compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py --quick
