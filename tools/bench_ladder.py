@@ -39,6 +39,16 @@ from paper_1312_0138_b200 import capi, datagen  # noqa: E402
 DEFAULT_SIZES = [1 << k for k in range(16, 27, 2)]
 
 
+def measured_hbm_gbs() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-written), else the profiling recipe's fallback."""
+    import json
+
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6557.8
+
+
 def fit_scaling(records):
     """bench.cpp:162-217: per algorithm, median elapsed per n, least squares of
     log(median) on log(n); (slope, RMS residual in log space, points)."""
@@ -103,8 +113,19 @@ def main():
             ns = max(1, int(e0.elapsed_time(e1) * 1e6))
             records.append(("bitwise_device", 32, n, a.seed, trial, ns, ns / n))
         assert np.array_equal(od.cpu().numpy().view(np.uint32), expected)
-    rec_csv = "algorithm,width,n,seed,trial,elapsed_ns,ns_per_element\n" + "".join(
-        f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]},{r[6]:.3f}\n" for r in records)
+    # the reference's seven columns first (bench.cpp:220), then the GPU
+    # extension of SURVEY.md §5: gpus, config, algorithmic bytes 8n + M/4,
+    # achieved GB/s and its fraction of the measured / nominal HBM peak
+    peak = measured_hbm_gbs()
+    rows = []
+    for r in records:
+        n = r[2]
+        alg_bytes = 8 * n + (4 * n) // 4
+        gbps = alg_bytes / r[5]  # bytes per ns == GB/s
+        rows.append(f"{r[0]},{r[1]},{n},{r[3]},{r[4]},{r[5]},{r[6]:.3f},1,n={n};M={4 * n},{alg_bytes},"
+                    f"{gbps:.1f},{gbps / peak:.4f},{gbps / 8000.0:.4f}\n")
+    rec_csv = ("algorithm,width,n,seed,trial,elapsed_ns,ns_per_element,"
+               "gpus,config,alg_bytes,gbps,roofline_frac_meas,roofline_frac_8tbs\n" + "".join(rows))
     fits = fit_scaling(records)
     slope_csv = "algorithm,slope,residual\n" + "".join(f"{alg},{s:.6f},{e:.6f}\n" for alg, s, e, _ in fits)
     Path(a.out + "_records.csv").parent.mkdir(parents=True, exist_ok=True)
