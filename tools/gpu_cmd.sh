@@ -1,3 +1,2 @@
-timeout 600 python tools/push_bench.py > gpurun_out/push_bench.jsonl 2> gpurun_out/push_bench.err
-timeout 300 python bench.py --config C2 --push --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c2_push_1rank.json 2> gpurun_out/bench_push.err
-timeout 300 python bench.py --config C2 --dist --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c2_rs_1rank.json 2>> gpurun_out/bench_push.err
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q > gpurun_out/pytest_scan.log 2>&1; echo "exit=$?" >> gpurun_out/pytest_scan.log
+timeout 300 python bench.py --config C1 --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/c1_small.json 2>>gpurun_out/c1.err
