@@ -33,3 +33,14 @@ def test_kernel_alg_bytes():
     assert bench.kernel_alg_bytes("bucket_hist", n, m) == 4 * n
     assert bench.kernel_alg_bytes("bitset_scatter", n, m) == 4 * n + m // 8
     assert bench.kernel_alg_bytes("bitset_scan", n, m, world=2) == m // 16 + 4 * n
+
+
+def test_native_stdout_goes_to_stderr():
+    """Anything native code writes to fd 1 (e.g. NCCL's version banner when
+    NCCL_DEBUG is set) must not reach stdout, which carries only result lines."""
+    code = ("import os, sys; sys.argv = ['bench.py']; sys.path.insert(0, %r); import bench; "
+            "bench.isolate_stdout(); os.write(1, b'NCCL version banner\\n'); "
+            "bench.emit({'metric': 'm', 'value': 1})" % str(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, check=True)
+    assert r.stdout.strip().splitlines() == ['{"metric": "m", "value": 1}']
+    assert "NCCL version banner" in r.stderr
