@@ -177,3 +177,38 @@ def test_widths_interleaved_with_32bit(capi):
         for dt in (np.uint8, np.uint32, np.int16, np.uint64, np.int32):
             keys = rng.integers(0, 200, size=5000).astype(dt)
             assert np.array_equal(_host(capi, keys), np.sort(keys))
+
+
+def test_concurrent_mixed_widths_and_shutdown(capi):
+    """Host threads sorting different widths (counting sort, bitset sort with
+    and without repeats, 64-bit narrowing and radix) at the same time share one
+    device context safely; bws_gpu_shutdown releases it and the next call
+    re-initialises."""
+    import threading
+
+    rng = np.random.default_rng(77)
+    inputs = [rng.integers(0, 256, size=300_000, dtype=np.uint8),
+              rng.integers(-(1 << 15), 1 << 15, size=300_000, dtype=np.int64).astype(np.int16),
+              rng.choice(1 << 26, size=1 << 21, replace=False).astype(np.uint32),
+              rng.integers(0, 1 << 20, size=1 << 21, dtype=np.uint32),
+              rng.integers(0, 1 << 30, size=300_000).astype(np.uint64) + np.uint64(7 << 40),
+              rng.integers(np.iinfo(np.int64).min, np.iinfo(np.int64).max, size=300_000, dtype=np.int64)]
+    expected = [np.sort(a) for a in inputs]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                assert np.array_equal(_host(capi, inputs[i]), expected[i])
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, e))
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(inputs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    capi.lib.bws_gpu_shutdown()
+    for a, e in zip(inputs, expected):
+        assert np.array_equal(_host(capi, a), e)
