@@ -456,6 +456,30 @@ def run_ours(args, cfg):
            "api": "dist.distributed_sort on pinned host shards" if use_dist
            else "bws_sort (C ABI) on a pinned host array"}
 
+    if not use_dist:
+        # the PCIe bound of this e2e: plain pinned copies of the same bytes
+        # each way (CUDA events), plus the device-resident step
+        xfer = torch.empty(shard_h.size, dtype=torch.int32, device=dev)
+        cp_ms = {}
+        for name, fn in (("h2d", lambda: xfer.copy_(pinned, non_blocking=True)),
+                         ("d2h", lambda: pinned.copy_(xfer, non_blocking=True))):
+            fn()
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record()
+            for _ in range(3):
+                fn()
+            b_ev.record()
+            b_ev.synchronize()
+            cp_ms[name] = a_ev.elapsed_time(b_ev) / 3
+        del xfer
+        nbytes = 4 * int(shard_h.size)
+        bound_ms = cp_ms["h2d"] + cp_ms["d2h"] + ms_per_step
+        e2e["pcie"] = {"h2d_GBps": round(nbytes / cp_ms["h2d"] / 1e6, 1),
+                       "d2h_GBps": round(nbytes / cp_ms["d2h"] / 1e6, 1),
+                       "bound_ms": round(bound_ms, 3),
+                       "frac_of_bound": round(bound_ms / (e2e_s * 1e3), 4),
+                       "note": "bound = pinned H2D + D2H of the keys + the device-resident step"}
+
     if not use_dist:  # the same drop-in call on ordinary (pageable) host memory
         pg = shard_h.copy()
         ptimes = []
