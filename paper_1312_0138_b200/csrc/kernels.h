@@ -124,13 +124,14 @@ struct BucketPlan {
 // Slab layout of the bucket buffer (KB3 without KB1/KB2): bucket b owns the
 // fixed slots [b * cap, (b + 1) * cap), cap = min(2^shift, n) rounded up to 4,
 // which no set of DISTINCT keys can overflow; per-bucket fill counters replace
-// the histogram pass. A spare tile of slots after the last bucket absorbs the
-// runs of a bucket that duplicates overflowed (that bucket then sorts nothing,
-// so the sort reports the duplicates).
+// the histogram pass. A claim that repeated keys push past a bucket's
+// capacity is aimed at `dump` (past the last bucket) and its stores are
+// skipped: that bucket then sorts nothing, so the popcount total reports the
+// repeats.
 struct SlabArgs {
     std::uint32_t* gcnt = nullptr;         // nb zeroed fill counters
     std::uint32_t cap = 0;                 // slots per bucket
-    std::uint32_t dump = 0;                // first slot of the overflow tile
+    std::uint32_t dump = 0;                // nb * cap: claims at or past it are overflow (dropped)
     std::uint32_t limit = 0;               // keys >= limit are counted as bad (check != 0)
     int check = 0;
     Ctrl* ctrl = nullptr;
