@@ -1676,7 +1676,11 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
             bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
-        else
+        else if (n >= (size_t(1) << 26))  // long shares: 20480-key tiles (C5 KB3 1449 -> 1376 us)
+            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, false>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS, PART_KPT_SLAB), stream>>>(
+                    ks, plan.map, plan.nb, H, tot, parted, base, sa);
+        else  // short shares (C4: ~7 tiles per CTA): 16384-key tiles keep the tail short
             bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
@@ -1745,6 +1749,10 @@ cudaError_t launch_bucket_push(const uint32_t* keys, size_t n, uint64_t key_rang
 cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     int sms = 0;
     cudaError_t err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS, PART_KPT_SLAB)));
     if (err != cudaSuccess) return err;
     auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>;
     auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>;
