@@ -68,7 +68,7 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2", help="C1..C5 (BASELINE.json configs[0..4]) or 'all'")
     ap.add_argument("--path", choices=["AUTO", "DIRECT", "BUCKETED"], default="AUTO")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample-keys", type=int, default=1 << 25,
                     help="keys in the cpu_baseline sample (about 10 s of reference CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
