@@ -66,3 +66,46 @@ def test_random_sweep(cuda):
     finally:
         capi.set_path(capi.Path.AUTO)
     assert done >= 50
+
+
+def test_random_sweep_full_contract(cuda):
+    """The rest of bws_sort's contract under the same kind of sweep: every
+    width and signedness, draws WITH replacement (repeats), host and device
+    arrays, the three pipelines. About thirty seconds."""
+    from paper_1312_0138_b200 import capi
+
+    dtypes = [np.uint8, np.int8, np.uint16, np.int16, np.uint32, np.int32, np.uint64, np.int64]
+    rng = np.random.default_rng(20261020)
+    deadline = time.time() + 30
+    done = 0
+    try:
+        while time.time() < deadline and done < 300:
+            dt = np.dtype(dtypes[int(rng.integers(0, len(dtypes)))])
+            info = np.iinfo(dt)
+            n = int(rng.choice([rng.integers(1, 3000), rng.integers(3000, 1 << 19), rng.integers(1 << 19, 1 << 22)]))
+            span_bits = int(rng.integers(1, info.bits + 1))
+            # base + (random & mask) modulo 2^bits: spans of 2^span_bits values
+            # anywhere in the type, wrapping across its ends
+            r = np.frombuffer(rng.bytes(8 * n), dtype=np.uint64)
+            base = np.frombuffer(rng.bytes(8), dtype=np.uint64)[0]
+            mask = np.uint64((1 << span_bits) - 1)
+            udt = np.dtype(f"uint{info.bits}")
+            keys = (base + (r & mask)).astype(udt).view(dt)
+            lo, hi = int(base), span_bits
+            path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED"]))
+            capi.set_path(getattr(capi.Path, path))
+            ctx = f"{dt} n={n} base={lo} span=2^{hi} path={path}"
+            if rng.random() < 0.5:
+                a = keys.copy()
+                assert capi.sort_raw(a.ctypes.data, n, info.bits, int(info.min == 0), 0) == capi.Status.OK, \
+                    ctx + capi.last_error()
+            else:
+                t = cuda.from_numpy(keys.view(np.uint8).copy()).cuda()
+                assert capi.sort_raw(t.data_ptr(), n, info.bits, int(info.min == 0), 0) == capi.Status.OK, \
+                    ctx + capi.last_error()
+                a = t.cpu().numpy().view(dt)
+            assert np.array_equal(a, np.sort(keys)), ctx
+            done += 1
+    finally:
+        capi.set_path(capi.Path.AUTO)
+    assert done >= 30
