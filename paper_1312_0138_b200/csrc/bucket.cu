@@ -26,6 +26,10 @@
 #include "kernels.h"
 #include "device_util.cuh"
 
+#ifndef KB4_RING
+#define KB4_RING 4  // packed-layout KB4: bulk-copy ring slots in the stage area (C5 KB4: 2 slots 830 us, 4 slots 816, 8 slots 849)
+#endif
+
 #include <cstdlib>
 #include <string>
 
@@ -929,8 +933,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     __shared__ unsigned s_b[2];
     __shared__ unsigned long long s_bbase[2];
     __shared__ uint32_t s_bcnt[2];
-    __shared__ __align__(8) unsigned long long s_lbar[2];  // dense scatter: bulk-load ring (full)
-    __shared__ __align__(8) unsigned long long s_ebar[2];  // ... and its slots consumed (NT arrivals)
+    __shared__ __align__(8) unsigned long long s_lbar[KB4_RING];  // dense scatter: bulk-load ring (full)
+    __shared__ __align__(8) unsigned long long s_ebar[KB4_RING];  // ... and its slots consumed (NT arrivals)
 
     const unsigned lane = threadIdx.x & 31;
     const unsigned warp = threadIdx.x >> 5;
@@ -939,16 +943,16 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     // Dense buckets stream their keys through the (then idle) stage area with
     // bulk copies: two chunks in flight, no L1 or registers tied up by the
     // loads (the SMEM bitset + stage leave KB4 a small L1).
-    constexpr uint32_t kChunk = ((NT / 32) * kStagePitch * 4 / 2) / 16 * 4;  // keys per ring slot
+    constexpr uint32_t kChunk = ((NT / 32) * kStagePitch * 4 / KB4_RING) / 16 * 4;  // keys per ring slot
     // (measured: the ring takes C5's packed-layout KB4 from 1025 to 959 us and
     // makes C2's and C3's slab-layout KB4 2-5% slower, so slab buckets keep
     // register loads)
     unsigned chunk_seq = 0;  // bulk chunks this CTA has consumed (block-uniform)
     if (threadIdx.x == 0) {
-        mbar_init(&s_lbar[0], 1);
-        mbar_init(&s_lbar[1], 1);
-        mbar_init(&s_ebar[0], NT);
-        mbar_init(&s_ebar[1], NT);
+        for (int q = 0; q < KB4_RING; ++q) {
+            mbar_init(&s_lbar[q], 1);
+            mbar_init(&s_ebar[q], NT);
+        }
         fence_mbar_init();
     }
     const uint32_t seg_words = W / (NT / 32);
@@ -1001,18 +1005,18 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                 const unsigned g = chunk_seq + c;
                 const uint32_t len = min(kChunk, body - c * kChunk);
                 fence_proxy_async_smem();
-                tma_load_bytes(s_stage_all + (g & 1u) * kChunk, src + head + c * kChunk, len * 4, &s_lbar[g & 1u]);
+                tma_load_bytes(s_stage_all + (g % KB4_RING) * kChunk, src + head + c * kChunk, len * 4,
+                               &s_lbar[g % KB4_RING]);
             };
             if (threadIdx.x == 0) {
-                if (nchunks > 0) issue(0);
-                if (nchunks > 1) issue(1);
+                for (uint32_t q = 0; q < KB4_RING && q < nchunks; ++q) issue(q);
             }
             if (threadIdx.x < head) set_key(__ldcs(src + threadIdx.x));
             if (threadIdx.x < cnt - head - body) set_key(__ldcs(src + head + body + threadIdx.x));
             for (uint32_t c = 0; c < nchunks; ++c) {
                 const unsigned g = chunk_seq + c;
-                mbar_wait(&s_lbar[g & 1u], (g >> 1) & 1u);
-                const uint4* r4 = reinterpret_cast<const uint4*>(s_stage_all + (g & 1u) * kChunk);
+                mbar_wait(&s_lbar[g % KB4_RING], (g / KB4_RING) & 1u);
+                const uint4* r4 = reinterpret_cast<const uint4*>(s_stage_all + (g % KB4_RING) * kChunk);
                 const uint32_t nv = min(kChunk, body - c * kChunk) / 4;
                 for (uint32_t i = threadIdx.x; i < nv; i += NT) {
                     const uint4 v = r4[i];
@@ -1021,10 +1025,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                     set_key(v.z);
                     set_key(v.w);
                 }
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_ebar[g & 1u])) : "memory");
-                if (threadIdx.x == 0 && c + 2 < nchunks) {  // refill once every thread is done with the slot
-                    mbar_wait(&s_ebar[g & 1u], (g >> 1) & 1u);
-                    issue(c + 2);
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_ebar[g % KB4_RING])) : "memory");
+                if (threadIdx.x == 0 && c + KB4_RING < nchunks) {  // refill once every thread is done with the slot
+                    mbar_wait(&s_ebar[g % KB4_RING], (g / KB4_RING) & 1u);
+                    issue(c + KB4_RING);
                 }
             }
             chunk_seq += nchunks;
