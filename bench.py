@@ -36,7 +36,6 @@ sys.path.insert(0, str(ROOT))
 METRIC = "sorted keys/sec (Gkeys/s) at 1/2/4/8 B200; achieved HBM GB/s fraction of roofline"
 UNIT = "Gkeys/s"
 NOMINAL_HBM_GBS = 8000.0  # B200 HBM3e nominal (SURVEY.md §8(d) reports both fractions)
-FALLBACK_HBM_GBPS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
 # The JSON lines go to the process's original stdout; everything else written
@@ -63,7 +62,7 @@ def emit(line: dict) -> None:
 def parse_args():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2", help="C1..C5 (BASELINE.json configs[0..4]) or 'all'")
@@ -80,6 +79,8 @@ def parse_args():
                     help="multi-GPU peer-to-peer variant (the exchange fused into the scan over CUDA IPC)")
     ap.add_argument("--push", action="store_true",
                     help="multi-GPU push variant (the exchange fused into the build: bulk ORs into peers' slices)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only, on gloo without a GPU (CPU test of the launcher)")
     return ap.parse_args()
 
 
@@ -103,13 +104,9 @@ def host_info():
 
 
 def measured_peak():
-    p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        try:
-            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-        except (ValueError, KeyError):
-            pass
-    return FALLBACK_HBM_GBPS, "fallback (B200_PROFILING.md)"
+    from paper_1312_0138_b200.configs import hbm_peak
+
+    return hbm_peak()
 
 
 # --- per-kernel algorithmic bytes ----------------------
@@ -225,36 +222,39 @@ def cpu_baseline(keys: np.ndarray, sample: int, workload: str):
 
 
 def run_reference(args, cfg):
+    """The reference's own CPU sort (bws_sort(…,32,1,BWS_ALG_BITWISE) from
+    oracle/_ref) on the SAME workload as our arm: every step sorts a fresh copy
+    of all cfg.n keys (C2: ~8 s per step on one core). The reference sort is
+    single-threaded (bitsort.hpp:122-128), so one host core does the work; the
+    copy that restores the unsorted input is outside the timed call, as in
+    the reference's own bench (bench.cpp:143-147)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     sort, kind, what = reference_sorter()
     keys = cfg.generate()
-    # size each step so that W + K steps take about two minutes at ~4 Mkeys/s
-    budget_s = 120.0
-    sample = int(min(cfg.n, max(1 << 16, 4e6 * budget_s / max(1, args.steps + args.warmup))))
-    base = keys[:sample].copy()
+    a = np.empty_like(keys)
     for _ in range(args.warmup):
-        a = base.copy()
+        np.copyto(a, keys)
         sort(a)
     times = []
     for _ in range(args.steps):
-        a = base.copy()
+        np.copyto(a, keys)
         t0 = time.perf_counter()
         sort(a)
         times.append(time.perf_counter() - t0)
-    assert np.all(a[1:] > a[:-1])
+    assert np.all(a[1:] > a[:-1]) and a.size == cfg.n
     ms = 1e3 * sum(times) / len(times)
-    value = sample / (ms / 1e3) / 1e9
+    value = cfg.n / (ms / 1e3) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "key_range": cfg.key_range,
-                   "recipe": cfg.recipe, "step_sample_keys": sample},
+                   "recipe": cfg.recipe, "step_sample_keys": cfg.n},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": kind,
-                         "sample": f"first {sample} keys of {cfg.name} per step ({what}); "
+                         "sample": f"all {cfg.n} keys of {cfg.name} per step ({what}); "
                                    "single-threaded reference (bitsort.hpp:122-128, SPEC.md:216)",
                          **host_info()},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -266,13 +266,18 @@ def run_reference(args, cfg):
 
 # --- our GPU arm ------------------------------------------------------------
 def traffic_from_profiles(workload: str, kernel: str):
+    """DRAM bytes (read + write) per launch from the committed ncu summary;
+    kernel "step" = the sum over the workload's kernels (one sort)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+        per = json.loads(p.read_text()).get(workload, {})
     except ValueError:
         return None
+    if kernel == "step":
+        return float(sum(per.values())) if per else None
+    return per.get(kernel)
 
 
 def run_ours(args, cfg):
@@ -391,36 +396,59 @@ def run_ours(args, cfg):
     ms_per_step = total_ms / args.steps
     value = n_total / (ms_per_step / 1e3) / 1e9
 
-    # dominant kernel roofline (live CUDA-event durations from the timed region)
+    # roofline: algorithmic bytes B_alg = 8n + M/4 per sort
+    # (key read + bitset write + bitset read + key write) over the step's
+    # kernel time (the sum of the live per-launch CUDA-event durations of the
+    # sort's kernels in one step; the slowest rank at N > 1), against the
+    # measured HBM peak of all N GPUs. The design's own per-kernel traffic
+    # fraction (bytes each kernel really has to move) is reported apart as
+    # `impl_frac`.
     peak, peak_src = measured_peak()
-    dom = max(ktimes.items(), key=lambda kv: kv[1][1]) if ktimes else None
-    roofline = None
     kernels = {}
     n_local = shard_h.size
+    kernel_ms_per_step = 0.0
     for name, (cnt, ms) in ktimes.items():
         avg_s = ms / cnt / 1e3
         bytes_ = kernel_alg_bytes(name, n_local, M, world)
         kernels[name] = {"launches": cnt, "avg_us": round(avg_s * 1e6, 2),
-                         "alg_bytes": bytes_, "GBps": round(bytes_ / avg_s / 1e9, 1) if bytes_ else None,
+                         "impl_bytes": bytes_, "GBps": round(bytes_ / avg_s / 1e9, 1) if bytes_ else None,
                          "share": round(ms / max(total_ms_k, 1e-9), 3)}
-    if dom:
-        name, (cnt, ms) = dom
-        avg_s = ms / cnt / 1e3
-        achieved = kernel_alg_bytes(name, n_local, M, world) / avg_s / 1e9
-        tr = traffic_from_profiles(cfg.name, name)
-        roofline = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1),
-                    "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
-                    "traffic": tr, "peak_source": peak_src,
-                    "timing": "per-launch CUDA events on the launching stream, from a second K-step pass "
-                              "(the events add ~10 us per step, so `value` comes from a pass without them)",
-                    "alg_bytes_per_launch": kernel_alg_bytes(name, n_local, M, world)}
+        kernel_ms_per_step += ms / args.steps
+    if use_dist and ktimes:
+        t = torch.tensor([kernel_ms_per_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kernel_ms_per_step = float(t.item())
     step_alg = 8 * n_total + M // 4
+    roofline = None
+    if ktimes:
+        dom_name, (dom_cnt, dom_ms) = max(ktimes.items(), key=lambda kv: kv[1][1])
+        dom_s = dom_ms / dom_cnt / 1e3
+        achieved = step_alg / (kernel_ms_per_step / 1e3) / 1e9
+        roofline = {
+            "bound": "hbm", "kernel": "+".join(sorted(ktimes)),
+            "achieved": round(achieved, 1), "peak": round(peak * world, 1), "unit": "GB/s",
+            "frac": round(achieved / (peak * world), 4),
+            "frac_of_nominal_8tbs": round(achieved / (NOMINAL_HBM_GBS * world), 4),
+            "traffic": traffic_from_profiles(cfg.name, "step"),
+            "alg_bytes_per_step": step_alg,
+            "formula": "SURVEY.md 8(d): B_alg = 8n + M/4 (key read + bitset write + bitset read + key write) "
+                       "/ the step's summed kernel time / (N x peak)",
+            "kernel_us_per_step": round(kernel_ms_per_step * 1e3, 2),
+            "peak_source": peak_src,
+            "timing": "per-launch CUDA events on the launching stream, from a second K-step pass "
+                      "(the events add ~10 us per step, so `value` comes from a pass without them)",
+            "impl_frac": {"kernel": dom_name,
+                          "impl_bytes_per_launch": kernel_alg_bytes(dom_name, n_local, M, world),
+                          "achieved": round(kernel_alg_bytes(dom_name, n_local, M, world) / dom_s / 1e9, 1),
+                          "frac": round(kernel_alg_bytes(dom_name, n_local, M, world) / dom_s / 1e9 / peak, 4),
+                          "traffic": traffic_from_profiles(cfg.name, dom_name),
+                          "note": "the dominant kernel's own bytes (the bytes this design moves, "
+                                  "DESIGN.md kernel table) over its average launch time"}}
     step_roofline = {"alg_bytes": step_alg,
                      "achieved": round(step_alg / (ms_per_step / 1e3) / 1e9, 1),
                      "frac": round(step_alg / (ms_per_step / 1e3) / 1e9 / (peak * world), 4),
                      "frac_of_nominal_8tbs": round(step_alg / (ms_per_step / 1e3) / 1e9 / (NOMINAL_HBM_GBS * world), 4),
-                     "formula": "8n + M/4 (key read + bitset write + bitset read + key write)"}
+                     "formula": "8n + M/4 over the whole step (events around the step, incl. memsets)"}
 
     # end to end through the public API: pinned host keys -> sorted host keys
     e2e_steps = max(1, args.e2e_steps)
@@ -525,8 +553,79 @@ def run_ours(args, cfg):
     return 0
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-executes this script
+    under torch.distributed.run with N ranks on 127.0.0.1 (one process per
+    GPU, the layout the driver's torchrun launch uses). The ranks inherit
+    this process's stdout, so rank 0's JSON line is the only result line."""
+    import subprocess
+
+    if not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py --gpus {args.gpus} needs {args.gpus} CUDA devices; "
+                             f"this host has {have}\n")
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, cfg):
+    """--dry-run: the multi-rank plumbing of a step without a GPU (gloo):
+    input-position shards, barrier-bracketed timing, max over ranks, one
+    JSON line from rank 0. Exercised by tests/test_bench_cpu.py."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1312_0138_b200.dist import shard_bounds, slice_words
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    lo, hi = shard_bounds(cfg.n, rank, world)
+    times = []
+    for _ in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        cnt = torch.tensor([hi - lo], dtype=torch.int64)
+        if world > 1:
+            dist.all_reduce(cnt)
+        times.append(time.perf_counter() - t0)
+    assert int(cnt.item()) == cfg.n
+    total = torch.tensor([sum(times[args.warmup:])], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    if rank == 0:
+        _, per = slice_words(cfg.key_range, world)
+        emit({"dry_run": True, "metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": round(1e3 * float(total.item()) / args.steps, 4),
+              "config": {"workload": cfg.name, "n": cfg.n, "key_range": cfg.key_range},
+              "shard_keys": hi - lo, "slice_words": per,
+              "nvlink_bytes_per_rank": (world - 1) * per * 4})
+    return 0
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":
+            args.gpus = 1  # rank 0 alone runs the reference arm: no ranks to spawn
+        else:
+            return launch_ranks(args)
     isolate_stdout()
     from paper_1312_0138_b200.configs import CONFIGS
 
@@ -534,7 +633,12 @@ def main():
     rc = 0
     for name in names:
         cfg = CONFIGS[name]
-        rc |= run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+        if args.dry_run:
+            rc |= run_dry(args, cfg)
+        elif args.impl == "reference":
+            rc |= run_reference(args, cfg)
+        else:
+            rc |= run_ours(args, cfg)
     return rc
 
 

@@ -5,12 +5,29 @@ M/8 + output write 4n.
 """
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
+from pathlib import Path
 from typing import Callable
 
 import numpy as np
 
 from . import datagen
+
+# /opt/skills/guides/B200_PROFILING.md: the HBM figure to use only when the
+# driver-written MEASURED_PEAKS.json is absent
+FALLBACK_HBM_GBPS = 6650.0
+_PEAKS = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+
+
+def hbm_peak() -> tuple[float, str]:
+    """(HBM GB/s, source): MEASURED_PEAKS.json hbm_gbs (the driver's measured
+    copy bandwidth on this pool's B200s), else the profiling recipe's fallback.
+    The one peak every tool divides by."""
+    try:
+        return float(json.loads(_PEAKS.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, ValueError, KeyError):
+        return FALLBACK_HBM_GBPS, "fallback (B200_PROFILING.md, 6.65 TB/s)"
 
 
 @dataclass(frozen=True)

@@ -25,9 +25,13 @@
 //                       (format: "BWSW" u32 version=1 u32 count, then per
 //                       record u32 width, is_unsigned, n, distribution index,
 //                       then n keys in, n keys out, little endian)
-//   anchors.json        C1/C2/C4 synthetic-input anchors
-//                       computed with the reference's splitmix64 and sorted by
-//                       the reference bws_sort; the test_capi.cpp:78-82 vector
+//   anchors.json        C1-C5 synthetic-input anchors:
+//                       C1/C2/C4 generated with the reference's splitmix64,
+//                       C3 (Feistel permutation) and C5 (clustered Zipf) with
+//                       csrc/datagen.c; every one sorted by the reference
+//                       bws_sort(...,32,1,BWS_ALG_BITWISE) and hashed (FNV-1a 64
+//                       over the little-endian bytes). C3 takes ~5 min and C5
+//                       ~1 min of single-threaded reference sort.
 //
 // Record format (little endian): "BWSG" u32 version=1 u32 count, then per
 // record: u32 n, u32 trial, u32 distinct(0/1), u32 pad, n x u32 input,
@@ -45,6 +49,13 @@
 #include <vector>
 
 #include "generator.hpp"  // bws::splitmix64, bws::generate_input (reference headers)
+
+// C3/C5 inputs come from this repo's seeded generator (csrc/datagen.c, linked
+// into this program by oracle/Makefile): the same bytes the tests and the bench
+// generate, so the reference's sorted output of them pins the GPU output.
+extern "C" int bws_gen_permutation(uint32_t* out, uint64_t n, uint64_t seed);
+extern "C" int bws_gen_clustered(uint32_t* out, uint64_t n, uint32_t clusters, double zipf_s,
+                                 uint64_t half_window, uint64_t seed, uint32_t* centres_out);
 
 namespace {
 
@@ -247,7 +258,26 @@ int main(int argc, char** argv) {
     std::fprintf(f, "  \"_generator\": \"tests/golden/gen_golden.cpp (reference bws_sort via oracle/_ref/libbitsort_ref.so)\",\n");
     anchor(f, "C1", shuffle_prefix(1000000, 1ull << 24, 42), false);
     anchor(f, "C2", shuffle_prefix(1ull << 26, 1ull << 28, 42), false);
-    anchor(f, "C4", dedup_draws(1ull << 24, 42), true);
+    anchor(f, "C4", dedup_draws(1ull << 24, 42), false);
+    {
+        // C5: 2^28 keys, 4096 clusters, Zipf(1.2), +-2^18 windows, seed 42 (configs.py)
+        std::vector<uint32_t> c5(1ull << 28);
+        std::vector<uint32_t> centres(4096);
+        if (bws_gen_clustered(c5.data(), c5.size(), 4096, 1.2, 1ull << 18, 42, centres.data()) != 0) {
+            std::fprintf(stderr, "bws_gen_clustered failed\n");
+            return 1;
+        }
+        anchor(f, "C5", c5, std::getenv("GOLDEN_SKIP_C3") != nullptr);
+    }
+    if (!std::getenv("GOLDEN_SKIP_C3")) {
+        // C3: Feistel permutation of [0, 2^30), seed 42 (configs.py); sorted = identity
+        std::vector<uint32_t> c3(1ull << 30);
+        if (bws_gen_permutation(c3.data(), c3.size(), 42) != 0) {
+            std::fprintf(stderr, "bws_gen_permutation failed\n");
+            return 1;
+        }
+        anchor(f, "C3", c3, true);
+    }
     std::fprintf(f, "}\n");
     std::fclose(f);
     std::printf("golden fixtures written to %s\n", dir.c_str());

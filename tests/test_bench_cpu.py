@@ -44,3 +44,32 @@ def test_native_stdout_goes_to_stderr():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, check=True)
     assert r.stdout.strip().splitlines() == ['{"metric": "m", "value": 1}']
     assert "NCCL version banner" in r.stderr
+
+
+def test_launcher_dry_run_two_ranks():
+    """`python bench.py --gpus 2` outside torchrun re-executes itself under
+    torch.distributed.run with two ranks; --dry-run runs the ranks' plumbing on
+    gloo (no GPU). Exactly one JSON line comes back, from rank 0."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run", "--config", "C2",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["dry_run"] is True and d["n_gpus"] == 2 and d["steps"] == 3
+    assert d["shard_keys"] == (1 << 26) // 2
+    assert d["nvlink_bytes_per_rank"] == (1 << 28) // 32 // 2 * 4
+
+
+def test_launcher_rejects_missing_devices():
+    """Without N CUDA devices `--gpus N` fails with a clear message (exit 2)
+    instead of a torchrun error."""
+    import torch
+
+    if torch.cuda.device_count() >= 4:
+        return
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 2
+    assert "needs 4 CUDA devices" in r.stderr
+    assert r.stdout.strip() == ""

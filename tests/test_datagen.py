@@ -26,6 +26,21 @@ def test_c2_c4_match_reference_anchors(anchors):
         assert int(k.min()) == anchors[name]["min"] and int(k.max()) == anchors[name]["max"]
 
 
+@pytest.mark.slow
+def test_c5_matches_reference_anchors(anchors):
+    """C5 comes from csrc/datagen.c (not the reference's generator); its input
+    hash and the reference bws_sort's output hash were recorded by
+    gen_golden.cpp from the same generator, so numpy's sort of the keys must
+    reproduce the reference's sorted hash."""
+    k = CONFIGS["C5"].generate()
+    a = anchors["C5"]
+    assert k.size == a["n"] and k[:8].tolist() == a["first8"]
+    assert datagen.fnv1a64(k) == a["fnv1a64_input"]
+    k.sort()
+    assert datagen.fnv1a64(k) == a["fnv1a64_sorted"]
+    assert int(k[0]) == a["min"] and int(k[-1]) == a["max"]
+
+
 def test_shuffle_prefix_is_distinct_and_in_range():
     k = datagen.shuffle_prefix(50_000, 1 << 16, seed=7)
     assert np.unique(k).size == k.size and int(k.max()) < 1 << 16

@@ -548,10 +548,14 @@ def test_config_vs_reference_hash(capi, cuda, anchors, name, path):
 
 
 @pytest.mark.parametrize("path", PATHS)
-def test_c3_dense_permutation(capi, cuda, path):
+def test_c3_dense_permutation(capi, cuda, anchors, path):
+    """C3 = a permutation of [0, 2^30): the output is the identity, and its
+    hash equals the reference sort's output hash (gen_golden.cpp)."""
     cfg, keys, out = _config_sort(capi, cuda, "C3", path)
+    assert fnv1a64(keys) == anchors["C3"]["fnv1a64_input"]
     del keys
     assert cuda.equal(out, cuda.arange(cfg.n, dtype=cuda.int32, device="cuda"))
+    assert fnv1a64(out.cpu().numpy().view(np.uint32)) == anchors["C3"]["fnv1a64_sorted"]
 
 
 @pytest.mark.slow
@@ -577,11 +581,14 @@ def test_more_than_2_31_keys(capi, cuda, path):
 
 
 @pytest.mark.parametrize("path", PATHS)
-def test_c5_clustered_properties(capi, cuda, path):
-    """Size-independent properties: strictly ascending, same count, and the same
-    sum and sum-of-squares (mod 2^64) as the input: together a permutation check
-    for a strictly ascending output."""
+def test_c5_clustered_properties(capi, cuda, anchors, path):
+    """Pinned to the reference: input and sorted-output hashes equal the ones
+    gen_golden.cpp recorded from the reference bws_sort of the same C5 keys.
+    Also the size-independent properties: strictly ascending, same count, and
+    the same sum and sum-of-squares (mod 2^64) as the input."""
     cfg, keys, out = _config_sort(capi, cuda, "C5", path)
+    assert fnv1a64(keys) == anchors["C5"]["fnv1a64_input"]
+    assert fnv1a64(out.cpu().numpy().view(np.uint32)) == anchors["C5"]["fnv1a64_sorted"]
     u = out.to(cuda.int64) & 0xFFFFFFFF
     assert u.numel() == cfg.n
     assert bool((u[1:] > u[:-1]).all())

@@ -29,36 +29,38 @@ import sys
 import time
 from pathlib import Path
 
-import numpy as np
-import torch
-
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-from paper_1312_0138_b200 import capi, datagen  # noqa: E402
 
 DEFAULT_SIZES = [1 << k for k in range(16, 27, 2)]
 
 
 def measured_hbm_gbs() -> float:
     """MEASURED_PEAKS.json hbm_gbs (driver-written), else the profiling recipe's fallback."""
-    import json
+    from paper_1312_0138_b200.configs import hbm_peak
 
-    try:
-        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
-    except Exception:
-        return 6557.8
+    return hbm_peak()[0]
+
+
+class ConfigError(ValueError):
+    """bench.cpp's config_error (a slope fit over fewer than 4 sizes)."""
 
 
 def fit_scaling(records):
-    """bench.cpp:162-217: per algorithm, median elapsed per n, least squares of
-    log(median) on log(n); (slope, RMS residual in log space, points)."""
+    """bench.cpp:162-217: per algorithm (first-seen order), median elapsed per n
+    (mean of the middle two for an even trial count), least squares of
+    log(median) on log(n); [(algorithm, slope, RMS residual in log space,
+    [(n, median), ...])]. Fewer than 4 distinct sizes -> ConfigError."""
     out = []
     for alg in dict.fromkeys(r[0] for r in records):
         by_n = {}
         for r in records:
             if r[0] == alg:
                 by_n.setdefault(r[2], []).append(r[5])
-        pts = [(n, statistics.median(v)) for n, v in sorted(by_n.items())]
+        if len(by_n) < 4:
+            raise ConfigError(f"slope fit needs at least 4 distinct sizes for algorithm '{alg}', "
+                              f"got {len(by_n)}")
+        pts = [(n, float(statistics.median(v))) for n, v in sorted(by_n.items())]
         xs = [math.log(n) for n, _ in pts]
         ys = [math.log(t) for _, t in pts]
         mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
@@ -70,6 +72,17 @@ def fit_scaling(records):
     return out
 
 
+def records_csv(records) -> str:
+    """bench.cpp:219-231: the reference's seven-column records CSV."""
+    return "algorithm,width,n,seed,trial,elapsed_ns,ns_per_element\n" + "".join(
+        f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]},{r[6]:.3f}\n" for r in records)
+
+
+def reports_csv(reports) -> str:
+    """bench.cpp reports_csv: algorithm,slope,residual with 6 decimals."""
+    return "algorithm,slope,residual\n" + "".join(f"{alg},{s:.6f},{e:.6f}\n" for alg, s, e, _ in reports)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default=",".join(map(str, DEFAULT_SIZES)))
@@ -77,6 +90,11 @@ def main():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "ladder"))
     a = ap.parse_args()
+    import numpy as np
+    import torch
+
+    from paper_1312_0138_b200 import capi, datagen
+
     sizes = [int(s) for s in a.sizes.split(",")]
     if len(sizes) < 4:
         raise SystemExit("slope fit needs at least 4 sizes (bench.cpp:117-124)")
@@ -124,10 +142,10 @@ def main():
         gbps = alg_bytes / r[5]  # bytes per ns == GB/s
         rows.append(f"{r[0]},{r[1]},{n},{r[3]},{r[4]},{r[5]},{r[6]:.3f},1,n={n};M={4 * n},{alg_bytes},"
                     f"{gbps:.1f},{gbps / peak:.4f},{gbps / 8000.0:.4f}\n")
-    rec_csv = ("algorithm,width,n,seed,trial,elapsed_ns,ns_per_element,"
+    rec_csv = ("algorithm,width,n,seed,trial,elapsed_ns,ns_per_element,"  # records_csv's 7 + GPU columns
                "gpus,config,alg_bytes,gbps,roofline_frac_meas,roofline_frac_8tbs\n" + "".join(rows))
     fits = fit_scaling(records)
-    slope_csv = "algorithm,slope,residual\n" + "".join(f"{alg},{s:.6f},{e:.6f}\n" for alg, s, e, _ in fits)
+    slope_csv = reports_csv(fits)
     Path(a.out + "_records.csv").parent.mkdir(parents=True, exist_ok=True)
     Path(a.out + "_records.csv").write_text(rec_csv)
     Path(a.out + "_slopes.csv").write_text(slope_csv)

@@ -17,7 +17,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1312_0138_b200 import capi  # noqa: E402
-from paper_1312_0138_b200.configs import CONFIGS  # noqa: E402
+from paper_1312_0138_b200.configs import CONFIGS, hbm_peak  # noqa: E402
 
 
 def timed(fn, flush, iters):
@@ -70,7 +70,7 @@ def main():
                               "build_us": round(tb[0] * 1e6, 1), "scan_us": round(ts[0] * 1e6, 1),
                               "sort_us": round(tf[0] * 1e6, 1), "sort_min_us": round(tf[1] * 1e6, 1),
                               "gkeys_s": round(cfg.n / tf[0] / 1e9, 2), "alg_GBps": round(gbs, 1),
-                              "frac_meas": round(gbs / 6557.8, 3), "ok": ok}), flush=True)
+                              "frac_meas": round(gbs / hbm_peak()[0], 3), "ok": ok}), flush=True)
         del keys, out, bits
 
 
