@@ -20,15 +20,19 @@
  * handle (:101-143) entry points are not on the sort path and are not part of
  * this library.
  *
- * Domain of the GPU bws_sort: BWS_ALG_BITWISE (or its BWS_ALG_BITWISE_SKIP_EMPTY
- * variant), unsigned or signed keys (mapped onto the unsigned order by flipping
- * the sign bit on load and store), naturally aligned:
+ * Domain of the GPU bws_sort: every algorithm id (a sort's output is unique, so
+ * BITWISE, BITWISE_SKIP_EMPTY, INSERTION, MERGE, COUNTING and PLATFORM all run
+ * the GPU pipelines below; COUNTING keeps the reference's span limit: max - min
+ * >= 2^26 is BWS_ERROR_RANGE, baselines.hpp:95-110), unsigned or signed keys
+ * (mapped onto the unsigned order by flipping the sign bit on load and store),
+ * naturally aligned:
  *   width 32  the bitset sort (the hot path); repeated keys are detected and
  *             sorted by a GPU counting-sort pass, as the reference sorts them;
  *   width 8/16  a GPU counting sort over the type's range;
  *   width 64  keys whose span max - min is below 2^32 narrowed to the 32-bit
  *             path; wider spans by a stable LSD radix sort (8-bit digits).
- * Other algorithms return BWS_ERROR_CONFIG. There is no CPU fallback.
+ * There is no CPU fallback: without a CUDA device every call that sorts
+ * returns BWS_ERROR_INTERNAL.
  * Additive GPU extensions live in bitsort_gpu.h.
  */
 
@@ -54,7 +58,7 @@ typedef enum bws_status {
     BWS_ERROR_CONFIG = 1,    /* unsupported width/signedness/algorithm, bad API usage */
     BWS_ERROR_DATA = 2,      /* null data, duplicate keys, key outside the range hint */
     BWS_ERROR_INTEGRITY = 3, /* kept for ABI value parity; not produced by bws_sort */
-    BWS_ERROR_RANGE = 4,     /* range hint out of bounds */
+    BWS_ERROR_RANGE = 4,     /* range hint out of bounds; COUNTING key span >= 2^26 */
     BWS_ERROR_INTERNAL = 5   /* CUDA / NCCL failure (message in bws_last_error) */
 } bws_status;
 

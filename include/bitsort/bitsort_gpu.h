@@ -24,10 +24,14 @@ extern "C" {
  * the max-reduction pass. Keys >= key_range -> BWS_ERROR_DATA, data untouched. */
 BITSORT_API bws_status bws_sort_u32_range(void* data, size_t count, uint64_t key_range);
 
-/* Device-resident sort, stream-ordered, no host synchronisation. `keys` and
- * `out` are device pointers (they may alias for an in-place sort). On return
- * the work is queued on `stream`; bws_gpu_sort_check() synchronises and
- * validates the most recent sort on this device. */
+/* Device-resident sort, stream-ordered, no host synchronisation (also with
+ * key_range == 0: the range is then derived on the device by the direct
+ * pipeline, which is slower for large inputs than giving the hint), so it can
+ * be captured in a CUDA graph. `keys` and `out` are device pointers (they may
+ * alias for an in-place sort). On return the work is queued on `stream`;
+ * bws_gpu_sort_check() synchronises and validates the most recent async sort
+ * on this device — other library calls in between do not disturb its result
+ * (its control block is set aside first). */
 BITSORT_API bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t count,
                                                  uint32_t* out, uint64_t key_range,
                                                  void* stream);
@@ -51,8 +55,9 @@ BITSORT_API bws_status bws_gpu_range_split(const uint32_t* keys, size_t count, u
                                            int parts, uint32_t* out, uint32_t* d_counts,
                                            uint64_t* part_width, void* stream);
 
-/* Synchronises `stream` and validates the last bws_gpu_sort_device_async on
- * the current device: BWS_ERROR_DATA on duplicates / out-of-range keys.
+/* Synchronises `stream` (and the sort's own stream) and validates the most
+ * recent bws_gpu_sort_(range_)device_async on the current device:
+ * BWS_ERROR_DATA on duplicates / out-of-range keys.
  * *distinct_out (optional) receives the number of keys written. */
 BITSORT_API bws_status bws_gpu_sort_check(void* stream, uint64_t* distinct_out);
 

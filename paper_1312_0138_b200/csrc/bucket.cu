@@ -1401,9 +1401,14 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
 // K0: max key (only when no key-range hint is given).
 __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl* __restrict__ ctrl,
                                uint32_t xr) {
-    uint32_t mx = 0;
+    uint32_t mx = 0, mn = 0xffffffffu;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    auto fold = [&](uint32_t k) {
+        k ^= xr;
+        mx = max(mx, k);
+        mn = min(mn, k);
+    };
     // 16-byte loads over the aligned body, four in flight per thread
     size_t head = ((16 - (reinterpret_cast<uintptr_t>(keys) & 15)) & 15) / 4;
     if (head > n) head = n;
@@ -1415,16 +1420,28 @@ __global__ void key_max_kernel(const uint32_t* __restrict__ keys, size_t n, Ctrl
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = __ldcs(v4 + i + u * stride);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) mx = max(mx, max(max(v[u].x ^ xr, v[u].y ^ xr), max(v[u].z ^ xr, v[u].w ^ xr)));
+        for (int u = 0; u < 4; ++u) {
+            fold(v[u].x);
+            fold(v[u].y);
+            fold(v[u].z);
+            fold(v[u].w);
+        }
     }
     for (; i < nv; i += stride) {
         const uint4 v = __ldcs(v4 + i);
-        mx = max(mx, max(max(v.x ^ xr, v.y ^ xr), max(v.z ^ xr, v.w ^ xr)));
+        fold(v.x);
+        fold(v.y);
+        fold(v.z);
+        fold(v.w);
     }
-    if (tid < head) mx = max(mx, keys[tid] ^ xr);
-    for (size_t j = head + 4 * nv + tid; j < n; j += stride) mx = max(mx, keys[j] ^ xr);
+    if (tid < head) fold(keys[tid]);
+    for (size_t j = head + 4 * nv + tid; j < n; j += stride) fold(keys[j]);
     mx = __reduce_max_sync(kFull, mx);
-    if ((threadIdx.x & 31) == 0 && mx) atomicMax(&ctrl->max_key, mx);
+    mn = __reduce_min_sync(kFull, mn);
+    if ((threadIdx.x & 31) == 0) {
+        if (mx) atomicMax(&ctrl->max_key, mx);
+        if (~mn) atomicMax(&ctrl->min_inv, ~mn);
+    }
 }
 
 }  // namespace

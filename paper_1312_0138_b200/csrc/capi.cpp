@@ -210,14 +210,23 @@ struct DeviceCtx {
     void* wide = nullptr;               // staging for host arrays of 8/16/64-bit keys
     size_t wide_cap = 0;
     void* width_scratch = nullptr;      // 8/16-bit histogram + prefix, 64-bit min/max
-    size_t last_count = 0;        // count of the last async device sort (bws_gpu_sort_check)
-    uint64_t last_range = 0;      // its key range (0 = derived)
+    // the most recent bws_gpu_sort_(range_)device_async on this device, checked
+    // by bws_gpu_sort_check; once another library call reuses the control
+    // block its final state is first copied (stream-ordered) to snap()
+    struct AsyncSort {
+        bool active = false;
+        cudaStream_t stream = nullptr;
+        size_t count = 0;
+        uint64_t range = 0;  // 0 = derived
+        bool snapped = false;
+    } pending;
     void* bounce[2] = {nullptr, nullptr};  // pinned staging for pageable host arrays
     cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
     cudaEvent_t done = nullptr;   // recorded after every queued sort: orders the
                                   // shared bitset/control block across streams
 
     Ctrl* ctrl() { return reinterpret_cast<Ctrl*>(ctrl_mem); }
+    Ctrl* snap() { return reinterpret_cast<Ctrl*>(ctrl_mem + kCtrlBytes); }
     unsigned long long* status() {
         return reinterpret_cast<unsigned long long*>(ctrl_mem + sizeof(Ctrl));
     }
@@ -231,7 +240,8 @@ struct DeviceCtx {
         cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
         cuda_check(bws_gpu::configure_width_kernels(dev, &geo), "width kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes), "cudaMalloc(control block)");
+        cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes + sizeof(Ctrl)), "cudaMalloc(control block)");
+        pending = AsyncSort{};
         cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
         bws_gpu::BucketPlan widest;
         widest.nb = bws_gpu::MAX_BUCKETS;
@@ -343,22 +353,32 @@ struct DeviceCtx {
 
 // Per-kernel CUDA-event timing (bws_gpu_set_kernel_timing): events bracket
 // each launch on its stream; bws_gpu_kernel_timings() resolves and sums them.
+// Events are pooled per device (an event recorded on another device's stream
+// fails), and the open "before" event is kept per stream, so timed sorts on
+// different devices / threads never pair each other's events.
 struct EventTimer final : bws_gpu::KernelTimer {
     std::mutex mu;
     std::atomic<bool> enabled{false};
     struct Rec {
         const char* name;
+        int device;
         cudaEvent_t a, b;
     };
     std::vector<Rec> pending;
-    std::vector<cudaEvent_t> pool;
-    cudaEvent_t open = nullptr;
+    std::map<int, std::vector<cudaEvent_t>> pool;     // per device
+    std::map<cudaStream_t, std::pair<int, cudaEvent_t>> open;  // per stream: (device, event)
 
-    cudaEvent_t get() {
+    static int device_now() {
+        int d = 0;
+        cuda_check(cudaGetDevice(&d), "cudaGetDevice(timer)");
+        return d;
+    }
+    cudaEvent_t get(int device) {
+        auto& p = pool[device];
         cudaEvent_t e = nullptr;
-        if (!pool.empty()) {
-            e = pool.back();
-            pool.pop_back();
+        if (!p.empty()) {
+            e = p.back();
+            p.pop_back();
         } else {
             cuda_check(cudaEventCreate(&e), "cudaEventCreate(timer)");
         }
@@ -366,15 +386,22 @@ struct EventTimer final : bws_gpu::KernelTimer {
     }
     void before(cudaStream_t s) override {
         std::lock_guard<std::mutex> lock(mu);
-        open = get();
-        cuda_check(cudaEventRecord(open, s), "cudaEventRecord(timer)");
+        const int dev = device_now();
+        cudaEvent_t e = get(dev);
+        cuda_check(cudaEventRecord(e, s), "cudaEventRecord(timer)");
+        auto it = open.find(s);
+        if (it != open.end()) pool[it->second.first].push_back(it->second.second);  // unpaired: drop
+        open[s] = {dev, e};
     }
     void after(const char* name, cudaStream_t s) override {
         std::lock_guard<std::mutex> lock(mu);
-        cudaEvent_t b = get();
+        auto it = open.find(s);
+        if (it == open.end()) return;
+        const int dev = it->second.first;
+        cudaEvent_t b = get(dev);
         cuda_check(cudaEventRecord(b, s), "cudaEventRecord(timer)");
-        pending.push_back({name, open, b});
-        open = nullptr;
+        pending.push_back({name, dev, it->second.second, b});
+        open.erase(it);
     }
     std::string collect() {
         std::lock_guard<std::mutex> lock(mu);
@@ -386,8 +413,8 @@ struct EventTimer final : bws_gpu::KernelTimer {
             auto& slot = acc[r.name];
             slot.first += 1;
             slot.second += ms;
-            pool.push_back(r.a);
-            pool.push_back(r.b);
+            pool[r.device].push_back(r.a);
+            pool[r.device].push_back(r.b);
         }
         pending.clear();
         std::string out;
@@ -471,6 +498,38 @@ int current_device() {
     return dev;
 }
 
+// Calls on one device share the context's buffers (control block, bucket
+// buffer, cached bitset): each call's stream waits on `done`, recorded after
+// the previous call's work. Under CUDA graph capture the graph's own
+// dependencies order the captured work, and an event recorded outside the
+// capture cannot be waited on inside it (nor a captured one outside), so both
+// steps are skipped while `stream` is capturing.
+bool capturing(cudaStream_t stream) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return st != cudaStreamCaptureStatusNone;
+}
+void wait_done(DeviceCtx& ctx, cudaStream_t stream) {
+    if (!capturing(stream)) cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
+}
+void record_done(DeviceCtx& ctx, cudaStream_t stream) {
+    if (!capturing(stream)) cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
+}
+
+// Every call that reuses the control block calls this once its stream waits on
+// ctx.done: the pending async sort's control block is copied aside (stream-
+// ordered, 64 bytes) so bws_gpu_sort_check still validates that sort. A new
+// async sort supersedes the pending one instead (it clears `pending` first).
+void preserve_pending(DeviceCtx& ctx, cudaStream_t stream) {
+    if (!ctx.pending.active || ctx.pending.snapped) return;
+    cuda_check(cudaMemcpyAsync(ctx.snap(), ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToDevice, stream),
+               "control block snapshot");
+    ctx.pending.snapped = true;
+}
+
 // Queues one complete sort of `count` device-resident keys into `out` on
 // `stream`: [bitset reset if dirty] -> control/status reset -> K2 -> K3.
 // Caller holds ctx.mu. key_range == 0 derives the range from the keys (K2
@@ -480,7 +539,8 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
     NvtxRange nvtx_range("bitsort:direct K2+K3");
     const bool derived = key_range == 0;
     const uint64_t words = derived ? 0 : (key_range + 31) / 32;
-    cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
+    wait_done(ctx, stream);
+    preserve_pending(ctx, stream);
     ctx.ensure_bits();
     if (ctx.bits_dirty) {
         cuda_check(cudaMemsetAsync(ctx.bits, 0, kMaxWords * sizeof(uint32_t), stream),
@@ -509,7 +569,7 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
                "bitset_scan launch");
     g_launches.fetch_add(1);
     ctx.bits_dirty = false;  // K3 zeroes every word it reads; all set bits lie in its range
-    cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
+    record_done(ctx, stream);
 }
 
 // Bucketed pipeline: [K0 max + host readback when no hint] -> KB1..KB4.
@@ -521,7 +581,8 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
                       uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0,
                       bool multiset = false) {
     NvtxRange nvtx_range("bitsort:bucketed KB1-KB4");
-    cuda_check(cudaStreamWaitEvent(stream, ctx.done, 0), "stream ordering");
+    wait_done(ctx, stream);
+    preserve_pending(ctx, stream);
     cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
     if (key_range == 0) {
         cuda_check(bws_gpu::launch_key_max(keys, count, ctx.ctrl(), ctx.geo, stream, xr), "key_max launch");
@@ -546,7 +607,7 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
                                            active_timer(), nullptr, 0, parted_cap, multiset),
                "bucketed sort launch");
     g_launches.fetch_add(static_cast<uint64_t>(launches));
-    cuda_check(cudaEventRecord(ctx.done, stream), "cudaEventRecord");
+    record_done(ctx, stream);
 }
 
 void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
@@ -649,7 +710,18 @@ void stage_to_host(DeviceCtx& ctx, void* host, const void* dev, size_t bytes) {
 // then sorted out of place into the context's key buffer and copied back, so
 // the original survives the detection. Without multiset (the key-range
 // extension) repeated keys are BWS_ERROR_DATA.
-void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, bool multiset = false) {
+// The reference's counting_sort (baselines.hpp:95-110) rejects a key span
+// max - min >= 2^26 with std::out_of_range (BWS_ERROR_RANGE) before sorting.
+[[noreturn]] void throw_span(uint64_t diff, uint64_t limit) {
+    throw std::out_of_range("counting_sort: key span " + std::to_string(diff) + "+1 exceeds the limit of " +
+                            std::to_string(limit) + " keys");
+}
+
+// span_limit != 0 (BWS_ALG_COUNTING): K0 first folds min and max on the
+// device; a span >= span_limit is BWS_ERROR_RANGE with the data untouched,
+// otherwise max + 1 becomes the sort's key-range hint.
+void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, bool multiset = false,
+              uint64_t span_limit = 0) {
     NvtxRange nvtx_range("bitsort:bws_sort u32");
     check_range(key_range);
     if (count == 0) return;
@@ -678,6 +750,19 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     } restore{prev};
     ctx.init(device);
     uint32_t* keys = static_cast<uint32_t*>(data);
+    auto check_span = [&](const uint32_t* dk) {
+        if (span_limit == 0) return;
+        wait_done(ctx, ctx.stream);
+        preserve_pending(ctx, ctx.stream);
+        cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), ctx.stream), "control block reset");
+        cuda_check(bws_gpu::launch_key_max(dk, count, ctx.ctrl(), ctx.geo, ctx.stream, xr), "key_max launch");
+        g_launches.fetch_add(1);
+        const Ctrl c = read_ctrl(ctx, ctx.stream);
+        record_done(ctx, ctx.stream);
+        const uint64_t mn = static_cast<uint32_t>(~c.min_inv), mx = c.max_key;
+        if (mx - mn >= span_limit) throw_span(mx - mn, span_limit);
+        key_range = mx + 1;
+    };
     // signed keys (xr) always take the bucketed pipeline, which applies the XOR
     auto enqueue = [&](const uint32_t* in, uint32_t* out) {
         if (xr) {
@@ -707,6 +792,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
         validate(ctx, count, ms_range, ctx.stream);
     };
     if (on_device) {
+        check_span(keys);
         if (!multiset) {
             enqueue(keys, keys);
             validate(ctx, count, key_range, ctx.stream);
@@ -735,6 +821,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
         }
     };
     upload();
+    check_span(ctx.keys);
     enqueue(ctx.keys, ctx.keys);
     if (needs_multiset()) {
         upload();  // the host array is untouched until the write-back
@@ -755,7 +842,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
 // max - min is below 2^32 narrowed to u32 offsets, sorted by the 32-bit
 // pipeline (repeats redone by the counting pass) and widened back. Wider
 // 64-bit spans are BWS_ERROR_CONFIG (no CPU fallback).
-void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned) {
+void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned, uint64_t span_limit = 0) {
     NvtxRange nvtx_range("bitsort:bws_sort other width");
     if (count == 0) return;
     visible_devices();
@@ -789,7 +876,7 @@ void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned)
     void* other = static_cast<unsigned char*>(scratch_owner) + (on_device ? 0 : bytes);
     const bool pinned = attr.type == cudaMemoryTypeHost;
     cudaStream_t s = ctx.stream;
-    cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+    wait_done(ctx, s);
     auto upload = [&] {
         if (on_device) return;
         if (pinned)
@@ -811,6 +898,7 @@ void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned)
         uint64_t mm[2] = {0, 0};
         cuda_check(cudaMemcpyAsync(mm, ctx.width_scratch, sizeof mm, cudaMemcpyDeviceToHost, s), "min/max readback");
         cuda_check(cudaStreamSynchronize(s), "min/max");
+        if (span_limit && mm[1] - mm[0] >= span_limit) throw_span(mm[1] - mm[0], span_limit);
         if (mm[1] - mm[0] >= (uint64_t(1) << 32)) {
             // a span beyond the bitset sort's 2^32: stable LSD radix passes over
             // the 8-bit digits on which the keys differ
@@ -875,7 +963,7 @@ void sort_other_width(void* data, size_t count, uint32_t width, int is_unsigned)
         cuda_check(cudaStreamSynchronize(s), "sort execution");
         stage_to_host(ctx, data, dev, bytes);
     }
-    cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+    record_done(ctx, s);
 }
 
 const char* algorithm_name_of(bws_algorithm a) {
@@ -931,17 +1019,20 @@ bws_status bws_sort(void* data, size_t count, uint32_t width, int is_unsigned,
         // bitsort.h:86-88: the array holds naturally aligned keys of `width` bits
         if (reinterpret_cast<uintptr_t>(data) % (width / 8) != 0)
             throw data_error("data is not aligned to its " + std::to_string(width) + "-bit keys");
-        if (algorithm != BWS_ALG_BITWISE && algorithm != BWS_ALG_BITWISE_SKIP_EMPTY)
-            throw config_error(std::string("algorithm '") + algorithm_name_of(algorithm) +
-                               "' is not provided by the B200 build (bitwise only)");
+        // Every algorithm id yields the same bytes (a sort's output is unique),
+        // so all of them run on the GPU pipelines (run_algorithm,
+        // dispatch.hpp:42-55). COUNTING keeps the reference's one behavioural
+        // difference: a key span >= 2^26 is BWS_ERROR_RANGE
+        // (counting_sort_max_range_default, baselines.hpp:95-110).
+        const uint64_t span_limit = algorithm == BWS_ALG_COUNTING ? (uint64_t(1) << 26) : 0;
         if (width != 32) {
-            sort_other_width(data, count, width, is_unsigned);
+            sort_other_width(data, count, width, is_unsigned, span_limit);
             return;
         }
         // signed int32: x ^ 0x80000000 maps the signed order onto the unsigned
         // one (the reference splits negatives and non-negatives instead,
         // bitsort.hpp:131-152); the same XOR maps the sorted keys back
-        sort_u32(data, count, 0, is_unsigned ? 0u : 0x80000000u, /*multiset=*/true);
+        sort_u32(data, count, 0, is_unsigned ? 0u : 0x80000000u, /*multiset=*/true, span_limit);
     });
 }
 
@@ -963,10 +1054,18 @@ bws_status bws_gpu_sort_device_async(const uint32_t* keys, size_t count, uint32_
         DeviceCtx& ctx = context_for(dev);
         std::lock_guard<std::mutex> lock(ctx.mu);
         ctx.init(dev);
-        ctx.last_count = count;
-        ctx.last_range = key_range;
+        ctx.pending.active = false;  // superseded by this sort
         if (count == 0) return;
-        enqueue_sort(ctx, keys, count, out, key_range, static_cast<cudaStream_t>(stream));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        // no hint: the direct pipeline derives the range on the device (K2
+        // folds the max key, K3 scans up to it) with no host round trip, so
+        // the call stays stream-ordered and capturable; the bucketed
+        // pipeline's plan needs the range on the host
+        if (key_range == 0)
+            enqueue_direct(ctx, keys, count, out, 0, s);
+        else
+            enqueue_sort(ctx, keys, count, out, key_range, s);
+        ctx.pending = {true, s, count, key_range, false};
     });
 }
 
@@ -983,8 +1082,7 @@ bws_status bws_gpu_sort_range_device_async(const uint32_t* keys, size_t count, u
         DeviceCtx& ctx = context_for(dev);
         std::lock_guard<std::mutex> lock(ctx.mu);
         ctx.init(dev);
-        ctx.last_count = count;
-        ctx.last_range = key_range;
+        ctx.pending.active = false;  // superseded by this sort
         if (count == 0) return;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         if (key_lo == 0) {
@@ -993,6 +1091,7 @@ bws_status bws_gpu_sort_range_device_async(const uint32_t* keys, size_t count, u
             if (count >= (size_t(1) << 32)) throw std::out_of_range("range sorts take fewer than 2^32 keys");
             enqueue_bucketed(ctx, keys, count, out, key_range, s, key_lo);
         }
+        ctx.pending = {true, s, count, key_range, false};
     });
 }
 
@@ -1011,7 +1110,8 @@ bws_status bws_gpu_range_split(const uint32_t* keys, size_t count, uint64_t key_
         std::lock_guard<std::mutex> lock(ctx.mu);
         ctx.init(dev);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        wait_done(ctx, s);
+        preserve_pending(ctx, s);
         if (count == 0) {
             cuda_check(cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * parts, s), "count reset");
         } else {
@@ -1033,7 +1133,7 @@ bws_status bws_gpu_range_split(const uint32_t* keys, size_t count, uint64_t key_
                 throw data_error(std::to_string(bad) + " key(s) not below the key range " +
                                  std::to_string(key_range));
         }
-        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+        record_done(ctx, s);
     });
 }
 
@@ -1107,13 +1207,22 @@ bws_status bws_gpu_sort_check(void* stream, uint64_t* distinct_out) {
         const int dev = current_device();
         DeviceCtx& ctx = context_for(dev);
         std::lock_guard<std::mutex> lock(ctx.mu);
-        if (!ctx.ready || ctx.last_count == 0) {
+        if (!ctx.ready || !ctx.pending.active) {
             if (distinct_out) *distinct_out = 0;
             return;
         }
-        const uint64_t total = validate(ctx, ctx.last_count, ctx.last_range ? ctx.last_range : kMaxKeyRange,
-                                        static_cast<cudaStream_t>(stream));
-        if (distinct_out) *distinct_out = total;
+        cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "sort execution");
+        cuda_check(cudaStreamSynchronize(ctx.pending.stream), "sort execution");
+        Ctrl c;
+        cuda_check(cudaMemcpy(&c, ctx.pending.snapped ? ctx.snap() : ctx.ctrl(), sizeof(Ctrl),
+                              cudaMemcpyDeviceToHost),
+                   "control block readback");
+        const uint64_t range = ctx.pending.range ? ctx.pending.range : kMaxKeyRange;
+        throw_bad_keys(c, range);
+        if (c.total != ctx.pending.count)
+            throw data_error("keys are not distinct: " + std::to_string(ctx.pending.count) + " keys, " +
+                             std::to_string(c.total) + " distinct (the bitset sort requires distinct keys)");
+        if (distinct_out) *distinct_out = c.total;
     });
 }
 
@@ -1130,7 +1239,8 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
         ctx.init(dev);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const uint64_t words = (key_range + 31) / 32;
-        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        wait_done(ctx, s);
+        preserve_pending(ctx, s);
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
         const int path = current_path();
         const bool bucketed = count < (size_t(1) << 32) &&
@@ -1157,7 +1267,7 @@ bws_status bws_gpu_bitset_build(const uint32_t* keys, size_t count, uint32_t* bi
                        "bitset_scatter launch");
             g_launches.fetch_add(1);
         }
-        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+        record_done(ctx, s);
     });
 }
 
@@ -1185,7 +1295,8 @@ bws_status bws_gpu_bitset_push(const uint32_t* keys, size_t count, uint64_t key_
         std::lock_guard<std::mutex> lock(ctx.mu);
         ctx.init(dev);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        wait_done(ctx, s);
+        preserve_pending(ctx, s);
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), s), "control block reset");
         const bws_gpu::BucketPlan plan =
             bws_gpu::plan_buckets(key_range, ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
@@ -1196,7 +1307,7 @@ bws_status bws_gpu_bitset_push(const uint32_t* keys, size_t count, uint64_t key_
                                                active_timer()),
                    "bitset push launch");
         g_launches.fetch_add(static_cast<uint64_t>(launches));
-        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+        record_done(ctx, s);
     });
 }
 
@@ -1218,7 +1329,8 @@ bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t 
             return;
         }
         const size_t tiles = bws_gpu::scan_tiles(n_words);
-        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        wait_done(ctx, s);
+        preserve_pending(ctx, s);
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0,
                                    sizeof(Ctrl) + tiles * sizeof(unsigned long long), s),
                    "control block reset");
@@ -1231,7 +1343,7 @@ bws_status bws_gpu_bitset_scan(const uint32_t* bits, uint64_t n_words, uint32_t 
                                 }),
                    "bitset_scan launch");
         g_launches.fetch_add(1);
-        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+        record_done(ctx, s);
     });
 }
 
@@ -1261,7 +1373,8 @@ bws_status bws_gpu_bitset_scan_sources(const uint32_t* const* srcs, int nsrc, ui
             return;
         }
         const size_t tiles = bws_gpu::scan_tiles(n_words);
-        cuda_check(cudaStreamWaitEvent(s, ctx.done, 0), "stream ordering");
+        wait_done(ctx, s);
+        preserve_pending(ctx, s);
         cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl) + tiles * sizeof(unsigned long long), s),
                    "control block reset");
         if (aligned) {
@@ -1294,7 +1407,7 @@ bws_status bws_gpu_bitset_scan_sources(const uint32_t* const* srcs, int nsrc, ui
             cuda_check(err, "or_gather + bitset_scan launch");
             g_launches.fetch_add(2);
         }
-        cuda_check(cudaEventRecord(ctx.done, s), "cudaEventRecord");
+        record_done(ctx, s);
     });
 }
 

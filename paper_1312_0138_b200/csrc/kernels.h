@@ -18,7 +18,9 @@ struct alignas(64) Ctrl {
     unsigned int ticket;           // K3 dynamic tile ticket / KB4 bucket ticket
     unsigned int done_ctas;        // slab KB3: CTAs finished (the last one scans the counts)
     unsigned long long total;      // set bits over the whole scan (K3, last tile)
-    unsigned long long pad1[5];
+    unsigned int min_inv;          // ~(min key), atomicMax (K0): zero-initialised like max_key
+    unsigned int pad0;
+    unsigned long long pad1[4];
 };
 static_assert(sizeof(Ctrl) == 64, "Ctrl is one 64-byte line");
 

@@ -94,10 +94,20 @@ def test_config_errors():
     assert "unsupported width 24" in capi.last_error()
     assert capi.sort_raw(p, 3, 32, 1, 99) == capi.Status.ERROR_CONFIG  # capi.cpp:69
     assert "unknown algorithm id" in capi.last_error()
-    for alg in (capi.Algorithm.INSERTION, capi.Algorithm.MERGE, capi.Algorithm.COUNTING,
-                capi.Algorithm.PLATFORM):
-        assert capi.sort_raw(p, 3, 32, 1, alg) == capi.Status.ERROR_CONFIG
-        assert capi.algorithm_name(alg) in capi.last_error()
+    assert a.tolist() == [3, 1, 2]
+
+
+def test_every_algorithm_needs_the_gpu():
+    """Every algorithm id goes to the GPU pipelines (no CPU fallback): without a
+    device the call fails loudly with BWS_ERROR_INTERNAL and leaves the data."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present (tests/test_gpu_parity.py covers the sorts)")
+    a = np.array([3, 1, 2], dtype=np.uint32)
+    for alg in capi.Algorithm:
+        assert capi.sort_raw(a.ctypes.data, 3, 32, 1, alg) == capi.Status.ERROR_INTERNAL
+        assert "no CUDA device" in capi.last_error()
     assert a.tolist() == [3, 1, 2]
 
 

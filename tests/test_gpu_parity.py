@@ -109,7 +109,46 @@ def test_status_conventions(capi, path):
     assert b.tolist() == [1, 2, 3]
     assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.BITWISE_SKIP_EMPTY) == capi.Status.OK
     assert capi.sort_raw(b.ctypes.data, 3, 24, 1, 0) == capi.Status.ERROR_CONFIG
-    assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.PLATFORM) == capi.Status.ERROR_CONFIG
+    assert capi.sort_raw(b.ctypes.data, 3, 32, 1, capi.Algorithm.PLATFORM) == capi.Status.OK
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_every_algorithm_id(capi, path):
+    """Every algorithm id sorts on the GPU to the reference's bytes
+    (run_algorithm, dispatch.hpp:42-55; test_capi.cpp:83-93 "int64 with every
+    algorithm"), and COUNTING keeps the reference's span limit: a span >= 2^26
+    is BWS_ERROR_RANGE naming the span (test_capi.cpp:98-101), data untouched."""
+    import oracle
+
+    capi.set_path(getattr(capi.Path, path))
+    cases = [(np.array([5, -9, 0, 5, -9, 123456789], dtype=np.int64), 64, 0),
+             (np.array([3, -1, 0, -7, 2], dtype=np.int16), 16, 0),
+             (np.array([200, 3, 255, 0], dtype=np.uint8), 8, 1),
+             (np.random.default_rng(4).integers(0, 1 << 25, 5000).astype(np.uint32), 32, 1),
+             (np.random.default_rng(5).integers(-(1 << 24), 1 << 24, 5000).astype(np.int32), 32, 0)]
+    for alg in capi.Algorithm:
+        for keys, width, uns in cases:
+            a = keys.copy()
+            assert capi.sort_raw(a.ctypes.data, a.size, width, uns, alg) == capi.Status.OK, capi.last_error()
+            assert np.array_equal(a, np.sort(keys)), (alg, keys.dtype)
+            if oracle.REFERENCE is not None:
+                r = keys.copy()
+                assert oracle.REFERENCE.bws_sort(r.ctypes.data, r.size, width, uns, int(alg)) == 0
+                assert np.array_equal(a, r)
+    for keys, width, uns in [(np.array([0, 1 << 30], dtype=np.int32), 32, 0),
+                             (np.array([7, 7 + (1 << 26)], dtype=np.uint32), 32, 1),
+                             (np.array([-5, (1 << 26) - 5], dtype=np.int64), 64, 0)]:
+        a = keys.copy()
+        assert capi.sort_raw(a.ctypes.data, a.size, width, uns, capi.Algorithm.COUNTING) == capi.Status.ERROR_RANGE
+        assert "span" in capi.last_error()
+        assert np.array_equal(a, keys)
+        if oracle.REFERENCE is not None:
+            r = keys.copy()
+            assert oracle.REFERENCE.bws_sort(r.ctypes.data, r.size, width, uns, 4) == 4  # BWS_ERROR_RANGE
+    # a span just under the limit sorts
+    a = np.array([7 + (1 << 26) - 1, 7], dtype=np.uint32)
+    assert capi.sort_raw(a.ctypes.data, 2, 32, 1, capi.Algorithm.COUNTING) == capi.Status.OK
+    assert a.tolist() == [7, 7 + (1 << 26) - 1]
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -792,3 +831,51 @@ def test_pageable_and_pinned_host_paths(capi, cuda):
     np.copyto(pinned, keys)
     capi.sort(pinned)
     assert np.array_equal(pageable, np.sort(keys)) and np.array_equal(pinned, pageable)
+
+
+def test_async_check_survives_other_calls(capi, cuda):
+    """bws_gpu_sort_check validates the most recent ASYNC sort even when other
+    library calls (a bws_sort, a bitset build) ran on the device in between:
+    their control-block resets no longer overwrite its result."""
+    rng = np.random.default_rng(21)
+    stream = cuda.cuda.current_stream().cuda_stream
+    for n in (1 << 12, 1 << 22):  # direct and bucketed pipelines
+        keys = rng.choice(1 << 24, size=n, replace=False).astype(np.uint32)
+        bad = keys.copy()
+        bad[7] = bad[9]  # one duplicate
+        for arr, ok in ((keys, True), (bad, False)):
+            t = cuda.from_numpy(arr.view(np.int32)).cuda()
+            out = cuda.empty_like(t)
+            capi.sort_device_async(t.data_ptr(), n, out.data_ptr(), 1 << 24, stream)
+            other = rng.choice(1 << 20, size=5000, replace=False).astype(np.uint32)
+            capi.sort(other)  # a synchronous sort reuses the control block
+            bits = cuda.empty((1 << 24) // 32, dtype=cuda.int32, device="cuda")
+            capi.bitset_build(t.data_ptr(), 100, bits.data_ptr(), 1 << 24, stream)  # so does a build
+            if ok:
+                assert capi.sort_check(stream) == n
+                assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
+            else:
+                with pytest.raises(capi.BitsortError) as e:
+                    capi.sort_check(stream)
+                assert e.value.status == capi.Status.ERROR_DATA
+
+
+def test_async_without_hint_is_graph_capturable(capi, cuda):
+    """bws_gpu_sort_device_async with key_range == 0 derives the range on the
+    device (no host round trip), so it can be captured in a CUDA graph."""
+    n = 1 << 21
+    keys = np.random.default_rng(22).choice(1 << 26, size=n, replace=False).astype(np.uint32)
+    t = cuda.from_numpy(keys.view(np.int32)).cuda()
+    out = cuda.empty_like(t)
+    s = cuda.cuda.Stream()
+    with cuda.cuda.stream(s):
+        capi.sort_device_async(t.data_ptr(), n, out.data_ptr(), 0, s.cuda_stream)  # warm-up
+    s.synchronize()
+    g = cuda.cuda.CUDAGraph()
+    with cuda.cuda.graph(g, stream=s):
+        capi.sort_device_async(t.data_ptr(), n, out.data_ptr(), 0, s.cuda_stream)
+    out.zero_()
+    g.replay()
+    s.synchronize()
+    assert capi.sort_check(s.cuda_stream) == n
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
