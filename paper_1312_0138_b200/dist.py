@@ -11,6 +11,14 @@ Rank r of G holds an input-position shard of the keys. Each rank
      so the total only drops) -> BWS_ERROR_DATA.
 The global sorted array is the rank-order concatenation of the local outputs.
 
+The p2p and push variants below are EXPERIMENTAL and opt-in (bench.py --p2p /
+--push): their cross-GPU memory ordering has only run with 2-3 processes
+sharing one GPU, never across NVLink peers. They fence with a host-side
+device synchronisation (every local kernel that wrote peer memory, or whose
+memory peers read, has completed) followed by a collective, rather than with
+the collective alone. ``distributed_sort`` (NCCL reduce-scatter) is the
+default.
+
 Peer-to-peer variant (``distributed_sort_p2p``, NVLink/NVSwitch node): steps 2
 and 3 become ONE kernel instead of NCCL + scan — every rank exports its full
 bitset through CUDA IPC, and after a cross-rank barrier scans its own slice of
@@ -279,6 +287,13 @@ def distributed_sort(keys: torch.Tensor, key_range: int, n_total: Optional[int] 
                        key_lo=key_lo, key_hi=key_hi)
 
 
+def _device_sync(dev: torch.device) -> None:
+    """Host-side completion of every kernel queued on this rank's device (a
+    no-op for the CPU tensors of the gloo tests)."""
+    if dev.type == "cuda":
+        torch.cuda.synchronize(dev)
+
+
 def _data_error(msg: str):
     from .capi import BitsortError, Status
 
@@ -365,13 +380,17 @@ def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[i
         dist.all_gather_object(handles, ops.export_bitset(bits), group=group)
         # the local bitset first: the fused scan copies it by TMA, peers by loads
         sources = [bits] + [ops.import_peer(r, h) for r, h in enumerate(handles) if r != rank]
-        # stream-ordered barrier: this rank's collective completes only after
-        # every rank's build (enqueued before its collective) has finished
+        # barrier: every rank's build has completed (host-side synchronisation,
+        # so its bitset writes are visible to the peers) before any rank
+        # enqueues the scan that reads the peers' bitsets
+        _device_sync(dev)
         fence = torch.zeros(1, dtype=torch.int32, device=dev)
         dist.all_reduce(fence, group=group)
+        _device_sync(dev)
     with nvtx.range("bitsort:p2p scan over peer bitsets"):
         out, count_t = ops.or_scan(sources, rank * per, per, key_lo, capacity)
     # the counts' all-gather doubles as the "peers are done reading" barrier
+    # (each rank's count is read back only after its scan has completed)
     counts = [torch.empty_like(count_t) for _ in range(world)]
     dist.all_gather(counts, count_t, group=group)
     counts_h = [int(c.item()) for c in counts]
@@ -409,13 +428,19 @@ def distributed_sort_push(keys: torch.Tensor, key_range: int, n_total: Optional[
         handles = [None] * world
         dist.all_gather_object(handles, ops.export_slice(own), group=group)
         targets = [own if r == rank else ops.import_slice(r, h) for r, h in enumerate(handles)]
-        # every slice is zeroed (stream-ordered before this collective) before anyone pushes
+        # every slice is zeroed (completed, host-synchronised) before anyone pushes
+        _device_sync(dev)
         dist.all_reduce(fence, group=group)
+        _device_sync(dev)
     if keys.numel():
         with nvtx.range("bitsort:push build into owners' slices"):
             ops.bitset_push(keys, key_range, targets, per)
     if world > 1:
-        dist.all_reduce(fence, group=group)  # every rank's pushes have landed
+        # every rank's pushes have completed (host-synchronised: the bulk ORs
+        # into the peers' slices are done) before any owner scans its slice
+        _device_sync(dev)
+        dist.all_reduce(fence, group=group)
+        _device_sync(dev)
 
     key_lo = rank * per * 32
     key_hi = min((rank + 1) * per * 32, key_range)
