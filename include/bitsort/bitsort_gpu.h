@@ -158,6 +158,27 @@ BITSORT_API uint64_t bws_gpu_launch_count(void);
 BITSORT_API bws_status bws_gpu_set_kernel_timing(int enable);
 BITSORT_API bws_status bws_gpu_kernel_timings(char* buf, size_t buf_size);
 
+/* Multi-GPU bws_sort in one process: with G > 1 devices,
+ * bws_sort / bws_sort_u32_range on a HOST array of unsigned 32-bit keys
+ * (>= 2^20 keys, env BITSORT_MULTI_MIN_KEYS) shards the array over the G
+ * devices (each shard over its own PCIe link), builds a full bitset per
+ * device, combines them (NCCL reduce-scatter with ncclSum on uint32 words when
+ * the devices are distinct and libnccl.so.2 loads, else — or with env
+ * BITSORT_EXCHANGE=p2p — a fused scan reading every device's bitset slice over
+ * peer access), scans one key-range slice per device and writes every slice
+ * back at its offset. Repeated keys take the single-GPU counting pass. Other
+ * widths, signed keys and device arrays run on one GPU.
+ *   bws_gpu_set_device_count(G): devices 0 .. G-1 (1 = single GPU; default:
+ *       env BITSORT_GPUS, else 1);
+ *   bws_gpu_set_devices(list, G): an explicit list (env BITSORT_DEVICES,
+ *       e.g. "0,1,2,3"); a device may appear more than once (logical ranks
+ *       sharing a GPU: the P2P exchange; used by the tests on one GPU);
+ *   bws_gpu_device_count(): the current G.
+ * At most 8 logical ranks. BWS_ERROR_CONFIG for an invisible device. */
+BITSORT_API bws_status bws_gpu_set_device_count(int count);
+BITSORT_API bws_status bws_gpu_set_devices(const int* devices, int count);
+BITSORT_API int bws_gpu_device_count(void);
+
 /* Releases cached device buffers, streams and communicators. */
 BITSORT_API void bws_gpu_shutdown(void);
 

@@ -102,6 +102,9 @@ def _load() -> ctypes.CDLL:
         "bws_gpu_launch_count": (u64, []),
         "bws_gpu_set_kernel_timing": (i32, [i32]),
         "bws_gpu_kernel_timings": (i32, [ctypes.c_char_p, sz]),
+        "bws_gpu_set_device_count": (i32, [i32]),
+        "bws_gpu_set_devices": (i32, [ctypes.POINTER(i32), i32]),
+        "bws_gpu_device_count": (i32, []),
         "bws_gpu_shutdown": (None, []),
     }
     for name, (res, args) in sigs.items():
@@ -122,6 +125,7 @@ EXPORTED = (
     "bws_gpu_bitset_build", "bws_gpu_bitset_scan", "bws_gpu_set_scatter_mode", "bws_gpu_set_path",
     "bws_gpu_launch_count",
     "bws_gpu_set_kernel_timing", "bws_gpu_kernel_timings",
+    "bws_gpu_set_device_count", "bws_gpu_set_devices", "bws_gpu_device_count",
     "bws_gpu_shutdown",
 )
 
@@ -283,6 +287,22 @@ def kernel_timings() -> dict[str, tuple[int, float]]:
         name, cnt, ms = line.split()
         out[name] = (int(cnt), float(ms))
     return out
+
+
+def set_device_count(count: int) -> None:
+    """Multi-GPU bws_sort on devices 0 .. count-1 (1 = single GPU)."""
+    _check(lib.bws_gpu_set_device_count(int(count)))
+
+
+def set_devices(devices) -> None:
+    """Multi-GPU bws_sort on an explicit device list (a device may repeat:
+    logical ranks sharing a GPU)."""
+    arr = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+    _check(lib.bws_gpu_set_devices(arr, len(devices)))
+
+
+def device_count() -> int:
+    return int(lib.bws_gpu_device_count())
 
 
 def shutdown() -> None:

@@ -16,7 +16,9 @@
 // bucket buffer and scratch of the bucketed path, a key staging buffer and
 // pinned bounce buffers for host arrays, and an internal stream. Calls on one
 // device are serialised by the context mutex; calls on different devices run
-// concurrently. Multi-GPU sorting runs one process per GPU (dist.py).
+// concurrently. Multi-GPU: bws_sort on a host array runs on the devices set by
+// bws_gpu_set_device_count / BITSORT_GPUS in this one process (multi.cpp);
+// dist.py is the one-process-per-GPU alternative (torch.distributed).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -37,33 +39,12 @@
 
 #include "bitsort/bitsort.h"
 #include "bitsort/bitsort_gpu.h"
+#include "host_internal.h"
 #include "kernels.h"
 
-namespace {
-
-// NVTX range over a host-side phase (enqueue of a pipeline, staging copies,
-// entry points), visible in nsys / ncu timelines as "bitsort:<name>".
-struct NvtxRange {
-    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-    ~NvtxRange() { nvtxRangePop(); }
-    NvtxRange(const NvtxRange&) = delete;
-    NvtxRange& operator=(const NvtxRange&) = delete;
-};
-
-
-using bws_gpu::Ctrl;
+namespace bws_host {
 
 thread_local std::string g_last_error;
-
-struct config_error : std::invalid_argument {
-    using std::invalid_argument::invalid_argument;
-};
-struct data_error : std::invalid_argument {
-    using std::invalid_argument::invalid_argument;
-};
-struct internal_error : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
 
 template <class F>
 bws_status wrap(F&& body) {
@@ -89,23 +70,9 @@ bws_status wrap(F&& body) {
     }
 }
 
-void cuda_check(cudaError_t err, const char* what) {
-    if (err != cudaSuccess)
-        throw internal_error(std::string(what) + ": " + cudaGetErrorName(err) + " (" +
-                             cudaGetErrorString(err) + ")");
-}
-
-constexpr uint64_t kMaxKeyRange = 1ull << 32;
-constexpr uint64_t kMaxWords = kMaxKeyRange / 32;               // 2^27 words = 512 MiB
-constexpr size_t kMaxTiles = (kMaxWords + bws_gpu::SCAN_TILE_WORDS - 1) / bws_gpu::SCAN_TILE_WORDS;
-// Ctrl + tile status (v1: 8 B per 2048-word tile; the two-pass v2 scan keeps
-// offsets, tile counts and 16 segment counts per 8192-word tile there)
-constexpr size_t kCtrlBytes = sizeof(Ctrl) + 4 * kMaxTiles * sizeof(unsigned long long);
-
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_scatter_mode{bws_gpu::kAuto};
 std::atomic<int> g_path{-1};         // bws_path; -1 = not yet read from BITSORT_PATH
-constexpr size_t kBucketedMinKeys = size_t(1) << 21;
 
 int current_path() {
     int p = g_path.load();
@@ -191,165 +158,7 @@ CopyPool& copy_pool() {
     return pool;
 }
 
-constexpr size_t kStageChunk = size_t(16) << 20;  // bytes per pinned bounce buffer
-
-struct DeviceCtx {
-    std::mutex mu;
-    bool ready = false;
-    int device = -1;
-    bws_gpu::LaunchGeometry geo;
-    cudaStream_t stream = nullptr;
-    uint32_t* bits = nullptr;  // kMaxWords words; all-zero between sorts unless bits_dirty
-    bool bits_dirty = true;
-    unsigned char* ctrl_mem = nullptr;  // Ctrl followed by the K3 tile-status array
-    uint32_t* keys = nullptr;           // staging for host arrays
-    size_t keys_cap = 0;
-    uint32_t* parted = nullptr;         // bucketed path: keys grouped by bucket
-    size_t parted_cap = 0;
-    void* bucket_scratch = nullptr;     // bucketed path: histograms, totals, bases
-    void* wide = nullptr;               // staging for host arrays of 8/16/64-bit keys
-    size_t wide_cap = 0;
-    void* width_scratch = nullptr;      // 8/16-bit histogram + prefix, 64-bit min/max
-    // the most recent bws_gpu_sort_(range_)device_async on this device, checked
-    // by bws_gpu_sort_check; once another library call reuses the control
-    // block its final state is first copied (stream-ordered) to snap()
-    struct AsyncSort {
-        bool active = false;
-        cudaStream_t stream = nullptr;
-        size_t count = 0;
-        uint64_t range = 0;  // 0 = derived
-        bool snapped = false;
-    } pending;
-    void* bounce[2] = {nullptr, nullptr};  // pinned staging for pageable host arrays
-    cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
-    cudaEvent_t done = nullptr;   // recorded after every queued sort: orders the
-                                  // shared bitset/control block across streams
-
-    Ctrl* ctrl() { return reinterpret_cast<Ctrl*>(ctrl_mem); }
-    Ctrl* snap() { return reinterpret_cast<Ctrl*>(ctrl_mem + kCtrlBytes); }
-    unsigned long long* status() {
-        return reinterpret_cast<unsigned long long*>(ctrl_mem + sizeof(Ctrl));
-    }
-
-    void init(int dev) {
-        if (ready) return;
-        device = dev;
-        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-        cuda_check(bws_gpu::query_geometry(dev, &geo), "occupancy query");
-        cuda_check(bws_gpu::configure_bucket_kernels(dev, &geo), "bucket kernel configuration");
-        cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
-        cuda_check(bws_gpu::configure_width_kernels(dev, &geo), "width kernel configuration");
-        cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes + sizeof(Ctrl)), "cudaMalloc(control block)");
-        pending = AsyncSort{};
-        cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
-        bws_gpu::BucketPlan widest;
-        widest.nb = bws_gpu::MAX_BUCKETS;
-        const int max_shares = geo.part_blocks > geo.part_blocks_narrow ? geo.part_blocks : geo.part_blocks_narrow;
-        const size_t scratch_bytes = bws_gpu::bucket_scratch_bytes(widest, max_shares) + 64;
-        cuda_check(cudaMalloc(&bucket_scratch, scratch_bytes), "cudaMalloc(bucket scratch)");
-        // the slab fill counters must start at zero (KB3 re-zeroes them after each sort)
-        cuda_check(cudaMemset(bucket_scratch, 0, scratch_bytes), "bucket scratch clear");
-        bits_dirty = true;
-        ready = true;
-    }
-
-    // The direct path's 2^32-bit bitset (512 MiB), allocated on its first use
-    // (bucketed sorts never need it).
-    void ensure_bits() {
-        if (bits) return;
-        cuda_check(cudaMalloc(&bits, kMaxWords * sizeof(uint32_t)), "cudaMalloc(bitset 512 MiB)");
-        bits_dirty = true;
-    }
-
-    void ensure_keys(size_t n) {
-        if (n <= keys_cap) return;
-        if (keys) cuda_check(cudaFree(keys), "cudaFree(keys)");
-        keys = nullptr;
-        keys_cap = 0;
-        const size_t cap = n + n / 4;
-        cuda_check(cudaMalloc(&keys, cap * sizeof(uint32_t)), "cudaMalloc(key staging)");
-        keys_cap = cap;
-    }
-
-    // Bucket buffer for n keys under `plan`: the slab layout's slots when it
-    // applies (bws_gpu::slab_slots), else n. Returns the usable capacity.
-    size_t ensure_parted(size_t n, const bws_gpu::BucketPlan& plan) {
-        const size_t need = static_cast<size_t>(bws_gpu::slab_slots(plan, n)) > n
-                                ? static_cast<size_t>(bws_gpu::slab_slots(plan, n))
-                                : n;
-        if (need <= parted_cap) return parted_cap;
-        if (parted) cuda_check(cudaFree(parted), "cudaFree(parted)");
-        parted = nullptr;
-        parted_cap = 0;
-        const size_t cap = need + n / 8 + 64;  // KB4 bulk copies may read up to 12 bytes past a bucket
-        if (cudaMalloc(&parted, cap * sizeof(uint32_t)) != cudaSuccess) {
-            // the slab is an optimisation: fall back to the packed layout's n slots
-            cudaGetLastError();
-            const size_t packed = n + n / 8 + 64;
-            cuda_check(cudaMalloc(&parted, packed * sizeof(uint32_t)), "cudaMalloc(bucket keys)");
-            parted_cap = packed - 64;
-            return parted_cap;
-        }
-        parted_cap = cap - 64;
-        return parted_cap;
-    }
-
-    void* ensure_wide(size_t bytes) {
-        if (bytes > wide_cap) {
-            if (wide) cuda_check(cudaFree(wide), "cudaFree(wide keys)");
-            wide = nullptr;
-            wide_cap = 0;
-            cuda_check(cudaMalloc(&wide, bytes), "cudaMalloc(wide keys)");
-            wide_cap = bytes;
-        }
-        if (!width_scratch)
-            cuda_check(cudaMalloc(&width_scratch, bws_gpu::width_scratch_bytes()), "cudaMalloc(width scratch)");
-        return wide;
-    }
-
-    void ensure_bounce() {
-        if (bounce[0]) return;
-        for (int i = 0; i < 2; ++i) {
-            cuda_check(cudaHostAlloc(&bounce[i], kStageChunk, cudaHostAllocDefault), "cudaHostAlloc(staging)");
-            cuda_check(cudaEventCreateWithFlags(&bounce_ev[i], cudaEventDisableTiming), "cudaEventCreate");
-        }
-    }
-
-    void release() {
-        if (!ready) return;
-        cudaSetDevice(device);
-        if (stream) cudaStreamSynchronize(stream);
-        for (int i = 0; i < 2; ++i) {
-            if (bounce[i]) cudaFreeHost(bounce[i]);
-            if (bounce_ev[i]) cudaEventDestroy(bounce_ev[i]);
-            bounce[i] = nullptr;
-            bounce_ev[i] = nullptr;
-        }
-        if (bits) cudaFree(bits);
-        cudaFree(ctrl_mem);
-        if (keys) cudaFree(keys);
-        if (parted) cudaFree(parted);
-        if (bucket_scratch) cudaFree(bucket_scratch);
-        if (wide) cudaFree(wide);
-        if (width_scratch) cudaFree(width_scratch);
-        wide = nullptr;
-        wide_cap = 0;
-        width_scratch = nullptr;
-        parted = nullptr;
-        parted_cap = 0;
-        bucket_scratch = nullptr;
-        if (stream) cudaStreamDestroy(stream);
-        if (done) cudaEventDestroy(done);
-        done = nullptr;
-        bits = nullptr;
-        ctrl_mem = nullptr;
-        keys = nullptr;
-        keys_cap = 0;
-        stream = nullptr;
-        ready = false;
-    }
-};
+void copy_parallel(void* dst, const void* src, size_t bytes) { copy_pool().copy(dst, src, bytes); }
 
 // Per-kernel CUDA-event timing (bws_gpu_set_kernel_timing): events bracket
 // each launch on its stream; bws_gpu_kernel_timings() resolves and sums them.
@@ -458,16 +267,6 @@ cudaError_t launch_scan_any(const uint32_t* bits, uint64_t n_words, uint32_t key
         err = bws_gpu::launch_scan(bits, n_words, key_base, out, cap, ctrl, status, d_total, clear, geo, s);
     }
     g_launches.fetch_add(static_cast<uint64_t>(launches - 1));  // callers count one
-    return err;
-}
-
-// Brackets one direct-path launch with the timer when it is enabled.
-template <class F>
-cudaError_t timed_launch(const char* name, cudaStream_t s, F&& launch) {
-    bws_gpu::KernelTimer* t = active_timer();
-    if (t) t->before(s);
-    const cudaError_t err = launch();
-    if (t) t->after(name, s);
     return err;
 }
 
@@ -710,6 +509,13 @@ void stage_to_host(DeviceCtx& ctx, void* host, const void* dev, size_t bytes) {
 // then sorted out of place into the context's key buffer and copied back, so
 // the original survives the detection. Without multiset (the key-range
 // extension) repeated keys are BWS_ERROR_DATA.
+// Host arrays below this many keys stay on one GPU even when G > 1 devices
+// are configured (env BITSORT_MULTI_MIN_KEYS; tests lower it).
+size_t multi_min_keys() {
+    const char* e = std::getenv("BITSORT_MULTI_MIN_KEYS");
+    return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : (size_t(1) << 20);
+}
+
 // The reference's counting_sort (baselines.hpp:95-110) rejects a key span
 // max - min >= 2^26 with std::out_of_range (BWS_ERROR_RANGE) before sorting.
 [[noreturn]] void throw_span(uint64_t diff, uint64_t limit) {
@@ -808,6 +614,15 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
                    "device-to-device copy");
         cuda_check(cudaStreamSynchronize(ctx.stream), "device-to-device copy");
         return;
+    }
+    // a host array of unsigned keys on G > 1 configured devices: the
+    // single-process multi-GPU sort (multi.cpp); repeated keys come back
+    // untouched and take the single-GPU counting pass below
+    if (xr == 0 && span_limit == 0 && count >= multi_min_keys() && multi_rank_count() > 1) {
+        if (multi_sort_host(data, count, key_range)) return;
+        if (!multiset)
+            throw data_error("keys are not distinct: " + std::to_string(count) +
+                             " keys (the bitset sort requires distinct keys)");
     }
     ctx.ensure_keys(count);
     const size_t bytes = count * sizeof(uint32_t);
@@ -978,7 +793,9 @@ const char* algorithm_name_of(bws_algorithm a) {
     return "unknown";
 }
 
-}  // namespace
+}  // namespace bws_host
+
+using namespace bws_host;
 
 extern "C" {
 
@@ -1443,7 +1260,36 @@ bws_status bws_gpu_kernel_timings(char* buf, size_t buf_size) {
     });
 }
 
+bws_status bws_gpu_set_device_count(int count) {
+    return wrap([&] {
+        if (count < 1) throw config_error("device count must be >= 1");
+        std::vector<int> devs;
+        if (count > 1)
+            for (int i = 0; i < count; ++i) devs.push_back(i);
+        multi_set_devices(devs);
+    });
+}
+
+bws_status bws_gpu_set_devices(const int* devices, int count) {
+    return wrap([&] {
+        if (count < 1 || devices == nullptr) throw config_error("need at least one device");
+        std::vector<int> devs(devices, devices + count);
+        if (count == 1) devs.clear();  // one rank: the single-GPU path on the current device
+        multi_set_devices(devs);
+    });
+}
+
+int bws_gpu_device_count(void) {
+    try {
+        const int g = multi_rank_count();
+        return g < 1 ? 1 : g;
+    } catch (...) {
+        return 1;
+    }
+}
+
 void bws_gpu_shutdown(void) {
+    multi_release();
     for (auto& ctx : g_ctx) {
         std::lock_guard<std::mutex> lock(ctx.mu);
         ctx.release();

@@ -177,3 +177,12 @@ def test_no_cpu_fallback():
     assert capi.sort_raw(s.ctypes.data, 3, 32, 0, 0) == capi.Status.ERROR_INTERNAL
     assert "no CPU fallback" in capi.last_error()
     assert s.tolist() == [3, -1, 2]
+
+
+def test_device_count_configuration_errors():
+    """bws_gpu_set_device_count / bws_gpu_set_devices reject bad arguments with
+    BWS_ERROR_CONFIG before touching a device."""
+    assert capi.lib.bws_gpu_set_device_count(0) == capi.Status.ERROR_CONFIG
+    assert "device count" in capi.last_error()
+    assert capi.lib.bws_gpu_set_devices(None, 2) == capi.Status.ERROR_CONFIG
+    assert capi.device_count() == 1

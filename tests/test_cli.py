@@ -112,3 +112,20 @@ def test_sort_other_widths(tmp_path, width, signed):
     r = run(["sort", str(f), "--width", str(width)] + ([] if signed else ["--unsigned"]))
     assert r.returncode == 0, r.stderr
     assert [int(x) for x in r.stdout.split()] == sorted(keys)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["0,0", "0,0,0,0"])
+def test_sort_on_logical_ranks(tmp_path, devices):
+    """The unchanged CLI sorts on G devices when BITSORT_DEVICES lists them
+    (here G logical ranks sharing the one GPU): bws_sort's multi-GPU path."""
+    import os
+
+    rng = np.random.default_rng(17)
+    keys = rng.permutation(np.unique(rng.integers(0, 1 << 32, size=400_000, dtype=np.uint64)))
+    f = tmp_path / "in.txt"
+    f.write_text("\n".join(str(int(k)) for k in keys) + "\n")
+    env = dict(os.environ, BITSORT_DEVICES=devices, BITSORT_MULTI_MIN_KEYS="0")
+    r = subprocess.run([str(CLI), "sort", str(f), "--unsigned"], capture_output=True, text=True, env=env)
+    assert r.returncode == 0, r.stderr
+    assert [int(x) for x in r.stdout.split()] == sorted(int(k) for k in keys)
