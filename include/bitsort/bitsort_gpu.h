@@ -133,15 +133,21 @@ typedef enum bws_scatter_mode {
 BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
 
 /* Sort pipeline for bws_sort / bws_sort_u32_range / bws_gpu_sort_device_async
- * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed).
+ * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed|fused).
  *   DIRECT   : K2 global-bitset scatter + K3 decoupled-lookback scan
  *   BUCKETED : key-range bucketing (coalesced) + per-bucket SMEM bitset +
  *              fused extraction; no global bitset
- *   AUTO     : BUCKETED for n >= 2^21, DIRECT below */
+ *   FUSED    : one persistent kernel; the bitset of a pass split into per-SM
+ *              shared-memory slices, keys routed to their slice's SM through
+ *              L2-resident rings (key ranges up to ~2^28 on a 148-SM B200;
+ *              larger ranges take BUCKETED)
+ *   AUTO     : FUSED when the key range fits it, else BUCKETED for
+ *              n >= 2^21 and DIRECT below */
 typedef enum bws_path {
     BWS_PATH_AUTO = 0,
     BWS_PATH_DIRECT = 1,
-    BWS_PATH_BUCKETED = 2
+    BWS_PATH_BUCKETED = 2,
+    BWS_PATH_FUSED = 3
 } bws_path;
 BITSORT_API bws_status bws_gpu_set_path(bws_path path);
 

@@ -60,6 +60,7 @@ class Path(enum.IntEnum):
     AUTO = 0
     DIRECT = 1
     BUCKETED = 2
+    FUSED = 3
 
 
 class BitsortError(RuntimeError):

@@ -81,6 +81,7 @@ int current_path() {
     p = BWS_PATH_AUTO;
     if (env && std::strcmp(env, "direct") == 0) p = BWS_PATH_DIRECT;
     if (env && std::strcmp(env, "bucketed") == 0) p = BWS_PATH_BUCKETED;
+    if (env && std::strcmp(env, "fused") == 0) p = BWS_PATH_FUSED;
     g_path.store(p);
     return p;
 }
@@ -376,22 +377,32 @@ void enqueue_direct(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t
 // key_lo: keys lie in [key_lo, key_lo + key_range) (range sorts). xr: keys
 // are XORed with it on load and store (signed int32 sorts: 0x80000000).
 // multiset: repeated keys are sorted too (packed layout + KB4m counting sort).
-void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
-                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0,
-                      bool multiset = false) {
+// K0 + host readback: the key range (max key + 1) of a sort without a hint,
+// for the pipelines whose plan needs it on the host (bucketed, fused).
+uint64_t derive_range(DeviceCtx& ctx, const uint32_t* keys, size_t count, cudaStream_t stream, uint32_t xr) {
+    cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
+    cuda_check(bws_gpu::launch_key_max(keys, count, ctx.ctrl(), ctx.geo, stream, xr), "key_max launch");
+    g_launches.fetch_add(1);
+    unsigned int mx = 0;
+    cuda_check(cudaMemcpyAsync(&mx, &ctx.ctrl()->max_key, sizeof(mx), cudaMemcpyDeviceToHost, stream),
+               "max key readback");
+    cuda_check(cudaStreamSynchronize(stream), "key_max execution");
+    return static_cast<uint64_t>(mx) + 1;
+}
+
+// Bucketed pipeline: [K0 max + host readback when no hint] -> KB1..KB4.
+// Leaves the cached bitset untouched. Returns the key range it sorted with.
+// key_lo: keys lie in [key_lo, key_lo + key_range) (range sorts). xr: keys
+// are XORed with it on load and store (signed int32 sorts: 0x80000000).
+// multiset: repeated keys are sorted too (packed layout + KB4m counting sort).
+uint64_t enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
+                          uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0,
+                          bool multiset = false) {
     NvtxRange nvtx_range("bitsort:bucketed KB1-KB4");
     wait_done(ctx, stream);
     preserve_pending(ctx, stream);
+    if (key_range == 0) key_range = derive_range(ctx, keys, count, stream, xr);
     cuda_check(cudaMemsetAsync(ctx.ctrl_mem, 0, sizeof(Ctrl), stream), "control block reset");
-    if (key_range == 0) {
-        cuda_check(bws_gpu::launch_key_max(keys, count, ctx.ctrl(), ctx.geo, stream, xr), "key_max launch");
-        g_launches.fetch_add(1);
-        unsigned int mx = 0;
-        cuda_check(cudaMemcpyAsync(&mx, &ctx.ctrl()->max_key, sizeof(mx), cudaMemcpyDeviceToHost, stream),
-                   "max key readback");
-        cuda_check(cudaStreamSynchronize(stream), "key_max execution");
-        key_range = static_cast<uint64_t>(mx) + 1;
-    }
     // signed sorts keep power-of-two bucket widths (the output XOR then
     // commutes with the in-bucket offsets)
     bws_gpu::BucketPlan plan =
@@ -407,18 +418,68 @@ void enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
                "bucketed sort launch");
     g_launches.fetch_add(static_cast<uint64_t>(launches));
     record_done(ctx, stream);
+    return key_range;
 }
 
-void enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
-                  uint64_t key_range, cudaStream_t stream) {
+// KF: the single-launch fused sort (fused.cu) for key ranges whose bitset
+// fits in the SMs' shared memory in <= 2 passes. key_lo as enqueue_bucketed.
+bws_gpu::FusedPlan fused_plan(const DeviceCtx& ctx, uint64_t key_range, size_t count) {
+    if (ctx.geo.fused_ctas <= 0 || count >= (size_t(1) << 32) || key_range == 0) return {};
+    return bws_gpu::plan_fused(key_range, ctx.geo.fused_ctas, ctx.geo.fused_smem_limit);
+}
+
+void enqueue_fused(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out, uint64_t key_range,
+                   const bws_gpu::FusedPlan& plan, cudaStream_t stream, uint32_t key_lo = 0) {
+    NvtxRange nvtx_range("bitsort:fused KF");
+    wait_done(ctx, stream);
+    preserve_pending(ctx, stream);
+    ctx.ensure_fused(plan, stream);
+    bws_gpu::KeySplit ks;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
+    size_t n_head = ((16 - (addr & 15)) & 15) / 4;
+    if (n_head > count) n_head = count;
+    ks.nv = (count - n_head) / 4;
+    ks.body = reinterpret_cast<const uint4*>(keys + n_head);
+    ks.head = keys;
+    ks.n_head = static_cast<int>(n_head);
+    ks.tail = keys + n_head + 4 * ks.nv;
+    ks.n_tail = static_cast<int>(count - n_head - 4 * ks.nv);
+    cuda_check(timed_launch("fused_sort", stream,
+                            [&] {
+                                return bws_gpu::launch_fused_sort(ks, key_range, key_lo, out, ctx.ctrl(),
+                                                                  ctx.fused, ctx.fused_saved, plan, stream);
+                            }),
+               "fused sort launch");
+    g_launches.fetch_add(1);
+    record_done(ctx, stream);
+}
+
+// One sort of distinct keys on the chosen pipeline. Returns the key range it
+// sorted with (0: derived on the device by the direct pipeline, ctrl->max_key).
+uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
+                      uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0) {
     const int path = current_path();
-    // bucket slots are 32-bit: the bucketed pipeline takes n < 2^32
-    const bool bucketed = count < (size_t(1) << 32) &&
-                          (path == BWS_PATH_BUCKETED || (path == BWS_PATH_AUTO && count >= kBucketedMinKeys));
-    if (bucketed)
-        enqueue_bucketed(ctx, keys, count, out, key_range, stream);
-    else
-        enqueue_direct(ctx, keys, count, out, key_range, stream);
+    if ((path == BWS_PATH_FUSED || (path == BWS_PATH_AUTO && count >= kFusedMinKeys)) && ctx.geo.fused_ctas > 0 &&
+        count < (size_t(1) << 32)) {
+        if (key_range == 0) {
+            wait_done(ctx, stream);
+            preserve_pending(ctx, stream);
+            key_range = derive_range(ctx, keys, count, stream, 0);
+        }
+        const bws_gpu::FusedPlan plan = fused_plan(ctx, key_range, count);
+        if (plan.ok) {
+            enqueue_fused(ctx, keys, count, out, key_range, plan, stream, key_lo);
+            return key_range;
+        }
+    }
+    // FUSED with a range it cannot hold falls back to AUTO's choice
+    const bool bucketed = key_lo != 0 || (count < (size_t(1) << 32) &&
+                                          (path == BWS_PATH_BUCKETED ||
+                                           ((path == BWS_PATH_AUTO || path == BWS_PATH_FUSED) &&
+                                            count >= kBucketedMinKeys)));
+    if (bucketed) return enqueue_bucketed(ctx, keys, count, out, key_range, stream, key_lo);
+    enqueue_direct(ctx, keys, count, out, key_range, stream);
+    return key_range;
 }
 
 // Synchronises and reads the control block back.
@@ -427,6 +488,10 @@ Ctrl read_ctrl(DeviceCtx& ctx, cudaStream_t stream) {
     Ctrl c;
     cuda_check(cudaMemcpy(&c, ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost),
                "control block readback");
+    if (c.error != 0) {  // KF ring protocol timeout: reset the ring state
+        ctx.fused_dirty = true;
+        throw internal_error("fused sort: ring protocol timeout (state reset)");
+    }
     return c;
 }
 
@@ -545,6 +610,16 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     } else {
         cuda_check(cudaGetDevice(&device), "cudaGetDevice");
     }
+    // a host array of unsigned keys on G > 1 configured devices: the
+    // single-process multi-GPU sort (multi.cpp, which locks every device
+    // context itself, so this runs before ctx.mu is taken); repeated keys come
+    // back untouched and take the single-GPU counting pass below
+    if (!on_device && xr == 0 && span_limit == 0 && count >= multi_min_keys() && multi_rank_count() > 1) {
+        if (multi_sort_host(data, count, key_range)) return;
+        if (!multiset)
+            throw data_error("keys are not distinct: " + std::to_string(count) +
+                             " keys (the bitset sort requires distinct keys)");
+    }
     DeviceCtx& ctx = context_for(device);
     std::lock_guard<std::mutex> lock(ctx.mu);
     int prev = 0;
@@ -570,12 +645,13 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
         key_range = mx + 1;
     };
     // signed keys (xr) always take the bucketed pipeline, which applies the XOR
+    uint64_t sorted_range = key_range;  // the range the bitset pass used (0: derived on the device)
     auto enqueue = [&](const uint32_t* in, uint32_t* out) {
         if (xr) {
             if (count >= (size_t(1) << 32)) throw std::out_of_range("signed sorts take fewer than 2^32 keys");
-            enqueue_bucketed(ctx, in, count, out, key_range, ctx.stream, 0, xr);
+            sorted_range = enqueue_bucketed(ctx, in, count, out, key_range, ctx.stream, 0, xr);
         } else {
-            enqueue_sort(ctx, in, count, out, key_range, ctx.stream);
+            sorted_range = enqueue_sort(ctx, in, count, out, key_range, ctx.stream);
         }
     };
     // after the bitset pass: true if the keys repeat and the counting-sort
@@ -590,7 +666,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
                              std::to_string(c.total) + " distinct (the bitset sort requires distinct keys)");
         if (count >= (size_t(1) << 32))
             throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
-        ms_range = key_range ? key_range : static_cast<uint64_t>(c.max_key) + 1;
+        ms_range = key_range ? key_range : sorted_range ? sorted_range : static_cast<uint64_t>(c.max_key) + 1;
         return true;
     };
     auto enqueue_multiset = [&](const uint32_t* in, uint32_t* out) {
@@ -614,15 +690,6 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
                    "device-to-device copy");
         cuda_check(cudaStreamSynchronize(ctx.stream), "device-to-device copy");
         return;
-    }
-    // a host array of unsigned keys on G > 1 configured devices: the
-    // single-process multi-GPU sort (multi.cpp); repeated keys come back
-    // untouched and take the single-GPU counting pass below
-    if (xr == 0 && span_limit == 0 && count >= multi_min_keys() && multi_rank_count() > 1) {
-        if (multi_sort_host(data, count, key_range)) return;
-        if (!multiset)
-            throw data_error("keys are not distinct: " + std::to_string(count) +
-                             " keys (the bitset sort requires distinct keys)");
     }
     ctx.ensure_keys(count);
     const size_t bytes = count * sizeof(uint32_t);
@@ -902,12 +969,9 @@ bws_status bws_gpu_sort_range_device_async(const uint32_t* keys, size_t count, u
         ctx.pending.active = false;  // superseded by this sort
         if (count == 0) return;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        if (key_lo == 0) {
-            enqueue_sort(ctx, keys, count, out, key_range, s);
-        } else {
-            if (count >= (size_t(1) << 32)) throw std::out_of_range("range sorts take fewer than 2^32 keys");
-            enqueue_bucketed(ctx, keys, count, out, key_range, s, key_lo);
-        }
+        if (key_lo != 0 && count >= (size_t(1) << 32))
+            throw std::out_of_range("range sorts take fewer than 2^32 keys");
+        enqueue_sort(ctx, keys, count, out, key_range, s, key_lo);
         ctx.pending = {true, s, count, key_range, false};
     });
 }
@@ -1238,7 +1302,7 @@ bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode) {
 
 bws_status bws_gpu_set_path(bws_path path) {
     return wrap([&] {
-        if (path < BWS_PATH_AUTO || path > BWS_PATH_BUCKETED) throw config_error("unknown path");
+        if (path < BWS_PATH_AUTO || path > BWS_PATH_FUSED) throw config_error("unknown path");
         g_path.store(static_cast<int>(path));
     });
 }

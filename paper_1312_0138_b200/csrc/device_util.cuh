@@ -182,6 +182,46 @@ __device__ __forceinline__ uint32_t extract_words64(const uint32_t* s_bits, uint
     return ctot;
 }
 
+// Extracts the `nwords` (multiple of 128) SMEM bitset words at s_bits[w0 ..)
+// to o[0 ..) in order; returns the number of keys. 128-word steps, lane-major
+// (lane owns 4 words); a step with <= STAGE keys is extracted in one pass
+// through the warp's stage, denser steps as two 64-word sub-steps (two words
+// per lane), and very dense ones word by word with ballots.
+template <int STAGE>
+__device__ __forceinline__ uint32_t extract_seg128(const uint32_t* s_bits, uint32_t w0, uint32_t nwords,
+                                                   uint32_t key_hi, uint32_t* __restrict__ o,
+                                                   uint32_t* s_stage, unsigned lane) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(s_bits);
+    uint32_t total = 0;
+    for (uint32_t w = w0; w < w0 + nwords; w += 128) {
+        const uint4 v = s4[w / 4 + lane];
+        const uint32_t cl = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        const uint32_t incl = warp_incl_scan(cl, lane);
+        const uint32_t ctot = __shfl_sync(kFull, incl, 31);
+        if (ctot == 0) continue;
+        uint32_t* od = o + total;
+        total += ctot;
+        if (ctot <= static_cast<uint32_t>(STAGE)) {
+            uint32_t p = incl - cl;
+            const uint32_t kb = key_hi + ((w + 4 * lane) << 5);
+            stage_bits(v.x, kb, p, s_stage);
+            stage_bits(v.y, kb + 32, p, s_stage);
+            stage_bits(v.z, kb + 64, p, s_stage);
+            stage_bits(v.w, kb + 96, p, s_stage);
+            drain_stage(s_stage, ctot, od, lane);
+            continue;
+        }
+        if (ctot > 2u * STAGE) {  // dense: word-by-word ballots
+#pragma unroll 1
+            for (uint32_t q = 0; q < 128; q += 32) od += extract_words32<STAGE>(s_bits, w + q, key_hi, od, s_stage, lane);
+            continue;
+        }
+        const uint32_t n0 = extract_words64<STAGE>(s_bits, w, key_hi, od, s_stage, lane);
+        extract_words64<STAGE>(s_bits, w + 64, key_hi, od + n0, s_stage, lane);
+    }
+    return total;
+}
+
 // Extracts the `nwords` (multiple of 512) SMEM bitset words at s_bits[w0 ..)
 // to o[0 ..) in order; returns the number of keys. 512-word steps: lane l
 // owns words [16l, 16l+16) of a step (4 LDS.128 in a lane-rotated order, so

@@ -61,6 +61,7 @@ constexpr size_t kCtrlBytes = sizeof(Ctrl) + 4 * kMaxTiles * sizeof(unsigned lon
 extern std::atomic<uint64_t> g_launches;
 extern std::atomic<int> g_scatter_mode;
 constexpr size_t kBucketedMinKeys = size_t(1) << 21;
+constexpr size_t kFusedMinKeys = size_t(1) << 16;  // AUTO: KF from here when the range fits
 
 int current_path();
 
@@ -83,6 +84,10 @@ struct DeviceCtx {
     void* wide = nullptr;               // staging for host arrays of 8/16/64-bit keys
     size_t wide_cap = 0;
     void* width_scratch = nullptr;      // 8/16-bit histogram + prefix, 64-bit min/max
+    void* fused = nullptr;              // KF ring state (persistent; re-initialised after a fault)
+    bool fused_dirty = true;
+    uint32_t* fused_saved = nullptr;    // KF pass-0 slices
+    size_t fused_saved_words = 0;
     // the most recent bws_gpu_sort_(range_)device_async on this device, checked
     // by bws_gpu_sort_check; once another library call reuses the control
     // block its final state is first copied (stream-ordered) to snap()
@@ -112,6 +117,7 @@ struct DeviceCtx {
         cuda_check(bws_gpu::configure_bucket_kernels(dev, &geo), "bucket kernel configuration");
         cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
         cuda_check(bws_gpu::configure_width_kernels(dev, &geo), "width kernel configuration");
+        cuda_check(bws_gpu::configure_fused(dev, &geo), "fused kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes + sizeof(Ctrl)), "cudaMalloc(control block)");
         pending = AsyncSort{};
@@ -181,6 +187,26 @@ struct DeviceCtx {
         return wide;
     }
 
+    // KF state (rings, counters) and the pass-0 slice buffer for `plan`.
+    void ensure_fused(const bws_gpu::FusedPlan& plan, cudaStream_t s) {
+        if (!fused) {
+            cuda_check(cudaMalloc(&fused, bws_gpu::fused_state_bytes(plan.G)), "cudaMalloc(fused rings)");
+            fused_dirty = true;
+        }
+        if (fused_dirty) {
+            cuda_check(bws_gpu::init_fused_state(fused, plan.G, s), "fused ring init");
+            fused_dirty = false;
+        }
+        const size_t words = plan.P == 2 ? static_cast<size_t>(plan.G) * (plan.S / 32) : 0;
+        if (words > fused_saved_words) {
+            if (fused_saved) cuda_check(cudaFree(fused_saved), "cudaFree(fused slices)");
+            fused_saved = nullptr;
+            fused_saved_words = 0;
+            cuda_check(cudaMalloc(&fused_saved, words * sizeof(uint32_t)), "cudaMalloc(fused slices)");
+            fused_saved_words = words;
+        }
+    }
+
     void ensure_bounce() {
         if (bounce[0]) return;
         for (int i = 0; i < 2; ++i) {
@@ -206,6 +232,12 @@ struct DeviceCtx {
         if (bucket_scratch) cudaFree(bucket_scratch);
         if (wide) cudaFree(wide);
         if (width_scratch) cudaFree(width_scratch);
+        if (fused) cudaFree(fused);
+        if (fused_saved) cudaFree(fused_saved);
+        fused = nullptr;
+        fused_dirty = true;
+        fused_saved = nullptr;
+        fused_saved_words = 0;
         wide = nullptr;
         wide_cap = 0;
         width_scratch = nullptr;

@@ -19,7 +19,7 @@ struct alignas(64) Ctrl {
     unsigned int done_ctas;        // slab KB3: CTAs finished (the last one scans the counts)
     unsigned long long total;      // set bits over the whole scan (K3, last tile)
     unsigned int min_inv;          // ~(min key), atomicMax (K0): zero-initialised like max_key
-    unsigned int pad0;
+    unsigned int error;            // KF: ring protocol timeout (the ring state is then reset)
     unsigned long long pad1[4];
 };
 static_assert(sizeof(Ctrl) == 64, "Ctrl is one 64-byte line");
@@ -89,6 +89,8 @@ struct LaunchGeometry {
     int bucket_blocks[MAX_BUCKET_SHIFT + 1] = {};  // KB4 CTAs per bucket shift
     int scan2_blocks = 0;                          // K3 v2 CTAs
     int multiset_blocks = 0;                       // KB4m CTAs (one per SM)
+    int fused_ctas = 0;                            // KF CTAs (one per SM; 0: no cooperative launch)
+    std::size_t fused_smem_limit = 0;              // KF dynamic SMEM ceiling
 };
 
 // A key array as seen by the bucketed kernels: 16-byte-aligned uint4 body plus
@@ -274,6 +276,49 @@ cudaError_t launch_radix64_hist(const std::uint64_t* keys, std::size_t n, int is
 cudaError_t launch_radix64_pass(const std::uint64_t* in, std::uint64_t* out, std::size_t n, int digit,
                                 std::uint64_t xin, std::uint64_t xout, void* scratch, const LaunchGeometry& geo,
                                 cudaStream_t stream);
+// KF (fused.cu): the whole sort in one persistent cooperative kernel, the
+// bitset of a pass split into per-SM slices held in shared memory, keys moved
+// to their slice's SM through L2-resident per-owner rings. For key ranges
+// whose bitset fits in <= 2 passes (plan_fused().ok).
+constexpr int KF_MAXG = 192;  // owners (CTAs = SMs) the state is sized for
+struct FusedPlan {
+    bool ok = false;
+    int P = 1;                 // passes over the keys
+    int G = 0;                 // CTAs = owners
+    std::uint32_t S = 0;       // slice bits per owner (multiple of 2^17)
+    std::uint32_t H = 0;       // G * S: keys [p H, (p + 1) H) in pass p (P == 2)
+    std::uint32_t mag = 0;     // ceil(2^32 / (S >> 12)): owner = umulhi(x >> 12, mag)
+    std::size_t smem = 0;      // dynamic SMEM per CTA
+};
+struct FusedArgs {
+    KeySplit ks;
+    std::uint32_t range_m1;    // keys x with (x ^ xr) - lo > range_m1 are bad
+    std::uint32_t lo;
+    std::uint32_t H, S, mag;
+    int P;
+    std::uint32_t* out;
+    Ctrl* ctrl;                // total, bad_keys, error = protocol timeout (written by CTA 0)
+    std::uint32_t* rings;      // 2 x G rings of 2^14 entries
+    std::uint32_t* tail;       // 2 x G claim counters
+    std::uint32_t* head;       // 2 x G consumed counters
+    std::uint32_t* sync;       // done[0], done[1], CTAs out, error
+    unsigned long long* counts;// 3 x G published counts (flag bit 63)
+    std::uint32_t* saved;      // G x S/32 words: pass-0 slices (P == 2)
+};
+FusedPlan plan_fused(std::uint64_t key_range, int sms, std::size_t smem_limit);
+std::size_t fused_state_bytes(int sms);
+cudaError_t configure_fused(int device, LaunchGeometry* geo);
+// (Re)initialises the persistent ring state (rings to 0xFF, counters to 0).
+cudaError_t init_fused_state(void* state, int sms, cudaStream_t stream);
+// Sorts the keys of `ks` (all (k ^ ks.xr) - key_lo < key_range, distinct) into
+// out (may alias the keys: every read precedes every write). ctrl->total =
+// distinct keys, ctrl->bad_keys = keys out of range, ctrl->error != 0 on a
+// protocol timeout (the state must then be re-initialised). `saved` holds
+// G * S / 32 words when plan.P == 2.
+cudaError_t launch_fused_sort(const KeySplit& ks, std::uint64_t key_range, std::uint32_t key_lo,
+                              std::uint32_t* out, Ctrl* ctrl, void* state, std::uint32_t* saved,
+                              const FusedPlan& plan, cudaStream_t stream);
+
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,
                            const LaunchGeometry& geo, cudaStream_t stream, std::uint32_t xr = 0);
