@@ -66,7 +66,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2", help="C1..C5 (BASELINE.json configs[0..4]) or 'all'")
-    ap.add_argument("--path", choices=["AUTO", "DIRECT", "BUCKETED"], default="AUTO")
+    ap.add_argument("--path", choices=["AUTO", "DIRECT", "BUCKETED", "FUSED"], default="AUTO")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample-keys", type=int, default=1 << 25,
                     help="keys in the cpu_baseline sample (about 10 s of reference CPU work)")
@@ -110,9 +110,19 @@ def measured_peak():
 
 
 # --- per-kernel algorithmic bytes ----------------------
+def fused_passes(key_range: int, sms: int = 148) -> int:
+    """Passes of the fused KF kernel over the keys (fused.cu plan_fused): one
+    when a per-SM slice of ceil(M / SMs) bits (rounded up to 2^17) fits next to
+    the producer's ~96 KB of SMEM, else two."""
+    per = -(-key_range // sms)
+    slice_bits = -(-per // (1 << 17)) * (1 << 17)
+    return 1 if slice_bits <= 8 * (1 << 17) else 2
+
+
 def kernel_alg_bytes(kernel: str, n: int, key_range: int, world: int = 1) -> int:
     words_bytes = (key_range + 31) // 32 * 4
     return {
+        "fused_sort": 4 * n * (fused_passes(key_range) + 1),  # read keys once per pass, write sorted keys
         "bucket_hist": 4 * n,                 # read keys
         "bucket_colscan": 0,
         "bucket_partition": 8 * n,            # read keys, write bucketed keys

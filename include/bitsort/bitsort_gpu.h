@@ -133,7 +133,7 @@ typedef enum bws_scatter_mode {
 BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
 
 /* Sort pipeline for bws_sort / bws_sort_u32_range / bws_gpu_sort_device_async
- * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed|fused).
+ * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed|fused|fused_direct).
  *   DIRECT   : K2 global-bitset scatter + K3 decoupled-lookback scan
  *   BUCKETED : key-range bucketing (coalesced) + per-bucket SMEM bitset +
  *              fused extraction; no global bitset
@@ -141,13 +141,17 @@ BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
  *              shared-memory slices, keys routed to their slice's SM through
  *              L2-resident rings (key ranges up to ~2^28 on a 148-SM B200;
  *              larger ranges take BUCKETED)
- *   AUTO     : FUSED when the key range fits it, else BUCKETED for
- *              n >= 2^21 and DIRECT below */
+ *   FUSED_DIRECT : one persistent kernel: keys ORed into the global bitset
+ *              (L2-resident), a grid barrier, then every SM counts and
+ *              extracts its slice in shared memory (small sorts)
+ *   AUTO     : FUSED_DIRECT for hinted sorts of 2^16..2^20 keys whose range
+ *              fits it, else BUCKETED for n >= 2^21 and DIRECT below */
 typedef enum bws_path {
     BWS_PATH_AUTO = 0,
     BWS_PATH_DIRECT = 1,
     BWS_PATH_BUCKETED = 2,
-    BWS_PATH_FUSED = 3
+    BWS_PATH_FUSED = 3,
+    BWS_PATH_FUSED_DIRECT = 4
 } bws_path;
 BITSORT_API bws_status bws_gpu_set_path(bws_path path);
 

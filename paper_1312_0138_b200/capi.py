@@ -61,6 +61,7 @@ class Path(enum.IntEnum):
     DIRECT = 1
     BUCKETED = 2
     FUSED = 3
+    FUSED_DIRECT = 4
 
 
 class BitsortError(RuntimeError):

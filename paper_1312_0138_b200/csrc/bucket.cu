@@ -854,15 +854,6 @@ constexpr std::size_t part_tma_smem_bytes(int maxb) {
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
 // with 4 per thread in flight, tail.
-// 16-byte streaming load that does not allocate in L1: KB4 keeps ~200 KB of
-// SMEM per SM, leaving a small L1 for the loads in flight
-__device__ __forceinline__ uint4 ld_na(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-}
 
 template <bool SPARSE, int NT = BUCKET_THREADS>
 __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__ src, uint32_t cnt,

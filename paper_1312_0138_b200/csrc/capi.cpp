@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
@@ -82,6 +83,7 @@ int current_path() {
     if (env && std::strcmp(env, "direct") == 0) p = BWS_PATH_DIRECT;
     if (env && std::strcmp(env, "bucketed") == 0) p = BWS_PATH_BUCKETED;
     if (env && std::strcmp(env, "fused") == 0) p = BWS_PATH_FUSED;
+    if (env && std::strcmp(env, "fused_direct") == 0) p = BWS_PATH_FUSED_DIRECT;
     g_path.store(p);
     return p;
 }
@@ -428,12 +430,23 @@ bws_gpu::FusedPlan fused_plan(const DeviceCtx& ctx, uint64_t key_range, size_t c
     return bws_gpu::plan_fused(key_range, ctx.geo.fused_ctas, ctx.geo.fused_smem_limit);
 }
 
+// direct: the KD mode (keys ORed into the cached global bitset, a grid
+// barrier, per-CTA slices counted and extracted); plan.P must be 1.
 void enqueue_fused(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out, uint64_t key_range,
-                   const bws_gpu::FusedPlan& plan, cudaStream_t stream, uint32_t key_lo = 0) {
-    NvtxRange nvtx_range("bitsort:fused KF");
+                   const bws_gpu::FusedPlan& plan, cudaStream_t stream, uint32_t key_lo = 0, bool direct = false) {
+    NvtxRange nvtx_range(direct ? "bitsort:fused KD" : "bitsort:fused KF");
     wait_done(ctx, stream);
     preserve_pending(ctx, stream);
     ctx.ensure_fused(plan, stream);
+    uint32_t* gbits = nullptr;
+    if (direct) {
+        ctx.ensure_bits();
+        if (ctx.bits_dirty) {
+            cuda_check(cudaMemsetAsync(ctx.bits, 0, kMaxWords * sizeof(uint32_t), stream), "bitset reset");
+            ctx.bits_dirty = false;
+        }
+        gbits = ctx.bits;  // KD zeroes every word it takes: all-zero again afterwards
+    }
     bws_gpu::KeySplit ks;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
     size_t n_head = ((16 - (addr & 15)) & 15) / 4;
@@ -444,13 +457,52 @@ void enqueue_fused(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
     ks.n_head = static_cast<int>(n_head);
     ks.tail = keys + n_head + 4 * ks.nv;
     ks.n_tail = static_cast<int>(count - n_head - 4 * ks.nv);
-    cuda_check(timed_launch("fused_sort", stream,
+    // BITSORT_KF_TRACE=1: per-CTA phase timestamps, summarised on stderr after
+    // every fused sort (synchronous; a debugging aid, not for timing runs)
+    static const bool trace_on = std::getenv("BITSORT_KF_TRACE") != nullptr;
+    unsigned long long* trace = nullptr;
+    if (trace_on) {
+        static unsigned long long* buf = nullptr;
+        if (!buf) cuda_check(cudaMalloc(&buf, bws_gpu::KF_MAXG * bws_gpu::KF_TRACE_WORDS * 8), "cudaMalloc(trace)");
+        cuda_check(cudaMemsetAsync(buf, 0, bws_gpu::KF_MAXG * bws_gpu::KF_TRACE_WORDS * 8, stream), "trace reset");
+        trace = buf;
+    }
+    cuda_check(timed_launch(direct ? "fused_direct" : "fused_sort", stream,
                             [&] {
                                 return bws_gpu::launch_fused_sort(ks, key_range, key_lo, out, ctx.ctrl(),
-                                                                  ctx.fused, ctx.fused_saved, plan, stream);
+                                                                  ctx.fused, ctx.fused_saved, plan, stream, trace,
+                                                                  gbits);
                             }),
                "fused sort launch");
     g_launches.fetch_add(1);
+    if (trace) {
+        std::vector<unsigned long long> h(static_cast<size_t>(plan.G) * bws_gpu::KF_TRACE_WORDS);
+        cuda_check(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, stream), "trace readback");
+        cuda_check(cudaStreamSynchronize(stream), "trace readback");
+        const char* names[] = {"start", "prod0", "cons0", "prod1", "cons1", "counts", "end", "offs_in", "seen"};
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < plan.G; ++c) t0 = std::min(t0, h[c * bws_gpu::KF_TRACE_WORDS]);
+        std::fprintf(stderr, "[KF trace] n=%zu P=%d S=%u:", count, plan.P, plan.S);
+        for (int ph = 0; ph < 9; ++ph) {
+            std::vector<double> v;
+            for (int c = 0; c < plan.G; ++c) {
+                const unsigned long long t = h[c * bws_gpu::KF_TRACE_WORDS + ph];
+                if (t) v.push_back((t - t0) / 1e3);
+            }
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, " %s %.1f/%.1f/%.1f", names[ph], v.front(), v[v.size() / 2], v.back());
+        }
+        std::fprintf(stderr, " us (min/med/max); producer clocks (median CTA, us at 1.9 GHz):");
+        const char* pn[] = {"wait", "rank", "A", "scan", "scatter", "store"};
+        for (int i = 0; i < 6; ++i) {
+            std::vector<double> v;
+            for (int c = 0; c < plan.G; ++c) v.push_back(h[c * bws_gpu::KF_TRACE_WORDS + 9 + i] / 1.9e3);
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, " %s %.1f", pn[i], v[v.size() / 2]);
+        }
+        std::fprintf(stderr, "\n");
+    }
     record_done(ctx, stream);
 }
 
@@ -459,8 +511,24 @@ void enqueue_fused(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
 uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
                       uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0) {
     const int path = current_path();
-    if ((path == BWS_PATH_FUSED || (path == BWS_PATH_AUTO && count >= kFusedMinKeys)) && ctx.geo.fused_ctas > 0 &&
-        count < (size_t(1) << 32)) {
+    const bool coop = ctx.geo.fused_ctas > 0 && count < (size_t(1) << 32);
+    // KD (fused direct) for hinted sorts of up to kFusedDirectMaxKeys keys
+    // whose bitset slices fit in SMEM in one pass; the KF ring mode only
+    // when asked for (BWS_PATH_FUSED: measured slower than BUCKETED on C2)
+    if (coop && (path == BWS_PATH_FUSED_DIRECT ||
+                 (path == BWS_PATH_AUTO && key_range != 0 && count >= kFusedMinKeys && count <= kFusedDirectMaxKeys))) {
+        if (key_range == 0) {
+            wait_done(ctx, stream);
+            preserve_pending(ctx, stream);
+            key_range = derive_range(ctx, keys, count, stream, 0);
+        }
+        const bws_gpu::FusedPlan plan = fused_plan(ctx, key_range, count);
+        if (plan.ok && plan.P == 1) {
+            enqueue_fused(ctx, keys, count, out, key_range, plan, stream, key_lo, /*direct=*/true);
+            return key_range;
+        }
+    }
+    if (coop && path == BWS_PATH_FUSED) {
         if (key_range == 0) {
             wait_done(ctx, stream);
             preserve_pending(ctx, stream);
@@ -472,11 +540,10 @@ uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
             return key_range;
         }
     }
-    // FUSED with a range it cannot hold falls back to AUTO's choice
+    // FUSED / FUSED_DIRECT with a range they cannot hold fall back to AUTO's choice
     const bool bucketed = key_lo != 0 || (count < (size_t(1) << 32) &&
                                           (path == BWS_PATH_BUCKETED ||
-                                           ((path == BWS_PATH_AUTO || path == BWS_PATH_FUSED) &&
-                                            count >= kBucketedMinKeys)));
+                                           (path != BWS_PATH_DIRECT && count >= kBucketedMinKeys)));
     if (bucketed) return enqueue_bucketed(ctx, keys, count, out, key_range, stream, key_lo);
     enqueue_direct(ctx, keys, count, out, key_range, stream);
     return key_range;
@@ -1302,7 +1369,7 @@ bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode) {
 
 bws_status bws_gpu_set_path(bws_path path) {
     return wrap([&] {
-        if (path < BWS_PATH_AUTO || path > BWS_PATH_FUSED) throw config_error("unknown path");
+        if (path < BWS_PATH_AUTO || path > BWS_PATH_FUSED_DIRECT) throw config_error("unknown path");
         g_path.store(static_cast<int>(path));
     });
 }

@@ -88,6 +88,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
+// 16-byte streaming load that does not allocate in L1 (kernels that keep
+// ~200 KB of SMEM per SM leave a small L1 for the loads in flight)
+__device__ __forceinline__ uint4 ld_na(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 // Writes kb + bit for every set bit of x, ascending, to the padded stage.
 __device__ __forceinline__ void stage_bits(uint32_t x, uint32_t kb, uint32_t& p, uint32_t* stage) {
     while (x) {

@@ -61,7 +61,8 @@ constexpr size_t kCtrlBytes = sizeof(Ctrl) + 4 * kMaxTiles * sizeof(unsigned lon
 extern std::atomic<uint64_t> g_launches;
 extern std::atomic<int> g_scatter_mode;
 constexpr size_t kBucketedMinKeys = size_t(1) << 21;
-constexpr size_t kFusedMinKeys = size_t(1) << 16;  // AUTO: KF from here when the range fits
+constexpr size_t kFusedMinKeys = size_t(1) << 16;        // AUTO: KD from here ...
+constexpr size_t kFusedDirectMaxKeys = size_t(1) << 20;  // ... up to here, when the range fits one pass
 
 int current_path();
 

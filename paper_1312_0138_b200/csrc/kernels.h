@@ -298,12 +298,15 @@ struct FusedArgs {
     int P;
     std::uint32_t* out;
     Ctrl* ctrl;                // total, bad_keys, error = protocol timeout (written by CTA 0)
-    std::uint32_t* rings;      // 2 x G rings of 2^14 entries
-    std::uint32_t* tail;       // 2 x G claim counters
-    std::uint32_t* head;       // 2 x G consumed counters
+    std::uint32_t* rings;      // 2 sets x G owners x 8 sub-rings of 2^12 entries
+    std::uint32_t* tail;       // claim counter per sub-ring
+    std::uint32_t* head;       // consumed counter per sub-ring
     std::uint32_t* sync;       // done[0], done[1], CTAs out, error
     unsigned long long* counts;// 3 x G published counts (flag bit 63)
     std::uint32_t* saved;      // G x S/32 words: pass-0 slices (P == 2)
+    unsigned long long* trace; // optional: per CTA phase timestamps + spin counts (9 words)
+    std::uint32_t* gbits;      // direct mode (KD, P == 1): the all-zero global bitset, >= G * S bits;
+                               // keys are ORed into it, then each CTA takes (and zeroes) its slice
 };
 FusedPlan plan_fused(std::uint64_t key_range, int sms, std::size_t smem_limit);
 std::size_t fused_state_bytes(int sms);
@@ -317,7 +320,10 @@ cudaError_t init_fused_state(void* state, int sms, cudaStream_t stream);
 // G * S / 32 words when plan.P == 2.
 cudaError_t launch_fused_sort(const KeySplit& ks, std::uint64_t key_range, std::uint32_t key_lo,
                               std::uint32_t* out, Ctrl* ctrl, void* state, std::uint32_t* saved,
-                              const FusedPlan& plan, cudaStream_t stream);
+                              const FusedPlan& plan, cudaStream_t stream,
+                              unsigned long long* trace = nullptr, std::uint32_t* gbits = nullptr);
+constexpr int KF_TRACE_WORDS = 15;  // per CTA: start, prod0, cons0, prod1, cons1, counts, end, spins x2,
+                                    // producer thread 0 clocks: wait, rank, barrier A, scan, scatter, store
 
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,

@@ -21,9 +21,11 @@ def capi(cuda):
     return c
 
 
-@pytest.fixture(autouse=True)
-def _fused(capi):
-    capi.set_path(capi.Path.FUSED)
+@pytest.fixture(autouse=True, params=["FUSED", "FUSED_DIRECT"])
+def _fused(capi, request):
+    """KF (ring mode) and KD (direct mode); ranges a mode cannot hold take
+    AUTO's pipeline."""
+    capi.set_path(getattr(capi.Path, request.param))
     yield
     capi.set_path(capi.Path.AUTO)
 

@@ -45,8 +45,26 @@ def run(keys, key_range, reps=1, time_it=False, path=capi.Path.FUSED):
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         t = float(np.median(ts))
+        capi.set_kernel_timing(True)
+        capi.kernel_timings()
+        for _ in range(5):
+            flush.fill_(1)
+            capi.sort_device_async(d.data_ptr(), keys.size, out.data_ptr(), key_range, s)
+        torch.cuda.synchronize()
+        kt = capi.kernel_timings()
+        capi.set_kernel_timing(False)
+        print("   kernels:", {k: round(v[1] / v[0] * 1000, 1) for k, v in kt.items()}, "us", flush=True)
     return ok, t
 
+
+if "--trace" in sys.argv:  # BITSORT_KF_TRACE=1 set by the caller
+    for cname in ["C1", "C2"]:
+        cfg = configs.CONFIGS[cname]
+        keys = cfg.generate()
+        run(keys, cfg.key_range, reps=4)
+        if cname == "C1":
+            run(keys, cfg.key_range, reps=4, path=capi.Path.FUSED_DIRECT)
+    sys.exit(0)
 
 rng = np.random.default_rng(1)
 cases = []
@@ -62,9 +80,19 @@ for name, keys, M in cases:
     ok, _ = run(keys, M, reps=3)
     print(f"{name}: {'ok' if ok else 'FAIL'}", flush=True)
     allok &= ok
+for n, M in [(1 << 16, 1 << 24), (1 << 20, 1 << 24), (1 << 22, 1 << 26), (1 << 22, 1 << 27)]:
+    keys = rng.choice(M, size=n, replace=False).astype(np.uint32)
+    for path in (capi.Path.FUSED_DIRECT, capi.Path.DIRECT, capi.Path.BUCKETED):
+        ok, t = run(keys, M, reps=2, time_it=True, path=path)
+        print(f"n=2^{n.bit_length()-1} M=2^{M.bit_length()-1} {path.name}: {'ok' if ok else 'FAIL'} {t*1000:.1f} us", flush=True)
+        allok &= ok
 for cname in ["C1", "C2"]:
     cfg = configs.CONFIGS[cname]
     keys = cfg.generate()
+    if cname == "C1":
+        okd, td = run(keys, cfg.key_range, reps=5, time_it=True, path=capi.Path.FUSED_DIRECT)
+        print(f"C1 fused_direct: {'ok' if okd else 'FAIL'}  {td*1000:.1f} us  {cfg.n / td / 1e6:.1f} Gkeys/s", flush=True)
+        allok &= okd
     ok, t = run(keys, cfg.key_range, reps=20, time_it=True)
     print(f"{cname} fused: {'ok' if ok else 'FAIL'}  {t*1000:.1f} us  {cfg.n / t / 1e6:.1f} Gkeys/s  frac {cfg.alg_bytes / (t*1e-3) / 6552e9:.3f}", flush=True)
     ok2, t2 = run(keys, cfg.key_range, reps=1, time_it=True, path=capi.Path.BUCKETED if cname == "C2" else capi.Path.DIRECT)
