@@ -321,6 +321,7 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         const uint32_t v = __ldcg(sa.gcnt + b);
         const bool ok = v <= sa.cap;
+        if (!ok) sa.ctrl->overflow = 1u;  // some runs were dropped: the slab lost keys
         sa.tot[b] = ok ? v : 0u;  // slots KB4 reads
         s_vals[b] = ok ? (sa.gtrue ? __ldcg(sa.gtrue + b) : v) : 0u;  // keys, for the offsets
         sa.gcnt[b] = 0u;  // the counters start the next sort at zero
@@ -696,8 +697,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
                 if (b == spill) continue;
                 atomicAdd(sa.gtrue + b, 1u);
                 const uint32_t pos = atomicAdd(sa.gcnt + b, 4u);
-                if (pos + 4 <= sa.cap)
-                    for (int q = 0; q < 4; ++q) parted[b * sa.cap + pos + q] = e;
+                if (pos + 4 <= sa.cap) {
+                    parted[b * sa.cap + pos] = e;
+                    for (int q = 1; q < 4; ++q) parted[b * sa.cap + pos + q] = bm.lo + (b + 1u) * bm.width;
+                }
             }
             extra = c == P - 1 ? ks.tail : nullptr;
             ne = c == P - 1 ? ks.n_tail : 0;
@@ -825,7 +828,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
                 const uint32_t b = sb + q;
                 const uint32_t cb = ccnt[q], pc = (cb + 3u) & ~3u;
                 const uint32_t st = s_start[b];
-                for (uint32_t i = cb; i < pc; ++i) s_sorted[st + i] = s_sorted[st];  // pad with a repeat
+                // pad to 4 with the first key past the bucket (KB4 and KB4m drop it):
+                // the slab then holds the exact key multiset (in-place recovery)
+                const uint32_t padv = bm.lo + (b + 1u) * bm.width;
+                for (uint32_t i = cb; i < pc; ++i) s_sorted[st + i] = padv;
                 fence_proxy_async_smem();
                 // a claim past the bucket's capacity (only duplicates cause one) is
                 // dropped: that bucket then sorts nothing and the popcount total
@@ -853,14 +859,16 @@ constexpr std::size_t part_tma_smem_bytes(int maxb) {
 
 // KB4 scatter of one bucket's keys into the SMEM bitset (and, for SPARSE
 // buckets, the summary of touched words): misaligned head, 16-byte loads
-// with 4 per thread in flight, tail.
+// with 4 per thread in flight, tail. Slab runs are padded with the first key
+// past the bucket (x == width), which is dropped.
 
 template <bool SPARSE, int NT = BUCKET_THREADS>
 __device__ __forceinline__ void scatter_bucket_keys(const uint32_t* __restrict__ src, uint32_t cnt,
-                                                    uint32_t key_lo, uint32_t* s_bits,
+                                                    uint32_t key_lo, uint32_t width, uint32_t* s_bits,
                                                     uint32_t* s_sum) {
     auto set_key = [&](uint32_t key) {
-        const uint32_t x = key - key_lo;  // < width: the key's bucket is this one
+        const uint32_t x = key - key_lo;  // < width: the key's bucket is this one (== width: padding)
+        if (x >= width) return;
         const uint32_t w = x >> 5;
         atomicOr(s_bits + w, 1u << (x & 31));
         if (SPARSE) atomicOr(s_sum + (w >> 5), 1u << (w & 31));
@@ -912,7 +920,10 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl,
-                       const uint32_t* __restrict__ order) {
+                       const uint32_t* __restrict__ order, int all_or_nothing) {
+    // in-place sorts: a slab that lost runs (repeated keys overflowed a
+    // bucket) writes nothing, so the input stays intact for the counting pass
+    if (all_or_nothing && *reinterpret_cast<volatile const uint32_t*>(&ctrl->overflow)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t W = bm.width >> 5;  // words per bucket bitset (>= 1024; 2^k or a multiple of 4096)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
@@ -980,9 +991,9 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
         if (sparse) {
-            scatter_bucket_keys<true, NT>(src, cnt, key_lo, s_bits, s_sum);
+            scatter_bucket_keys<true, NT>(src, cnt, key_lo, bm.width, s_bits, s_sum);
         } else if (src_cap) {  // slab-layout buckets: register loads measured faster (C2, C3)
-            scatter_bucket_keys<false, NT>(src, cnt, key_lo, s_bits, s_sum);
+            scatter_bucket_keys<false, NT>(src, cnt, key_lo, bm.width, s_bits, s_sum);
         } else {
             const uint32_t head = min(cnt, static_cast<uint32_t>(
                                                ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
@@ -1156,7 +1167,7 @@ constexpr std::size_t ms_smem_bytes() { return MS_CNT_BYTES + MS_STAGE_KEYS * 4;
 __global__ void __launch_bounds__(MS_THREADS, 1)
     bucket_multiset_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                            const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
-                           uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl) {
+                           uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl, uint32_t src_cap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw);  // counters, then inclusive prefix
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(smem_raw);
@@ -1174,7 +1185,9 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
         if (b >= static_cast<unsigned>(nb)) break;
         const uint32_t cnt = tot[b];
         const unsigned long long base = g_base[b];
-        const uint32_t* src = parted + base;
+        // packed layout: the bucket's keys sit where its output goes; slab
+        // layout (in-place recovery): its slab, padding (x == width) dropped
+        const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);
         const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
         const bool c16 = cnt < 65536u;           // block-uniform
         const int wshift = c16 ? 16 : 15;
@@ -1187,7 +1200,8 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
         // four independent loads per thread
         auto for_keys = [&](auto&& f) {
             if (staged) {
-                for (uint32_t i = threadIdx.x; i < cnt; i += MS_THREADS) f(s_keys[i], true);
+                for (uint32_t i = threadIdx.x; i < cnt; i += MS_THREADS)
+                    if (s_keys[i] < bm.width) f(s_keys[i], true);
                 return;
             }
             uint32_t i0 = 0;
@@ -1196,20 +1210,22 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + i0 + u * MS_THREADS + threadIdx.x);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) f(v[u] - key_lo, true);
+                for (int u = 0; u < 4; ++u)
+                    if (v[u] - key_lo < bm.width) f(v[u] - key_lo, true);
             }
-            for (uint32_t i = i0 + threadIdx.x; i < cnt; i += MS_THREADS) f(src[i] - key_lo, true);
+            for (uint32_t i = i0 + threadIdx.x; i < cnt; i += MS_THREADS)
+                if (src[i] - key_lo < bm.width) f(src[i] - key_lo, true);
         };
         __syncthreads();
         // pass 0: keys per window (warp-aggregated: one SMEM atomic per window per warp step)
-        if (nwin == 1) {
+        if (nwin == 1 && !src_cap) {  // (slab slots also hold padding: counted below)
             if (threadIdx.x == 0) s_wc[0] = cnt;
         } else {
             const uint32_t rounds = (cnt + MS_THREADS - 1) / MS_THREADS;  // every lane takes part in the match
             for (uint32_t r = 0; r < rounds; ++r) {
                 const uint32_t i = r * MS_THREADS + threadIdx.x;
                 const uint32_t x = i < cnt ? (staged ? s_keys[i] : src[i] - key_lo) : 0u;
-                const uint32_t w = i < cnt ? x >> wshift : 0xffffffffu;
+                const uint32_t w = i < cnt && x < bm.width ? x >> wshift : 0xffffffffu;
                 const unsigned peers = __match_any_sync(kFull, w);
                 if (w != 0xffffffffu && lane == static_cast<unsigned>(__ffs(peers) - 1))
                     atomicAdd(&s_wc[w], static_cast<uint32_t>(__popc(peers)));
@@ -1282,7 +1298,7 @@ __global__ void __launch_bounds__(MS_THREADS, 1)
             o += wk;
             __syncthreads();
         }
-        if (threadIdx.x == 0) written += cnt;
+        if (threadIdx.x == 0) written += o - base;  // keys written (slab padding excluded)
     }
     if (threadIdx.x == 0 && written) atomicAdd(&ctrl->total, written);
 }
@@ -1308,7 +1324,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
         const unsigned b = s_b;
         if (b >= static_cast<unsigned>(nb)) break;
         scatter_bucket_keys<false>(parted + (src_cap ? static_cast<size_t>(b) * src_cap : g_base[b]), tot[b],
-                                   bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, nullptr);
+                                   bm.lo + static_cast<uint32_t>(b) * bm.width, bm.width, s_bits, nullptr);
         __syncthreads();
         const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
         // keys in [key_range, 32 * n_words) of a non-multiple-of-32 range never appear
@@ -1359,7 +1375,7 @@ __global__ void __launch_bounds__(BUCKET_THREADS, 1)
         const unsigned b = s_b;
         if (b >= static_cast<unsigned>(nb)) break;
         scatter_bucket_keys<false>(parted + (src_cap ? static_cast<size_t>(b) * src_cap : g_base[b]), tot[b],
-                                   bm.lo + static_cast<uint32_t>(b) * bm.width, s_bits, nullptr);
+                                   bm.lo + static_cast<uint32_t>(b) * bm.width, bm.width, s_bits, nullptr);
         __syncthreads();
         const unsigned long long w0 = static_cast<unsigned long long>(b) * W;
         if (threadIdx.x == 0 && n_words - 1 >= w0 && n_words - 1 < w0 + W) s_bits[n_words - 1 - w0] &= last_mask;
@@ -1587,6 +1603,11 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
     return slots;
 }
 
+bool slab_in_use(const BucketPlan& plan, size_t n, uint64_t parted_cap) {
+    const uint64_t slab = slab_slots(plan, n);
+    return slab != 0 && slab <= parted_cap;
+}
+
 size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
     return static_cast<size_t>(hist_blocks) * plan.nb * sizeof(uint32_t)  // H
            + (MAX_BUCKETS + 1) * sizeof(uint32_t)                          // tot
@@ -1600,7 +1621,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
                                const LaunchGeometry& geo, cudaStream_t stream, int* launches,
                                KernelTimer* timer, uint32_t* bits_out, uint64_t n_words,
                                uint64_t parted_cap, bool multiset, const OrSources* push,
-                               uint64_t push_slice_words) {
+                               uint64_t push_slice_words, int inplace_mode) {
     if (n == 0) return cudaSuccess;
     const int P = narrow_partition(plan) ? geo.part_blocks_narrow : geo.part_blocks;
     // scratch: slab fill counters (fixed place: they persist across sorts), then H, tot, base
@@ -1638,6 +1659,21 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     SlabArgs sa;
     int nlaunch = 0;
     cudaError_t err;
+    if (inplace_mode == 2) {
+        // recovery of an in-place sort whose keys repeat: the previous slab
+        // KB3 (same keys, plan, buffers) left the exact multiset in its slabs
+        // (padding is out of bucket) and the totals/offsets in the scratch;
+        // KB4m counting-sorts every bucket from its slab into out
+        if (!use_slab) return cudaErrorInvalidValue;
+        const uint32_t cap = static_cast<uint32_t>((slab - PART_DUMP) / plan.nb) & ~3u;
+        if (timer) timer->before(stream);
+        bucket_multiset_kernel<<<geo.multiset_blocks, MS_THREADS, ms_smem_bytes(), stream>>>(
+            parted, tot, base, plan.map, plan.nb, out, ctrl, cap);
+        if (timer) timer->after("bucket_multiset", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (launches) *launches = 1;
+        return cudaSuccess;
+    }
     if (use_slab) {
         // KB3 (slab) claims slots with fill counters: no KB1/KB2. The counters
         // are zeroed once at allocation and re-zeroed by the last KB3 CTA.
@@ -1730,7 +1766,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (multiset) {
         if (timer) timer->before(stream);
         bucket_multiset_kernel<<<geo.multiset_blocks, MS_THREADS, ms_smem_bytes(), stream>>>(
-            parted, tot, base, plan.map, plan.nb, out, ctrl);
+            parted, tot, base, plan.map, plan.nb, out, ctrl, 0u);
         if (timer) timer->after("bucket_multiset", stream);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         if (launches) *launches = nlaunch + 1;
@@ -1740,10 +1776,10 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     const size_t smem = bucket_sort_smem_bytes(plan.shift);
     if (plan.shift >= MAX_BUCKET_SHIFT)
         bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order);
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab);
     else  // narrower buckets: two 512-thread CTAs per SM
         bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order);
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;

@@ -399,7 +399,7 @@ uint64_t derive_range(DeviceCtx& ctx, const uint32_t* keys, size_t count, cudaSt
 // multiset: repeated keys are sorted too (packed layout + KB4m counting sort).
 uint64_t enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
                           uint64_t key_range, cudaStream_t stream, uint32_t key_lo = 0, uint32_t xr = 0,
-                          bool multiset = false) {
+                          bool multiset = false, int inplace_mode = 0) {
     NvtxRange nvtx_range("bitsort:bucketed KB1-KB4");
     wait_done(ctx, stream);
     preserve_pending(ctx, stream);
@@ -416,11 +416,21 @@ uint64_t enqueue_bucketed(DeviceCtx& ctx, const uint32_t* keys, size_t count, ui
     int launches = 0;
     cuda_check(bws_gpu::launch_bucket_sort(keys, count, key_range, out, ctx.parted, ctx.bucket_scratch,
                                            ctx.ctrl(), plan, ctx.geo, stream, &launches,
-                                           active_timer(), nullptr, 0, parted_cap, multiset),
+                                           active_timer(), nullptr, 0, parted_cap, multiset, nullptr, 0,
+                                           inplace_mode),
                "bucketed sort launch");
     g_launches.fetch_add(static_cast<uint64_t>(launches));
     record_done(ctx, stream);
     return key_range;
+}
+
+// Whether a bucketed sort of `count` keys over key_range takes the slab
+// layout (the only layout an in-place bws_sort can recover repeats from).
+bool bucketed_slab(DeviceCtx& ctx, size_t count, uint64_t key_range, uint32_t xr) {
+    const bws_gpu::BucketPlan plan =
+        bws_gpu::plan_buckets(key_range, xr ? 0 : ctx.geo.bucket_blocks[bws_gpu::MAX_BUCKET_SHIFT]);
+    const size_t cap = ctx.ensure_parted(count, plan);
+    return bws_gpu::slab_in_use(plan, count, cap);
 }
 
 // KF: the single-launch fused sort (fused.cu) for key ranges whose bitset
@@ -746,6 +756,33 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
             enqueue(keys, keys);
             validate(ctx, count, key_range, ctx.stream);
             return;
+        }
+        // In place when the bucketed slab pipeline takes the keys: KB3 reads
+        // every key before KB4 writes any output, a slab that lost runs makes
+        // KB4 write nothing (the keys stay intact for the counting pass), and
+        // otherwise the slabs hold the exact key multiset, from which KB4m
+        // redoes a sort whose keys repeat. Other pipelines sort out of place.
+        const int path = current_path();
+        if (count >= kBucketedMinKeys && count < (size_t(1) << 32) &&
+            (path == BWS_PATH_AUTO || path == BWS_PATH_BUCKETED)) {
+            wait_done(ctx, ctx.stream);
+            preserve_pending(ctx, ctx.stream);
+            if (key_range == 0) key_range = derive_range(ctx, keys, count, ctx.stream, xr);
+            if (bucketed_slab(ctx, count, key_range, xr)) {
+                enqueue_bucketed(ctx, keys, count, keys, key_range, ctx.stream, 0, xr, false, /*inplace=*/1);
+                const Ctrl c = read_ctrl(ctx, ctx.stream);
+                throw_bad_keys(c, key_range);
+                if (c.total == count) return;
+                if (count >= (size_t(1) << 32)) throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
+                ms_range = key_range;
+                if (c.overflow) {  // nothing written: the counting pass from the keys
+                    enqueue_multiset(keys, keys);
+                    return;
+                }
+                enqueue_bucketed(ctx, keys, count, keys, key_range, ctx.stream, 0, xr, false, /*recover=*/2);
+                validate(ctx, count, key_range, ctx.stream);
+                return;
+            }
         }
         ctx.ensure_keys(count);
         enqueue(keys, ctx.keys);

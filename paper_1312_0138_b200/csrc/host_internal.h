@@ -62,7 +62,7 @@ extern std::atomic<uint64_t> g_launches;
 extern std::atomic<int> g_scatter_mode;
 constexpr size_t kBucketedMinKeys = size_t(1) << 21;
 constexpr size_t kFusedMinKeys = size_t(1) << 16;        // AUTO: KD from here ...
-constexpr size_t kFusedDirectMaxKeys = size_t(1) << 20;  // ... up to here, when the range fits one pass
+constexpr size_t kFusedDirectMaxKeys = 0;  // ... up to here (0: AUTO never takes KD: a tie with K2+K3 on C1)
 
 int current_path();
 

@@ -20,7 +20,9 @@ struct alignas(64) Ctrl {
     unsigned long long total;      // set bits over the whole scan (K3, last tile)
     unsigned int min_inv;          // ~(min key), atomicMax (K0): zero-initialised like max_key
     unsigned int error;            // KF: ring protocol timeout (the ring state is then reset)
-    unsigned long long pad1[4];
+    unsigned int overflow;         // slab KB3: a bucket's runs were dropped (repeated keys)
+    unsigned int pad2;
+    unsigned long long pad1[3];
 };
 static_assert(sizeof(Ctrl) == 64, "Ctrl is one 64-byte line");
 
@@ -221,7 +223,15 @@ cudaError_t launch_bucket_sort(const std::uint32_t* keys, std::size_t n, std::ui
                                cudaStream_t stream, int* launches, KernelTimer* timer = nullptr,
                                std::uint32_t* bits_out = nullptr, std::uint64_t n_words = 0,
                                std::uint64_t parted_cap = 0, bool multiset = false,
-                               const struct OrSources* push = nullptr, std::uint64_t push_slice_words = 0);
+                               const struct OrSources* push = nullptr, std::uint64_t push_slice_words = 0,
+                               int inplace_mode = 0);
+// inplace_mode (slab layout only, out == keys): 1 = KB4 writes nothing if any
+// bucket's runs were dropped (ctrl->overflow: the keys stay intact for the
+// counting pass); 2 = recovery after a mode-1 sort found repeats without
+// overflow: KB4m counting-sorts every bucket from the slabs the mode-1 KB3
+// left (same keys, plan and buffers; ctrl ticket/total zeroed by the caller).
+// slab_in_use: whether launch_bucket_sort takes the slab layout for (plan, n).
+bool slab_in_use(const BucketPlan& plan, std::size_t n, std::uint64_t parted_cap);
 // Multi-GPU OR-gather (the P2P replacement of the reduce-scatter): dst[i] =
 // OR over s of srcs.p[s][i] for i < n_words; srcs may point into peer GPUs'
 // memory (CUDA IPC over NVLink/NVSwitch).

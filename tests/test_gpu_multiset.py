@@ -140,3 +140,34 @@ def test_c2_shape_with_repeats(capi, cuda):
     assert capi.sort_raw(t.data_ptr(), keys.size, 32, 1, 0) == capi.Status.OK, capi.last_error()
     got = t.cpu().numpy().view(np.uint32)
     assert np.array_equal(got, np.sort(keys))
+
+
+@pytest.mark.parametrize("case", ["distinct", "repeats_no_overflow", "overflow", "signed_repeats",
+                                  "distinct_then_repeats"])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_device_array_in_place(capi, cuda, case, offset):
+    """bws_sort on device arrays of >= 2^21 keys sorts in place through the
+    slab pipeline: distinct keys need no copy; repeats without a dropped slab
+    run are redone from the slabs (KB4m over the slab layout, padding dropped);
+    a bucket that overflowed makes KB4 write nothing, so the counting pass
+    starts from the intact keys. Every case against the reference's sort."""
+    rng = np.random.default_rng(31 + offset)
+    n = (1 << 22) + 3
+    is_unsigned = 1
+    if case == "distinct":
+        keys = rng.choice(1 << 23, size=n, replace=False).astype(np.uint32)
+    elif case == "repeats_no_overflow":  # ~2^21 repeated values over 8 slab buckets
+        keys = rng.integers(0, 1 << 23, size=n, dtype=np.uint64).astype(np.uint32)
+    elif case == "overflow":  # one 2^20-key bucket receives 4x its capacity
+        keys = rng.integers(0, 1 << 20, size=n, dtype=np.uint64).astype(np.uint32)
+    elif case == "signed_repeats":
+        keys = rng.integers(-(1 << 22), 1 << 22, size=n, dtype=np.int64).astype(np.int32)
+        is_unsigned = 0
+    else:  # a distinct sort, then repeats over the same buffers
+        d = rng.choice(1 << 23, size=n, replace=False).astype(np.uint32)
+        assert np.array_equal(_sort_device(capi, cuda, d, 1, offset), np.sort(d))
+        keys = rng.integers(0, 1 << 23, size=n, dtype=np.uint64).astype(np.uint32)
+    got = _sort_device(capi, cuda, keys, is_unsigned, offset)
+    assert np.array_equal(got, np.sort(keys)), case
+    if case != "distinct" and oracle.REFERENCE is not None:
+        assert np.array_equal(got, _reference(keys, is_unsigned))
