@@ -94,7 +94,7 @@ for cname in ["C1", "C2"]:
         print(f"C1 fused_direct: {'ok' if okd else 'FAIL'}  {td*1000:.1f} us  {cfg.n / td / 1e6:.1f} Gkeys/s", flush=True)
         allok &= okd
     ok, t = run(keys, cfg.key_range, reps=20, time_it=True)
-    print(f"{cname} fused: {'ok' if ok else 'FAIL'}  {t*1000:.1f} us  {cfg.n / t / 1e6:.1f} Gkeys/s  frac {cfg.alg_bytes / (t*1e-3) / 6552e9:.3f}", flush=True)
+    print(f"{cname} fused: {'ok' if ok else 'FAIL'}  {t*1000:.1f} us  {cfg.n / t / 1e6:.1f} Gkeys/s  frac {cfg.alg_bytes / (t*1e-3) / (configs.hbm_peak()[0] * 1e9):.3f}", flush=True)
     ok2, t2 = run(keys, cfg.key_range, reps=1, time_it=True, path=capi.Path.BUCKETED if cname == "C2" else capi.Path.DIRECT)
     print(f"{cname} previous: {t2*1000:.1f} us", flush=True)
     allok &= ok
