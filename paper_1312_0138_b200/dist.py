@@ -273,9 +273,7 @@ def distributed_sort(keys: torch.Tensor, key_range: int, n_total: Optional[int] 
     capacity = max(0, min(n_total, key_hi - key_lo))
     out, count_t = ops.bitset_scan(slice_, key_lo, capacity)
 
-    counts = [torch.empty_like(count_t) for _ in range(world)]
-    dist.all_gather(counts, count_t, group=group)
-    counts_h = [int(c.item()) for c in counts]
+    counts_h = _gather_counts(count_t, world, group)
     total = sum(counts_h)
     if total != n_total:
         from .capi import BitsortError, Status
@@ -285,6 +283,14 @@ def distributed_sort(keys: torch.Tensor, key_range: int, n_total: Optional[int] 
     count = counts_h[rank]
     return SliceResult(keys=out[:count], count=count, offset=sum(counts_h[:rank]), total=total,
                        key_lo=key_lo, key_hi=key_hi)
+
+
+def _gather_counts(count_t: torch.Tensor, world: int, group) -> list[int]:
+    """Every rank's count (one all-gather, then ONE device-to-host read for all
+    of them rather than one blocking read per rank)."""
+    counts = [torch.empty_like(count_t) for _ in range(world)]
+    dist.all_gather(counts, count_t, group=group)
+    return [int(c) for c in torch.stack(counts).reshape(-1).tolist()]
 
 
 def _device_sync(dev: torch.device) -> None:
@@ -341,8 +347,9 @@ def distributed_sort_a2a(keys: torch.Tensor, key_range: int, n_total: Optional[i
     stat = torch.tensor([recv.numel(), 0 if ok else 1], dtype=torch.int64, device=dev)
     stats = [torch.empty_like(stat) for _ in range(world)]
     dist.all_gather(stats, stat, group=group)
-    counts_h = [int(x[0].item()) for x in stats]
-    errors = sum(int(x[1].item()) for x in stats)
+    st = torch.stack(stats).tolist()  # one device-to-host read
+    counts_h = [int(x[0]) for x in st]
+    errors = sum(int(x[1]) for x in st)
     total = sum(counts_h)
     if errors or total != n_total:
         raise _data_error(f"keys are not distinct: {n_total} keys, duplicates within "
@@ -391,9 +398,7 @@ def distributed_sort_p2p(keys: torch.Tensor, key_range: int, n_total: Optional[i
         out, count_t = ops.or_scan(sources, rank * per, per, key_lo, capacity)
     # the counts' all-gather doubles as the "peers are done reading" barrier
     # (each rank's count is read back only after its scan has completed)
-    counts = [torch.empty_like(count_t) for _ in range(world)]
-    dist.all_gather(counts, count_t, group=group)
-    counts_h = [int(c.item()) for c in counts]
+    counts_h = _gather_counts(count_t, world, group)
     total = sum(counts_h)
     if total != n_total:
         raise _data_error(f"keys are not distinct or out of range: {n_total} keys, {total} distinct")
@@ -446,9 +451,7 @@ def distributed_sort_push(keys: torch.Tensor, key_range: int, n_total: Optional[
     key_hi = min((rank + 1) * per * 32, key_range)
     capacity = max(0, min(n_total, key_hi - key_lo))
     out, count_t = ops.bitset_scan(own, key_lo, capacity)
-    counts = [torch.empty_like(count_t) for _ in range(world)]
-    dist.all_gather(counts, count_t, group=group)
-    counts_h = [int(c.item()) for c in counts]
+    counts_h = _gather_counts(count_t, world, group)
     total = sum(counts_h)
     if total != n_total:
         raise _data_error(f"keys are not distinct or out of range: {n_total} keys, {total} distinct")
