@@ -299,6 +299,24 @@ __device__ void compute_kb4_order(const uint32_t* __restrict__ tot, int nb, uint
     }
 }
 
+// Chunked layout (packed sorts without KB1/KB2): a bucket's keys live in
+// KC_CHUNK-slot chunks of a pool, chunk j of bucket b at pool chunk
+// chunk_tab[b * max_chunks + j] - 1 (0: not allocated yet). Tiles claim runs
+// in a bucket with one atomicAdd on its fill counter, as in the slab layout;
+// the claim that holds a chunk's first slot allocates it, others wait for it.
+__device__ __forceinline__ uint32_t chunk_alloc(const SlabArgs& sa, uint32_t b, uint32_t j) {
+    const uint32_t id = atomicAdd(sa.pool_next, 1u);
+    atomicExch(sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j, id + 1u);
+    return id;
+}
+__device__ __forceinline__ uint32_t chunk_get(const SlabArgs& sa, uint32_t b, uint32_t j) {
+    const volatile uint32_t* t = sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j;
+    uint32_t v;
+    while ((v = *t) == 0u) {
+    }  // the allocating claim precedes ours and every KB3 CTA is resident
+    return v - 1u;
+}
+
 // Slab epilogue shared by the slab KB3 variants: folds the CTA's bad-key
 // count into ctrl, and the last CTA to finish turns the fill counters into
 // bucket totals (0 for an overflowed bucket: its keys are lost, so the sort
@@ -331,6 +349,10 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
     const unsigned long long total = block_exclusive_scan_u64(s_vals, nb, s_out64, s_scratch);
     for (int b = threadIdx.x; b < nb; b += blockDim.x) sa.g_base[b] = s_out64[b];
     if (threadIdx.x == 0) sa.g_base[nb] = total;
+    if (sa.order) {  // chunked layout: KB4's ticket order from the totals
+        __syncthreads();
+        compute_kb4_order(sa.tot, nb, sa.order);
+    }
 }
 
 // KB3: partition, one persistent CTA per SM. CTA c streams its share in
@@ -354,15 +376,20 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
 // written 32-byte sectors of ~4096 short runs per tile stay in L2 until
 // complete instead of being evicted half-written (measured: C5 KB3 1570 ->
 // 1462 us, C4 116 -> 104 us; the slab layout's longer runs (C3) got slower).
-template <int THREADS, int KPT, int MAXB, bool SLAB>
+template <int THREADS, int KPT, int MAXB, int LAYOUT>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     bucket_partition_kernel(KeySplit ks, BucketMap bm, int nb,
                             const uint32_t* __restrict__ H, const uint32_t* __restrict__ tot,
                             uint32_t* __restrict__ parted, unsigned long long* __restrict__ g_base,
                             SlabArgs sa) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    // LAYOUT 0: packed (KB1/KB2 offsets); 1: slab (fixed per-bucket capacity,
+    // claims); 2: chunked (claims into pool chunks allocated on first touch)
+    constexpr bool SLAB = LAYOUT != 0;
+    constexpr bool CHUNK = LAYOUT == 2;
     constexpr int kSlots = MAXB + 1;
     constexpr int TILE = THREADS * KPT;
+    static_assert(!CHUNK || TILE <= 32767, "chunked crossings are 15-bit tile positions");
     constexpr int NWARPS = THREADS / 32;
     constexpr int PER_MAX = (kSlots + THREADS - 1) / THREADS;
     uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 x TILE
@@ -405,7 +432,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         for (size_t t = 0; t < 2 && t < ntiles; ++t) {
             const size_t v0 = vlo + t * kTileVec;
             const size_t nvec = min(kTileVec, vhi - v0);
-            if (!SLAB)
+            if (!SLAB || CHUNK)
                 tma_load_bytes_hint(s_buf + t * TILE, ks.body + v0, static_cast<unsigned>(nvec * 16), &s_bar[t],
                                     l2_policy_evict_first());
             else
@@ -440,7 +467,19 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             for (int i = 0; i < ne; ++i) {
                 const uint32_t e = extra[i] ^ ks.xr;
                 const uint32_t b = slot_of(e, true);
-                if constexpr (SLAB) {
+                if constexpr (CHUNK) {
+                    bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
+                    if (b != spill) {
+                        const uint32_t pos = atomicAdd(sa.gcnt + b, 1u);
+                        const uint32_t j = pos / KC_CHUNK;
+                        if (j < sa.max_chunks) {
+                            const uint32_t id = pos % KC_CHUNK == 0 ? chunk_alloc(sa, b, j) : chunk_get(sa, b, j);
+                            parted[static_cast<size_t>(id) * KC_CHUNK + pos % KC_CHUNK] = e;
+                        } else {
+                            sa.ctrl->overflow = 1u;
+                        }
+                    }
+                } else if constexpr (SLAB) {
                     bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
                         const uint32_t pos = atomicAdd(sa.gcnt + b, 1u);
@@ -569,7 +608,38 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         for (int q = 0; q < KPT; ++q) rb[q] = s_start[rb[q] >> 16] + (rb[q] & 0xffffu);
 #pragma unroll
         for (int q = 0; q < KPT; ++q) buf[rb[q]] = k[q];
-        if constexpr (SLAB) {
+        if constexpr (CHUNK) {
+            // every chunk whose first slot lies in this tile's run is allocated
+            // here (allocation never waits); the run's first chunk, when an
+            // earlier claim owns it, is waited for (all KB3 CTAs are resident)
+#pragma unroll
+            for (int q = 0; q < PER_MAX; ++q) {
+                if (ccnt[q]) {
+                    const uint32_t b = sb + q;
+                    const uint32_t cl = claim[q], cb = ccnt[q];
+                    const uint32_t j0 = cl / KC_CHUNK, j1 = (cl + cb - 1) / KC_CHUNK;
+                    if (j1 >= sa.max_chunks) {  // repeated keys overflowed the bucket
+                        sa.ctrl->overflow = 1u;
+                        s_cur[b] = KC_DROP;  // (any 32-bit delta is a valid slot offset)
+                        continue;
+                    }
+                    uint32_t id0 = 0;
+                    for (uint32_t j = j0; j <= j1; ++j) {
+                        if (j * KC_CHUNK >= cl) {
+                            const uint32_t id = chunk_alloc(sa, b, j);
+                            if (j == j0) id0 = id;
+                        }
+                    }
+                    if (cl % KC_CHUNK != 0) id0 = chunk_get(sa, b, j0);
+                    const uint32_t st = s_start[b];
+                    s_delta[b] = id0 * KC_CHUNK + cl % KC_CHUNK - st;
+                    // tile position where the run leaves its first chunk (0x7fff: never),
+                    // with the next chunk's index above it for the slow path
+                    const uint32_t room = KC_CHUNK - cl % KC_CHUNK;
+                    s_cur[b] = cb > room ? (st + room) | ((j0 + 1) << 15) : 0x7fffu;
+                }
+            }
+        } else if constexpr (SLAB) {
 #pragma unroll
             for (int q = 0; q < PER_MAX; ++q) {
                 if (ccnt[q]) {
@@ -593,6 +663,23 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 const uint32_t key = buf[i];
                 st_hint(parted + s_delta[bucket_id(key, bm)] + i, key, pol);
             }
+        } else if constexpr (CHUNK) {
+            const unsigned long long pol = l2_policy_evict_last();
+#pragma unroll 4
+            for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
+                const uint32_t key = buf[i];
+                const uint32_t b = bucket_id(key, bm);
+                const uint32_t d = s_delta[b];
+                const uint32_t x = s_cur[b];
+                if (x == KC_DROP) continue;  // an overflowed (repeated-key) run
+                size_t dst = d + i;  // (32-bit wrap: d is the slot minus the tile position)
+                if (i >= (x & 0x7fffu)) {  // past the run's first chunk (rare)
+                    const uint32_t k2 = i - (x & 0x7fffu);
+                    const uint32_t id = chunk_get(sa, b, (x >> 15) + k2 / KC_CHUNK);
+                    dst = static_cast<size_t>(id) * KC_CHUNK + k2 % KC_CHUNK;
+                }
+                st_hint(parted + dst, key, pol);
+            }
         } else {
 #pragma unroll 4
             for (uint32_t i = threadIdx.x; i < tile_valid; i += THREADS) {
@@ -606,7 +693,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             const size_t v2 = vlo + (t + 2) * kTileVec;
             const size_t nv2 = min(kTileVec, vhi - v2);
             fence_proxy_async_smem();
-            if (!SLAB)
+            if (!SLAB || CHUNK)
                 tma_load_bytes_hint(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p],
                                     l2_policy_evict_first());
             else
@@ -920,7 +1007,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
     bucket_sort_kernel(const uint32_t* __restrict__ parted, const uint32_t* __restrict__ tot,
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl,
-                       const uint32_t* __restrict__ order, int all_or_nothing) {
+                       const uint32_t* __restrict__ order, int all_or_nothing,
+                       const uint32_t* __restrict__ chunk_tab, uint32_t max_chunks) {
     // in-place sorts: a slab that lost runs (repeated keys overflowed a
     // bucket) writes nothing, so the input stays intact for the counting pass
     if (all_or_nothing && *reinterpret_cast<volatile const uint32_t*>(&ctrl->overflow)) return;
@@ -990,36 +1078,66 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
-        if (sparse) {
+        // chunked layout: the bucket's keys are KC_CHUNK-slot pool chunks
+        auto chunk_src = [&](uint32_t j) {
+            return parted + static_cast<size_t>(chunk_tab[static_cast<size_t>(b) * max_chunks + j] - 1u) * KC_CHUNK;
+        };
+        if (chunk_tab && (sparse || cnt <= 2 * KC_CHUNK)) {
+            for (uint32_t j = 0; j * KC_CHUNK < cnt; ++j) {
+                const uint32_t cj = min(KC_CHUNK, cnt - j * KC_CHUNK);
+                if (sparse)
+                    scatter_bucket_keys<true, NT>(chunk_src(j), cj, key_lo, bm.width, s_bits, s_sum);
+                else
+                    scatter_bucket_keys<false, NT>(chunk_src(j), cj, key_lo, bm.width, s_bits, s_sum);
+            }
+        } else if (sparse) {
             scatter_bucket_keys<true, NT>(src, cnt, key_lo, bm.width, s_bits, s_sum);
         } else if (src_cap) {  // slab-layout buckets: register loads measured faster (C2, C3)
             scatter_bucket_keys<false, NT>(src, cnt, key_lo, bm.width, s_bits, s_sum);
         } else {
-            const uint32_t head = min(cnt, static_cast<uint32_t>(
-                                               ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
+            // packed: one contiguous range; chunked: the same ring pieces, each
+            // loaded as at most two bulk copies (one per pool chunk it touches)
+            const uint32_t piece = kChunk;
+            static_assert(KC_CHUNK >= kChunk, "a ring piece touches at most two pool chunks");
+            const uint32_t head = chunk_tab ? 0u : min(cnt, static_cast<uint32_t>(
+                                                               ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
             const uint32_t body = (cnt - head) & ~3u;
-            const uint32_t nchunks = (body + kChunk - 1) / kChunk;
+            const uint32_t nchunks = (body + piece - 1) / piece;
             auto set_key = [&](uint32_t key) {
                 const uint32_t x = key - key_lo;
                 atomicOr(s_bits + (x >> 5), 1u << (x & 31));
             };
+            auto at = [&](uint32_t k) {  // address of the bucket's k-th key slot
+                return chunk_tab ? chunk_src(k / KC_CHUNK) + k % KC_CHUNK : src + k;
+            };
             auto issue = [&](uint32_t c) {  // thread 0
                 const unsigned g = chunk_seq + c;
-                const uint32_t len = min(kChunk, body - c * kChunk);
+                const uint32_t len = min(piece, body - c * piece);
+                uint32_t* dst = s_stage_all + (g % KB4_RING) * kChunk;
                 fence_proxy_async_smem();
-                tma_load_bytes(s_stage_all + (g % KB4_RING) * kChunk, src + head + c * kChunk, len * 4,
-                               &s_lbar[g % KB4_RING]);
+                const uint32_t k0 = head + c * piece;
+                const uint32_t first = chunk_tab ? min(len, KC_CHUNK - k0 % KC_CHUNK) : len;
+                if (first == len) {
+                    tma_load_bytes(dst, at(k0), len * 4, &s_lbar[g % KB4_RING]);
+                } else {  // the piece crosses into the next pool chunk: one arrival, two copies
+                    unsigned long long* bar = &s_lbar[g % KB4_RING];
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                                 "r"(len * 4)
+                                 : "memory");
+                    tma_copy_bytes(dst, at(k0), first * 4, bar);
+                    tma_copy_bytes(dst + first, at(k0 + first), (len - first) * 4, bar);
+                }
             };
             if (threadIdx.x == 0) {
                 for (uint32_t q = 0; q < KB4_RING && q < nchunks; ++q) issue(q);
             }
             if (threadIdx.x < head) set_key(__ldcs(src + threadIdx.x));
-            if (threadIdx.x < cnt - head - body) set_key(__ldcs(src + head + body + threadIdx.x));
+            if (threadIdx.x < cnt - head - body) set_key(__ldcs(at(head + body + threadIdx.x)));
             for (uint32_t c = 0; c < nchunks; ++c) {
                 const unsigned g = chunk_seq + c;
                 mbar_wait(&s_lbar[g % KB4_RING], (g / KB4_RING) & 1u);
                 const uint4* r4 = reinterpret_cast<const uint4*>(s_stage_all + (g % KB4_RING) * kChunk);
-                const uint32_t nv = min(kChunk, body - c * kChunk) / 4;
+                const uint32_t nv = min(piece, body - c * piece) / 4;
                 for (uint32_t i = threadIdx.x; i < nv; i += NT) {
                     const uint4 v = r4[i];
                     set_key(v.x);
@@ -1603,6 +1721,24 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
     return slots;
 }
 
+// Chunked layout (the packed layout's replacement for distinct-key sorts:
+// no KB1 histogram read, no KB2): pool slots for n keys in nb buckets.
+constexpr uint32_t kMaxChunksPerBucket = (1u << MAX_BUCKET_SHIFT) / KC_CHUNK + 2;
+uint32_t chunk_max(const BucketPlan& plan, size_t n) {
+    const uint64_t cap = std::min<uint64_t>(plan.map.width, n);
+    return static_cast<uint32_t>((cap + KC_CHUNK - 1) / KC_CHUNK + 1);
+}
+uint64_t chunk_slots(const BucketPlan& plan, size_t n) {
+    static const bool off = [] {
+        const char* e = std::getenv("BITSORT_CHUNK");
+        return e && std::string(e) == "0";
+    }();
+    if (off || plan.partition_only || plan.nb > MAX_BUCKETS) return 0;
+    const uint64_t chunks = static_cast<uint64_t>(n) / KC_CHUNK + plan.nb + 2;
+    const uint64_t slots = chunks * KC_CHUNK;
+    return slots < (1ull << 32) / KC_CHUNK * KC_CHUNK ? slots : 0;
+}
+
 bool slab_in_use(const BucketPlan& plan, size_t n, uint64_t parted_cap) {
     const uint64_t slab = slab_slots(plan, n);
     return slab != 0 && slab <= parted_cap;
@@ -1613,7 +1749,8 @@ size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks) {
            + (MAX_BUCKETS + 1) * sizeof(uint32_t)                          // tot
            + (MAX_BUCKETS + 2) * sizeof(unsigned long long)                // base (8-aligned)
            + MAX_BUCKETS * sizeof(uint32_t)                                // KB4 ticket order
-           + 2 * MAX_BUCKETS * sizeof(uint32_t);                           // slab fill + true counts
+           + 2 * MAX_BUCKETS * sizeof(uint32_t)                            // slab fill + true counts
+           + (8 + static_cast<size_t>(MAX_BUCKETS) * kMaxChunksPerBucket) * sizeof(uint32_t);  // chunks
 }
 
 cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_range, uint32_t* out,
@@ -1649,6 +1786,13 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     const uint64_t slab = slab_slots(plan, n);
     // multiset sorts take the packed layout: exact for any key multiplicity
     const bool use_slab = !multiset && slab != 0 && slab <= parted_cap;
+    // distinct-key sorts that do not fit the slab: the chunked layout (no
+    // KB1/KB2); the multiset, range-split and multi-GPU builds keep the packed one
+    const uint64_t cslots = chunk_slots(plan, n);
+    const bool use_chunk = !use_slab && !multiset && !bits_out && !push && !plan.partition_only &&
+                           inplace_mode == 0 && cslots != 0 && cslots <= parted_cap;
+    uint32_t* pool_next = order_buf + MAX_BUCKETS + 4;  // (order[nb] is written) then the chunk table
+    uint32_t* chunk_tab = pool_next + 4;
     static const bool order_off = [] {
         const char* e = std::getenv("BITSORT_KB4_ORDER");
         return e && std::string(e) == "0";
@@ -1674,7 +1818,36 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (launches) *launches = 1;
         return cudaSuccess;
     }
-    if (use_slab) {
+    if (use_chunk) {
+        const uint32_t maxc = chunk_max(plan, n);
+        err = cudaMemsetAsync(pool_next, 0, (4 + static_cast<size_t>(plan.nb) * maxc) * sizeof(uint32_t), stream);
+        if (err != cudaSuccess) return err;
+        sa.gcnt = gcnt;
+        sa.gtrue = nullptr;
+        sa.cap = maxc * KC_CHUNK;  // more slots means repeated keys: the bucket sorts nothing
+        sa.dump = 0xffffffffu;
+        sa.limit = limit;
+        sa.check = check;
+        sa.ctrl = ctrl;
+        sa.tot = tot;
+        sa.g_base = base;
+        sa.order = kb4_order;
+        sa.chunk_tab = chunk_tab;
+        sa.max_chunks = maxc;
+        sa.pool_next = pool_next;
+        if (timer) timer->before(stream);
+        if (n >= (size_t(1) << 26))  // long shares: 20480-key tiles
+            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, 2>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS, PART_KPT_SLAB), stream>>>(
+                    ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+        else
+            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 2>
+                <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
+                    ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
+        if (timer) timer->after("bucket_partition", stream);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        nlaunch = 1;
+    } else if (use_slab) {
         // KB3 (slab) claims slots with fill counters: no KB1/KB2. The counters
         // are zeroed once at allocation and re-zeroed by the last KB3 CTA.
         sa.gcnt = gcnt;
@@ -1691,15 +1864,15 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
             bucket_partition_tma_kernel<512>
                 <<<P, PART_THREADS, part_tma_smem_bytes(512), stream>>>(ks, plan.map, plan.nb, parted, sa);
         else if (narrow_partition(plan))
-            bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>
+            bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, 1>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         else if (plan.nb <= PART_NARROW_MAXB)  // fewer slot-scan iterations per thread
-            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, true>
+            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, 1>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, PART_NARROW_MAXB, PART_KPT_SLAB), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         else
-            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>
+            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 1>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
                     ks, plan.map, plan.nb, nullptr, nullptr, parted, nullptr, sa);
         if (timer) timer->after("bucket_partition", stream);
@@ -1721,15 +1894,15 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.order = kb4_order;
         if (timer) timer->before(stream);
         if (narrow_partition(plan))
-            bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>
+            bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, 0>
                 <<<P, PART_NARROW_THREADS, part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB), stream>>>(
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
         else if (n >= (size_t(1) << 26))  // long shares: 20480-key tiles (C5 KB3 1449 -> 1376 us)
-            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, false>
+            bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, 0>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS, PART_KPT_SLAB), stream>>>(
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
         else  // short shares (C4: ~7 tiles per CTA): 16384-key tiles keep the tail short
-            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>
+            bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 0>
                 <<<P, PART_THREADS, part_smem_bytes(PART_THREADS, MAX_BUCKETS), stream>>>(
                     ks, plan.map, plan.nb, H, tot, parted, base, sa);
         if (timer) timer->after("bucket_partition", stream);
@@ -1776,10 +1949,12 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     const size_t smem = bucket_sort_smem_bytes(plan.shift);
     if (plan.shift >= MAX_BUCKET_SHIFT)
         bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab);
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
+            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks);
     else  // narrower buckets: two 512-thread CTAs per SM
         bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab);
+            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
+            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;
@@ -1798,27 +1973,36 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     int sms = 0;
     cudaError_t err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, false>,
+    for (auto kern : {bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, 2>}) {
+        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS, PART_KPT_SLAB)));
+        if (err != cudaSuccess) return err;
+    }
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 2>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, MAX_BUCKETS, 0>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS, PART_KPT_SLAB)));
     if (err != cudaSuccess) return err;
-    auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, false>;
-    auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, false>;
+    auto wide = bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 0>;
+    auto narrow = bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, 0>;
     err = cudaFuncSetAttribute(wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, true>,
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_tma_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_tma_smem_bytes(512)));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, true>,
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT_SLAB, PART_NARROW_MAXB, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, PART_NARROW_MAXB, PART_KPT_SLAB)));
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, true>,
+    err = cudaFuncSetAttribute(bucket_partition_kernel<PART_NARROW_THREADS, PART_KPT, PART_NARROW_MAXB, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_NARROW_THREADS, PART_NARROW_MAXB)));
     if (err != cudaSuccess) return err;

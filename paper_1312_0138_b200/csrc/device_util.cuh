@@ -52,6 +52,16 @@ __device__ __forceinline__ void tma_load_bytes(void* dst, const void* src, unsig
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// A bulk global->shared copy completing `bytes` of a transaction the caller
+// has already announced on `bar` (mbarrier.arrive.expect_tx).
+__device__ __forceinline__ void tma_copy_bytes(void* dst, const void* src, unsigned bytes,
+                                               unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 // L2 eviction-priority policies (createpolicy) for cache-hinted accesses.
 __device__ __forceinline__ unsigned long long l2_policy_evict_first() {
     unsigned long long p;

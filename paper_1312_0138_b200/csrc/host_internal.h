@@ -155,9 +155,11 @@ struct DeviceCtx {
     // Bucket buffer for n keys under `plan`: the slab layout's slots when it
     // applies (bws_gpu::slab_slots), else n. Returns the usable capacity.
     size_t ensure_parted(size_t n, const bws_gpu::BucketPlan& plan) {
-        const size_t need = static_cast<size_t>(bws_gpu::slab_slots(plan, n)) > n
-                                ? static_cast<size_t>(bws_gpu::slab_slots(plan, n))
-                                : n;
+        size_t need = static_cast<size_t>(bws_gpu::slab_slots(plan, n)) > n
+                          ? static_cast<size_t>(bws_gpu::slab_slots(plan, n))
+                          : n;
+        if (static_cast<size_t>(bws_gpu::chunk_slots(plan, n)) > need)
+            need = static_cast<size_t>(bws_gpu::chunk_slots(plan, n));
         if (need <= parted_cap) return parted_cap;
         if (parted) cuda_check(cudaFree(parted), "cudaFree(parted)");
         parted = nullptr;

@@ -147,7 +147,12 @@ struct SlabArgs {
                                            // slots, padded to multiples of 4); zeroed like gcnt
     std::uint32_t* order = nullptr;        // packed KB3 (CTA 0): KB4 ticket order, largest
                                            // buckets first; order[nb] = 0 means identity
+    std::uint32_t* chunk_tab = nullptr;    // chunked layout: nb x max_chunks pool chunk ids + 1 (zeroed)
+    std::uint32_t max_chunks = 0;
+    std::uint32_t* pool_next = nullptr;    // chunked layout: next free pool chunk (zeroed)
 };
+constexpr std::uint32_t KC_CHUNK = 8192;          // slots per pool chunk (chunked layout)
+constexpr std::uint32_t KC_DROP = 0xffffffffu;    // a dropped (overflowed) run
 
 // Optional per-kernel timing hook (bench.py's live roofline): before() and
 // after() bracket every kernel launch on the launching stream.
@@ -206,6 +211,8 @@ BucketPlan plan_multiset(std::uint64_t key_range);
 // Bucket-buffer slots the slab layout needs for n keys (0: use the packed
 // histogram layout: the slab would exceed 4n slots or 2^32).
 std::uint64_t slab_slots(const BucketPlan& plan, std::size_t n);
+// Pool slots the chunked layout needs for n keys (0: disabled, BITSORT_CHUNK=0).
+std::uint64_t chunk_slots(const BucketPlan& plan, std::size_t n);
 std::size_t bucket_scratch_bytes(const BucketPlan& plan, int hist_blocks);
 cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo);
 // KB1..KB4: sorts n keys (all < key_range) into out via the `parted` buffer
