@@ -311,9 +311,21 @@ __device__ __forceinline__ uint32_t chunk_alloc(const SlabArgs& sa, uint32_t b, 
 }
 __device__ __forceinline__ uint32_t chunk_get(const SlabArgs& sa, uint32_t b, uint32_t j) {
     const volatile uint32_t* t = sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j;
-    uint32_t v;
+    uint32_t v = *t;
+    if (v) return v - 1u;
+    // the allocating claim precedes ours and every KB3 CTA is resident, so the
+    // entry appears within microseconds; a protocol fault must not hang the
+    // GPU: after 2 s the sort is flagged (Ctrl.error) and this run goes to chunk 0
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while ((v = *t) == 0u) {
-    }  // the allocating claim precedes ours and every KB3 CTA is resident
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 2000000000ull) {
+            atomicExch(&sa.ctrl->error, 1u);
+            return 0u;
+        }
+    }
     return v - 1u;
 }
 
@@ -611,33 +623,47 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         if constexpr (CHUNK) {
             // every chunk whose first slot lies in this tile's run is allocated
             // here (allocation never waits); the run's first chunk, when an
-            // earlier claim owns it, is waited for (all KB3 CTAs are resident)
+            // earlier claim owns it, is waited for (all KB3 CTAs are resident).
+            // Two passes: all of this thread's allocations and table loads are
+            // issued before any result is waited for (the loads' L2 latency
+            // overlaps instead of adding up per bucket).
+            uint32_t id0[PER_MAX];
 #pragma unroll
             for (int q = 0; q < PER_MAX; ++q) {
-                if (ccnt[q]) {
-                    const uint32_t b = sb + q;
-                    const uint32_t cl = claim[q], cb = ccnt[q];
-                    const uint32_t j0 = cl / KC_CHUNK, j1 = (cl + cb - 1) / KC_CHUNK;
-                    if (j1 >= sa.max_chunks) {  // repeated keys overflowed the bucket
-                        sa.ctrl->overflow = 1u;
-                        s_cur[b] = KC_DROP;  // (any 32-bit delta is a valid slot offset)
-                        continue;
+                id0[q] = 0u;
+                if (!ccnt[q]) continue;
+                const uint32_t b = sb + q;
+                const uint32_t cl = claim[q], cb = ccnt[q];
+                const uint32_t j0 = cl / KC_CHUNK, j1 = (cl + cb - 1) / KC_CHUNK;
+                if (j1 >= sa.max_chunks) continue;  // overflow: handled below
+                for (uint32_t j = j0; j <= j1; ++j) {
+                    if (j * KC_CHUNK >= cl) {
+                        const uint32_t id = chunk_alloc(sa, b, j);
+                        if (j == j0) id0[q] = id + 1u;
                     }
-                    uint32_t id0 = 0;
-                    for (uint32_t j = j0; j <= j1; ++j) {
-                        if (j * KC_CHUNK >= cl) {
-                            const uint32_t id = chunk_alloc(sa, b, j);
-                            if (j == j0) id0 = id;
-                        }
-                    }
-                    if (cl % KC_CHUNK != 0) id0 = chunk_get(sa, b, j0);
-                    const uint32_t st = s_start[b];
-                    s_delta[b] = id0 * KC_CHUNK + cl % KC_CHUNK - st;
-                    // tile position where the run leaves its first chunk (0x7fff: never),
-                    // with the next chunk's index above it for the slow path
-                    const uint32_t room = KC_CHUNK - cl % KC_CHUNK;
-                    s_cur[b] = cb > room ? (st + room) | ((j0 + 1) << 15) : 0x7fffu;
                 }
+                if (cl % KC_CHUNK != 0)  // owned by an earlier claim: look it up (0 = not yet)
+                    id0[q] = *reinterpret_cast<const volatile uint32_t*>(
+                        sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j0);
+            }
+#pragma unroll
+            for (int q = 0; q < PER_MAX; ++q) {
+                if (!ccnt[q]) continue;
+                const uint32_t b = sb + q;
+                const uint32_t cl = claim[q], cb = ccnt[q];
+                const uint32_t j0 = cl / KC_CHUNK, j1 = (cl + cb - 1) / KC_CHUNK;
+                if (j1 >= sa.max_chunks) {  // repeated keys overflowed the bucket
+                    sa.ctrl->overflow = 1u;
+                    s_cur[b] = KC_DROP;  // (any 32-bit delta is a valid slot offset)
+                    continue;
+                }
+                const uint32_t id = id0[q] ? id0[q] - 1u : chunk_get(sa, b, j0);
+                const uint32_t st = s_start[b];
+                s_delta[b] = id * KC_CHUNK + cl % KC_CHUNK - st;
+                // tile position where the run leaves its first chunk (0x7fff: never),
+                // with the next chunk's index above it for the slow path
+                const uint32_t room = KC_CHUNK - cl % KC_CHUNK;
+                s_cur[b] = cb > room ? (st + room) | ((j0 + 1) << 15) : 0x7fffu;
             }
         } else if constexpr (SLAB) {
 #pragma unroll

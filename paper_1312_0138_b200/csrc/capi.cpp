@@ -565,9 +565,10 @@ Ctrl read_ctrl(DeviceCtx& ctx, cudaStream_t stream) {
     Ctrl c;
     cuda_check(cudaMemcpy(&c, ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost),
                "control block readback");
-    if (c.error != 0) {  // KF ring protocol timeout: reset the ring state
+    if (c.error != 0) {  // KF ring / chunk-table protocol timeout: reset the ring state
         ctx.fused_dirty = true;
-        throw internal_error("fused sort: ring protocol timeout (state reset)");
+        ctx.bits_dirty = true;  // a KD sort may have stopped before taking its slices
+        throw internal_error("sort protocol timeout (a kernel gave up waiting; state reset)");
     }
     return c;
 }
