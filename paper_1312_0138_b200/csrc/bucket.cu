@@ -300,16 +300,19 @@ __device__ void compute_kb4_order(const uint32_t* __restrict__ tot, int nb, uint
 }
 
 // Chunked layout (packed sorts without KB1/KB2): a bucket's keys live in
-// KC_CHUNK-slot chunks of a pool, chunk j of bucket b at pool chunk
-// chunk_tab[b * max_chunks + j] - 1 (0: not allocated yet). Tiles claim runs
-// in a bucket with one atomicAdd on its fill counter, as in the slab layout;
-// the claim that holds a chunk's first slot allocates it, others wait for it.
-__device__ __forceinline__ uint32_t chunk_alloc(const SlabArgs& sa, uint32_t b, uint32_t j) {
-    const uint32_t id = atomicAdd(sa.pool_next, 1u);
+// 2^chunk_shift-slot chunks of a pool. Chunk 0 of bucket b is pool chunk b
+// (implicit); chunk j >= 1 is pool chunk chunk_tab[b * max_chunks + j] - 1
+// (0: not allocated yet), allocated from pool chunk nb upwards. Tiles claim
+// runs in a bucket with one atomicAdd on its fill counter, as in the slab
+// layout; the claim that holds a chunk's first slot allocates it, others wait.
+__device__ __forceinline__ uint32_t chunk_alloc(const SlabArgs& sa, int nb, uint32_t b, uint32_t j) {
+    if (j == 0) return b;
+    const uint32_t id = static_cast<uint32_t>(nb) + atomicAdd(sa.pool_next, 1u);
     atomicExch(sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j, id + 1u);
     return id;
 }
 __device__ __forceinline__ uint32_t chunk_get(const SlabArgs& sa, uint32_t b, uint32_t j) {
+    if (j == 0) return b;
     const volatile uint32_t* t = sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j;
     uint32_t v = *t;
     if (v) return v - 1u;
@@ -483,10 +486,11 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                     bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
                         const uint32_t pos = atomicAdd(sa.gcnt + b, 1u);
-                        const uint32_t j = pos / KC_CHUNK;
+                        const uint32_t cs = sa.chunk_shift, cm = (1u << cs) - 1u;
+                        const uint32_t j = pos >> cs;
                         if (j < sa.max_chunks) {
-                            const uint32_t id = pos % KC_CHUNK == 0 ? chunk_alloc(sa, b, j) : chunk_get(sa, b, j);
-                            parted[static_cast<size_t>(id) * KC_CHUNK + pos % KC_CHUNK] = e;
+                            const uint32_t id = (pos & cm) == 0 ? chunk_alloc(sa, nb, b, j) : chunk_get(sa, b, j);
+                            parted[(static_cast<size_t>(id) << cs) + (pos & cm)] = e;
                         } else {
                             sa.ctrl->overflow = 1u;
                         }
@@ -628,30 +632,32 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             // issued before any result is waited for (the loads' L2 latency
             // overlaps instead of adding up per bucket).
             uint32_t id0[PER_MAX];
+            const uint32_t cs = sa.chunk_shift, cm = (1u << cs) - 1u;
 #pragma unroll
             for (int q = 0; q < PER_MAX; ++q) {
                 id0[q] = 0u;
                 if (!ccnt[q]) continue;
                 const uint32_t b = sb + q;
                 const uint32_t cl = claim[q], cb = ccnt[q];
-                const uint32_t j0 = cl / KC_CHUNK, j1 = (cl + cb - 1) / KC_CHUNK;
+                const uint32_t j0 = cl >> cs, j1 = (cl + cb - 1) >> cs;
                 if (j1 >= sa.max_chunks) continue;  // overflow: handled below
                 for (uint32_t j = j0; j <= j1; ++j) {
-                    if (j * KC_CHUNK >= cl) {
-                        const uint32_t id = chunk_alloc(sa, b, j);
+                    if ((j << cs) >= cl) {
+                        const uint32_t id = chunk_alloc(sa, nb, b, j);
                         if (j == j0) id0[q] = id + 1u;
                     }
                 }
-                if (cl % KC_CHUNK != 0)  // owned by an earlier claim: look it up (0 = not yet)
-                    id0[q] = *reinterpret_cast<const volatile uint32_t*>(
-                        sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j0);
+                if ((cl & cm) != 0)  // owned by an earlier claim: look it up (0 = not yet)
+                    id0[q] = j0 == 0 ? b + 1u
+                                     : *reinterpret_cast<const volatile uint32_t*>(
+                                           sa.chunk_tab + static_cast<size_t>(b) * sa.max_chunks + j0);
             }
 #pragma unroll
             for (int q = 0; q < PER_MAX; ++q) {
                 if (!ccnt[q]) continue;
                 const uint32_t b = sb + q;
                 const uint32_t cl = claim[q], cb = ccnt[q];
-                const uint32_t j0 = cl / KC_CHUNK, j1 = (cl + cb - 1) / KC_CHUNK;
+                const uint32_t j0 = cl >> cs, j1 = (cl + cb - 1) >> cs;
                 if (j1 >= sa.max_chunks) {  // repeated keys overflowed the bucket
                     sa.ctrl->overflow = 1u;
                     s_cur[b] = KC_DROP;  // (any 32-bit delta is a valid slot offset)
@@ -659,10 +665,11 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 }
                 const uint32_t id = id0[q] ? id0[q] - 1u : chunk_get(sa, b, j0);
                 const uint32_t st = s_start[b];
-                s_delta[b] = id * KC_CHUNK + cl % KC_CHUNK - st;
-                // tile position where the run leaves its first chunk (0x7fff: never),
-                // with the next chunk's index above it for the slow path
-                const uint32_t room = KC_CHUNK - cl % KC_CHUNK;
+                s_delta[b] = (id << cs) + (cl & cm) - st;
+                // tile position where the run leaves its first chunk (0x7fff: never;
+                // a crossing lies inside the tile, so it fits 15 bits), with the
+                // next chunk's index above it for the slow path
+                const uint32_t room = (1u << cs) - (cl & cm);
                 s_cur[b] = cb > room ? (st + room) | ((j0 + 1) << 15) : 0x7fffu;
             }
         } else if constexpr (SLAB) {
@@ -701,8 +708,8 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 size_t dst = d + i;  // (32-bit wrap: d is the slot minus the tile position)
                 if (i >= (x & 0x7fffu)) {  // past the run's first chunk (rare)
                     const uint32_t k2 = i - (x & 0x7fffu);
-                    const uint32_t id = chunk_get(sa, b, (x >> 15) + k2 / KC_CHUNK);
-                    dst = static_cast<size_t>(id) * KC_CHUNK + k2 % KC_CHUNK;
+                    const uint32_t id = chunk_get(sa, b, (x >> 15) + (k2 >> sa.chunk_shift));
+                    dst = (static_cast<size_t>(id) << sa.chunk_shift) + (k2 & ((1u << sa.chunk_shift) - 1u));
                 }
                 st_hint(parted + dst, key, pol);
             }
@@ -1034,7 +1041,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl,
                        const uint32_t* __restrict__ order, int all_or_nothing,
-                       const uint32_t* __restrict__ chunk_tab, uint32_t max_chunks) {
+                       const uint32_t* __restrict__ chunk_tab, uint32_t max_chunks, uint32_t chunk_shift) {
     // in-place sorts: a slab that lost runs (repeated keys overflowed a
     // bucket) writes nothing, so the input stays intact for the counting pass
     if (all_or_nothing && *reinterpret_cast<volatile const uint32_t*>(&ctrl->overflow)) return;
@@ -1104,13 +1111,15 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         const uint32_t* src = parted + (src_cap ? static_cast<size_t>(b) * src_cap : base);  // slab / packed
         const bool sparse = static_cast<unsigned long long>(cnt) * 4 < W;
         const uint32_t key_lo = bm.lo + static_cast<uint32_t>(b) * bm.width;
-        // chunked layout: the bucket's keys are KC_CHUNK-slot pool chunks
+        // chunked layout: the bucket's keys are 2^chunk_shift-slot pool chunks
+        const uint32_t CH = 1u << chunk_shift;
         auto chunk_src = [&](uint32_t j) {
-            return parted + static_cast<size_t>(chunk_tab[static_cast<size_t>(b) * max_chunks + j] - 1u) * KC_CHUNK;
+            const uint32_t id = j == 0 ? b : chunk_tab[static_cast<size_t>(b) * max_chunks + j] - 1u;
+            return parted + (static_cast<size_t>(id) << chunk_shift);
         };
-        if (chunk_tab && (sparse || cnt <= 2 * KC_CHUNK)) {
-            for (uint32_t j = 0; j * KC_CHUNK < cnt; ++j) {
-                const uint32_t cj = min(KC_CHUNK, cnt - j * KC_CHUNK);
+        if (chunk_tab && (sparse || cnt <= 2 * CH)) {
+            for (uint32_t j = 0; j * CH < cnt; ++j) {
+                const uint32_t cj = min(CH, cnt - j * CH);
                 if (sparse)
                     scatter_bucket_keys<true, NT>(chunk_src(j), cj, key_lo, bm.width, s_bits, s_sum);
                 else
@@ -1124,7 +1133,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
             // packed: one contiguous range; chunked: the same ring pieces, each
             // loaded as at most two bulk copies (one per pool chunk it touches)
             const uint32_t piece = kChunk;
-            static_assert(KC_CHUNK >= kChunk, "a ring piece touches at most two pool chunks");
+            static_assert(KC_CHUNK_MIN >= kChunk, "a ring piece touches at most two pool chunks");
             const uint32_t head = chunk_tab ? 0u : min(cnt, static_cast<uint32_t>(
                                                                ((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4));
             const uint32_t body = (cnt - head) & ~3u;
@@ -1134,7 +1143,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                 atomicOr(s_bits + (x >> 5), 1u << (x & 31));
             };
             auto at = [&](uint32_t k) {  // address of the bucket's k-th key slot
-                return chunk_tab ? chunk_src(k / KC_CHUNK) + k % KC_CHUNK : src + k;
+                return chunk_tab ? chunk_src(k >> chunk_shift) + (k & (CH - 1u)) : src + k;
             };
             auto issue = [&](uint32_t c) {  // thread 0
                 const unsigned g = chunk_seq + c;
@@ -1142,7 +1151,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                 uint32_t* dst = s_stage_all + (g % KB4_RING) * kChunk;
                 fence_proxy_async_smem();
                 const uint32_t k0 = head + c * piece;
-                const uint32_t first = chunk_tab ? min(len, KC_CHUNK - k0 % KC_CHUNK) : len;
+                const uint32_t first = chunk_tab ? min(len, CH - (k0 & (CH - 1u))) : len;
                 if (first == len) {
                     tma_load_bytes(dst, at(k0), len * 4, &s_lbar[g % KB4_RING]);
                 } else {  // the piece crosses into the next pool chunk: one arrival, two copies
@@ -1749,10 +1758,19 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
 
 // Chunked layout (the packed layout's replacement for distinct-key sorts:
 // no KB1 histogram read, no KB2): pool slots for n keys in nb buckets.
-constexpr uint32_t kMaxChunksPerBucket = (1u << MAX_BUCKET_SHIFT) / KC_CHUNK + 2;
+constexpr uint32_t kMaxChunksPerBucket = (1u << MAX_BUCKET_SHIFT) / KC_CHUNK_MIN + 2;
+// Chunk size: about a quarter of a bucket's mean key count (few allocations,
+// at most a quarter-bucket of pool slots wasted per bucket), 2^13 .. 2^16.
+uint32_t chunk_shift(const BucketPlan& plan, size_t n) {
+    const uint64_t per = static_cast<uint64_t>(n) / (4ull * static_cast<uint64_t>(plan.nb));
+    uint32_t s = 13;
+    while (s < 16 && (uint64_t(1) << (s + 1)) <= per) ++s;
+    return s;
+}
 uint32_t chunk_max(const BucketPlan& plan, size_t n) {
     const uint64_t cap = std::min<uint64_t>(plan.map.width, n);
-    return static_cast<uint32_t>((cap + KC_CHUNK - 1) / KC_CHUNK + 1);
+    const uint64_t ch = uint64_t(1) << chunk_shift(plan, n);
+    return static_cast<uint32_t>((cap + ch - 1) / ch + 1);
 }
 uint64_t chunk_slots(const BucketPlan& plan, size_t n) {
     static const bool off = [] {
@@ -1760,9 +1778,10 @@ uint64_t chunk_slots(const BucketPlan& plan, size_t n) {
         return e && std::string(e) == "0";
     }();
     if (off || plan.partition_only || plan.nb > MAX_BUCKETS) return 0;
-    const uint64_t chunks = static_cast<uint64_t>(n) / KC_CHUNK + plan.nb + 2;
-    const uint64_t slots = chunks * KC_CHUNK;
-    return slots < (1ull << 32) / KC_CHUNK * KC_CHUNK ? slots : 0;
+    const uint64_t ch = uint64_t(1) << chunk_shift(plan, n);
+    const uint64_t chunks = static_cast<uint64_t>(n) / ch + plan.nb + 2;  // implicit chunk 0 per bucket
+    const uint64_t slots = chunks * ch;
+    return slots < (1ull << 32) - ch ? slots : 0;
 }
 
 bool slab_in_use(const BucketPlan& plan, size_t n, uint64_t parted_cap) {
@@ -1850,7 +1869,8 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         if (err != cudaSuccess) return err;
         sa.gcnt = gcnt;
         sa.gtrue = nullptr;
-        sa.cap = maxc * KC_CHUNK;  // more slots means repeated keys: the bucket sorts nothing
+        sa.chunk_shift = chunk_shift(plan, n);
+        sa.cap = maxc << sa.chunk_shift;  // more slots means repeated keys: the bucket sorts nothing
         sa.dump = 0xffffffffu;
         sa.limit = limit;
         sa.check = check;
@@ -1976,11 +1996,11 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (plan.shift >= MAX_BUCKET_SHIFT)
         bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
             parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
-            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks);
+            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift);
     else  // narrower buckets: two 512-thread CTAs per SM
         bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
             parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
-            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks);
+            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;

@@ -149,9 +149,10 @@ struct SlabArgs {
                                            // buckets first; order[nb] = 0 means identity
     std::uint32_t* chunk_tab = nullptr;    // chunked layout: nb x max_chunks pool chunk ids + 1 (zeroed)
     std::uint32_t max_chunks = 0;
-    std::uint32_t* pool_next = nullptr;    // chunked layout: next free pool chunk (zeroed)
+    std::uint32_t* pool_next = nullptr;    // chunked layout: next free pool chunk - nb (zeroed)
+    std::uint32_t chunk_shift = 13;        // chunked layout: log2 slots per pool chunk
 };
-constexpr std::uint32_t KC_CHUNK = 8192;          // slots per pool chunk (chunked layout)
+constexpr std::uint32_t KC_CHUNK_MIN = 8192;      // smallest pool chunk (chunked layout)
 constexpr std::uint32_t KC_DROP = 0xffffffffu;    // a dropped (overflowed) run
 
 // Optional per-kernel timing hook (bench.py's live roofline): before() and
