@@ -100,8 +100,9 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// the published counts carry no other data: relaxed stores (no release fence)
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 // ring entries are read from L2 (another SM wrote them)
 __device__ __forceinline__ uint4 ld_ring(const uint32_t* p) {
@@ -204,13 +205,13 @@ __global__ void __launch_bounds__(KF_THREADS, 1) fused_sort_kernel(FusedArgs a) 
         s_bad = 0;
         s_spin[0] = s_spin[1] = 0;
     }
-    {
+    if (!a.gbits) {  // ring mode (KD overwrites its slice from the global bitset)
         uint4* b4 = reinterpret_cast<uint4*>(s_bits);
         for (uint32_t i = threadIdx.x; i < Sw / 4; i += KF_THREADS) b4[i] = make_uint4(0, 0, 0, 0);
+        for (uint32_t i = threadIdx.x; i <= G; i += KF_THREADS) s_cnt[i] = 0;
+        for (uint32_t i = threadIdx.x; i < 2 * G; i += KF_THREADS)
+            s_headc[i] = ld_relaxed(a.head + ring_index(i / G, i % G, sub));
     }
-    for (uint32_t i = threadIdx.x; i <= G; i += KF_THREADS) s_cnt[i] = 0;
-    for (uint32_t i = threadIdx.x; i < 2 * G; i += KF_THREADS)
-        s_headc[i] = ld_acquire(a.head + ring_index(i / G, i % G, sub));
     __syncthreads();
 
     if (a.gbits) {
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(KF_THREADS, 1) fused_sort_kernel(FusedArgs a) 
         if (threadIdx.x == 0) {
             uint32_t tot = 0;
             for (int w = 0; w < KF_THREADS / 32; ++w) tot += s_warp[w];
-            st_release64(a.counts + c, (1ull << 63) | tot);
+            st_relaxed64(a.counts + c, (1ull << 63) | tot);
             if (tr) tr[kTrCons0] = now_ns();
         }
     } else if (threadIdx.x < KF_PROD) {
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(KF_THREADS, 1) fused_sort_kernel(FusedArgs a) 
             if (ct == 0) {
                 uint32_t tot = 0;
                 for (int w = 0; w < KF_CONS_WARPS; ++w) tot += s_cons_cnt[w];
-                st_release64(a.counts + p * G + c, (1ull << 63) | tot);
+                st_relaxed64(a.counts + p * G + c, (1ull << 63) | tot);
                 if (tr) tr[p == 0 ? kTrCons0 : kTrCons1] = now_ns();
             }
             if (p + 1 < P) {  // keep the pass-0 slice for the end; clear for pass 1
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(KF_THREADS, 1) fused_sort_kernel(FusedArgs a) 
     if (warp == 0) {
         if (tr && lane == 0) tr[kTrProdSpin] = now_ns();  // (slot reused: offsets phase entered)
         // publish the bad-key count with the counts, then read every CTA's
-        if (lane == 0) st_release64(a.counts + 2 * G + c, (1ull << 63) | s_bad);
+        if (lane == 0) st_relaxed64(a.counts + 2 * G + c, (1ull << 63) | s_bad);
         unsigned long long before[2] = {0, 0}, tot[2] = {0, 0}, bad = 0;
         constexpr int kPer = (3 * KF_MAXG + 31) / 32;
         unsigned long long w[kPer];
@@ -723,14 +724,20 @@ __global__ void __launch_bounds__(KF_THREADS, 1) fused_sort_kernel(FusedArgs a) 
 
     // --------------------------------------------------------------- teardown
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (tr) tr[kTrEnd] = now_ns();
-        __threadfence();
-        if (atomicAdd(a.sync + 2, 1u) == G - 1) {  // last CTA out: reset the per-launch counters
-            a.sync[0] = 0;
-            a.sync[1] = 0;
-            for (uint32_t i = 0; i < 3 * G; ++i) a.counts[i] = 0;
-            a.sync[2] = 0;
+    if (warp == 0) {
+        uint32_t last = 0;
+        if (lane == 0) {
+            if (tr) tr[kTrEnd] = now_ns();
+            __threadfence();
+            last = atomicAdd(a.sync + 2, 1u) == G - 1;
+        }
+        if (__shfl_sync(kFull, last, 0)) {  // last CTA out: reset the per-launch counters
+            for (uint32_t i = lane; i < 3 * G; i += 32) a.counts[i] = 0;
+            if (lane == 0) {
+                a.sync[0] = 0;
+                a.sync[1] = 0;
+                a.sync[2] = 0;
+            }
             __threadfence();
         }
     }
