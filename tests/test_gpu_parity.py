@@ -887,3 +887,38 @@ def test_async_without_hint_is_graph_capturable(capi, cuda):
     s.synchronize()
     assert capi.sort_check(s.cuda_stream) == n
     assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys))
+
+
+@pytest.mark.parametrize("layout", ["uniform", "clustered", "sorted"])
+def test_chunked_layout(capi, cuda, layout):
+    """Distinct keys over 2^32 that do not fit the slab take the chunked
+    layout (no KB1 histogram): runs claimed into pool chunks allocated on
+    first touch, including runs longer than a chunk (sorted / clustered)."""
+    capi.set_path(capi.Path.BUCKETED)
+    rng = np.random.default_rng(23)
+    n = (1 << 22) + 5
+    if layout == "uniform":
+        keys = np.unique(rng.integers(0, 1 << 32, size=n + n // 64, dtype=np.uint64).astype(np.uint32))[:n]
+        rng.shuffle(keys)
+    elif layout == "clustered":  # 64 dense clusters, cluster-ordered
+        centres = rng.choice((1 << 32) - (1 << 20), size=64, replace=False)
+        keys = np.unique(np.concatenate([c + rng.choice(1 << 19, size=n // 64 + 1, replace=False)
+                                         for c in centres]).astype(np.uint32))
+        keys = np.concatenate([np.sort(keys[i::64]) for i in range(64)])
+    else:
+        keys = np.sort(np.unique(rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)))
+    s = cuda.cuda.current_stream().cuda_stream
+    d = cuda.from_numpy(keys.view(np.int32)).cuda()
+    out = cuda.full((keys.size + 4,), -1, dtype=cuda.int32, device="cuda")
+    capi.set_kernel_timing(True)
+    capi.kernel_timings()
+    try:
+        capi.sort_device_async(d.data_ptr(), keys.size, out.data_ptr(), 1 << 32, s)
+        assert capi.sort_check(s) == keys.size
+        kernels = capi.kernel_timings()
+    finally:
+        capi.set_kernel_timing(False)
+    assert "bucket_hist" not in kernels and "bucket_partition" in kernels, kernels
+    got = out.cpu().numpy().view(np.uint32)
+    assert got[keys.size:].tolist() == [0xFFFFFFFF] * 4
+    assert np.array_equal(got[: keys.size], np.sort(keys))
