@@ -337,12 +337,16 @@ __device__ __forceinline__ uint32_t chunk_get(const SlabArgs& sa, uint32_t b, ui
 // bucket totals (0 for an overflowed bucket: its keys are lost, so the sort
 // sees fewer set bits than keys) and output offsets for KB4. `s_vals` holds
 // nb uint32, `s_out64` nb uint64 (both SMEM).
-__device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t bad, uint32_t* s_vals,
-                                            unsigned long long* s_out64, unsigned long long* s_scratch,
-                                            uint32_t* s_last) {
+__device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t bad, uint32_t kmax,
+                                            uint32_t* s_vals, unsigned long long* s_out64,
+                                            unsigned long long* s_scratch, uint32_t* s_last) {
     const unsigned lane = threadIdx.x & 31;
     const uint32_t wb = __reduce_add_sync(kFull, bad);
     if (lane == 0 && wb) atomicAdd(&sa.ctrl->bad_keys, wb);
+    // the largest key seen (biased key, like K0's ctrl->max_key): the host
+    // learns the true range of a sort that ran on a speculated one
+    const uint32_t wm = __reduce_max_sync(kFull, kmax);
+    if (lane == 0 && wm) atomicMax(&sa.ctrl->max_key, wm);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -351,6 +355,9 @@ __device__ __forceinline__ void slab_finish(const SlabArgs& sa, int nb, uint32_t
     __syncthreads();
     if (!*s_last) return;
     __threadfence();
+    // keys beyond the range were left out of the slabs: an in-place KB4 must
+    // write nothing then (the caller redoes the sort from the intact keys)
+    if (threadIdx.x == 0 && *reinterpret_cast<volatile const uint32_t*>(&sa.ctrl->bad_keys)) sa.ctrl->overflow = 1u;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         const uint32_t v = __ldcg(sa.gcnt + b);
         const bool ok = v <= sa.cap;
@@ -457,6 +464,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 
     unsigned long long* s_base64 = reinterpret_cast<unsigned long long*>(s_cnt);  // spans cnt+start
     uint32_t bad = 0;  // slab: keys >= sa.limit (KB1 counts them in the packed layout)
+    uint32_t kmax = 0;  // slab: largest (biased) key this thread saw
     if constexpr (!SLAB) {
         // bucket bases (exclusive prefix of totals) + this CTA's first slot per bucket
         for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cur[b] = tot[b];
@@ -482,6 +490,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             for (int i = 0; i < ne; ++i) {
                 const uint32_t e = extra[i] ^ ks.xr;
                 const uint32_t b = slot_of(e, true);
+                kmax = max(kmax, e);
                 if constexpr (CHUNK) {
                     bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
                     if (b != spill) {
@@ -545,6 +554,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
         // every key of the warp step below the fast limit (and no padding
         // lanes): buckets without per-key range checks
         if (__all_sync(kFull, all_in) && rmax <= fast_last) {
+            if constexpr (SLAB) kmax = max(kmax, rmax + bm.lo);
 #pragma unroll
             for (int q = 0; q < KPT; ++q) rb[q] = __umulhi(((k[q] - bm.lo) >> bm.ms) << 12, bm.mq);
         } else {
@@ -552,7 +562,10 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             for (int j = 0; j < VPT; ++j) {
                 const bool in = j * THREADS + threadIdx.x < nvec;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) rb[4 * j + q] = slot_of(k[4 * j + q], in);
+                for (int q = 0; q < 4; ++q) {
+                    rb[4 * j + q] = slot_of(k[4 * j + q], in);
+                    if constexpr (SLAB) kmax = max(kmax, in ? k[4 * j + q] : 0u);
+                }
             }
         }
         const uint32_t blo = slot_of(rmin + bm.lo, true);
@@ -733,7 +746,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
         }
     }
-    if constexpr (SLAB) slab_finish(sa, nb, bad, s_cur, s_base64, s_scratch, &s_last);
+    if constexpr (SLAB) slab_finish(sa, nb, bad, kmax, s_cur, s_base64, s_scratch, &s_last);
 }
 
 
@@ -806,6 +819,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
     if (threadIdx.x == 0)
         for (size_t t = 0; t < 2 && t < ntiles; ++t) load_tile(t, static_cast<int>(t));
     uint32_t bad = 0;
+    uint32_t kmax = 0;  // largest (biased) key this thread saw
     if (threadIdx.x == 0) {  // misaligned head (CTA 0) / tail (CTA P-1): one padded claim each
         const uint32_t* extra = c == 0 ? ks.head : nullptr;
         int ne = c == 0 ? ks.n_head : 0;
@@ -813,6 +827,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             for (int i = 0; i < ne; ++i) {
                 const uint32_t e = extra[i] ^ ks.xr;
                 bad += (sa.check && e - bm.lo >= sa.limit) ? 1u : 0u;
+                kmax = max(kmax, e);
                 const uint32_t b = slot_of(e, true);
                 if (b == spill) continue;
                 atomicAdd(sa.gtrue + b, 1u);
@@ -862,6 +877,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         // a warp step with every key in range (and no padding lanes) needs no
         // per-key range check: the common case
         if (__all_sync(kFull, all_in) && rmax <= last) {
+            kmax = max(kmax, rmax + bm.lo);
 #pragma unroll
             for (int q = 0; q < KPT; ++q) rb[q] = __umulhi(((k[q] - bm.lo) >> bm.ms) << 12, bm.mq);
         } else {
@@ -869,7 +885,10 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
             for (int j = 0; j < VPT; ++j) {
                 const bool in = j * THREADS + threadIdx.x < nvec;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) rb[4 * j + q] = slot_of(k[4 * j + q], in);
+                for (int q = 0; q < 4; ++q) {
+                    rb[4 * j + q] = slot_of(k[4 * j + q], in);
+                    kmax = max(kmax, in ? k[4 * j + q] : 0u);
+                }
             }
         }
         const uint32_t blo = slot_of(rmin + bm.lo, true);
@@ -968,7 +987,7 @@ __global__ void __launch_bounds__(PART_THREADS, 1)
         if (stores_pending) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     if (stores_pending) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    slab_finish(sa, nb, bad, s_cnt, reinterpret_cast<unsigned long long*>(s_sorted), s_scratch, &s_last);
+    slab_finish(sa, nb, bad, kmax, s_cnt, reinterpret_cast<unsigned long long*>(s_sorted), s_scratch, &s_last);
 }
 
 constexpr std::size_t part_tma_smem_bytes(int maxb) {

@@ -666,6 +666,27 @@ size_t multi_min_keys() {
                             std::to_string(limit) + " keys");
 }
 
+// BITSORT_SPECULATE=0: every in-place device-array sort without a hint runs K0.
+bool speculate_range() {
+    static const bool on = [] {
+        const char* e = std::getenv("BITSORT_SPECULATE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// The range planned for after a sort whose keys had `range`: rounded up to 1/64
+// of the enclosing power of two, so the next array of the same kind (its
+// largest key a little above or below) still fits, capped at 2^32.
+uint64_t spec_round(uint64_t range) {
+    if (range == 0) return 0;
+    uint64_t p = 1;
+    while (p < range) p <<= 1;
+    const uint64_t g = p >> 6 ? p >> 6 : 1;
+    const uint64_t r = (range + g - 1) / g * g;
+    return r > kMaxKeyRange ? kMaxKeyRange : r;
+}
+
 // span_limit != 0 (BWS_ALG_COUNTING): K0 first folds min and max on the
 // device; a span >= span_limit is BWS_ERROR_RANGE with the data untouched,
 // otherwise max + 1 becomes the sort's key-range hint.
@@ -709,6 +730,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     } restore{prev};
     ctx.init(device);
     uint32_t* keys = static_cast<uint32_t*>(data);
+    const uint64_t hinted_range = key_range;  // 0: the caller gave no range
     auto check_span = [&](const uint32_t* dk) {
         if (span_limit == 0) return;
         wait_done(ctx, ctx.stream);
@@ -768,11 +790,41 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
             (path == BWS_PATH_AUTO || path == BWS_PATH_BUCKETED)) {
             wait_done(ctx, ctx.stream);
             preserve_pending(ctx, ctx.stream);
-            if (key_range == 0) key_range = derive_range(ctx, keys, count, ctx.stream, xr);
+            // No hint: instead of K0 (a read of every key plus a host round
+            // trip before KB3 can be planned) the sort is planned for the range
+            // the previous such sort's keys had (KB3 folds the largest key it
+            // sees, ctrl->max_key). Keys beyond a speculated range are counted
+            // as bad and make the in-place KB4 write nothing, so a miss costs
+            // one KB3 and is redone from the intact keys with K0's range.
+            bool speculated = false;
+            if (key_range == 0) {
+                if (ctx.spec_range != 0 && speculate_range()) {
+                    key_range = ctx.spec_range;
+                    speculated = true;
+                } else {
+                    key_range = derive_range(ctx, keys, count, ctx.stream, xr);
+                }
+            }
+            if (speculated && !bucketed_slab(ctx, count, key_range, xr)) {
+                key_range = derive_range(ctx, keys, count, ctx.stream, xr);
+                speculated = false;
+            }
             if (bucketed_slab(ctx, count, key_range, xr)) {
                 enqueue_bucketed(ctx, keys, count, keys, key_range, ctx.stream, 0, xr, false, /*inplace=*/1);
-                const Ctrl c = read_ctrl(ctx, ctx.stream);
+                Ctrl c = read_ctrl(ctx, ctx.stream);
+                if (speculated && c.bad_keys != 0) {  // the keys outgrew the speculated range
+                    ctx.spec_range = 0;
+                    key_range = derive_range(ctx, keys, count, ctx.stream, xr);
+                    speculated = false;
+                    if (!bucketed_slab(ctx, count, key_range, xr)) {
+                        ctx.spec_range = spec_round(key_range);
+                        goto out_of_place;
+                    }
+                    enqueue_bucketed(ctx, keys, count, keys, key_range, ctx.stream, 0, xr, false, /*inplace=*/1);
+                    c = read_ctrl(ctx, ctx.stream);
+                }
                 throw_bad_keys(c, key_range);
+                if (hinted_range == 0) ctx.spec_range = spec_round(static_cast<uint64_t>(c.max_key) + 1);
                 if (c.total == count) return;
                 if (count >= (size_t(1) << 32)) throw std::out_of_range("sorting repeated keys takes fewer than 2^32 keys");
                 ms_range = key_range;
@@ -785,6 +837,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
                 return;
             }
         }
+    out_of_place:
         ctx.ensure_keys(count);
         enqueue(keys, ctx.keys);
         if (needs_multiset()) {

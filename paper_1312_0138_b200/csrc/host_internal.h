@@ -99,6 +99,10 @@ struct DeviceCtx {
         uint64_t range = 0;  // 0 = derived
         bool snapped = false;
     } pending;
+    // key range the next in-place bws_sort of a device array without a hint is
+    // planned for (0: none yet, K0 derives it): the range the previous such
+    // sort's keys really had, rounded up — see sort_u32
+    uint64_t spec_range = 0;
     void* bounce[2] = {nullptr, nullptr};  // pinned staging for pageable host arrays
     cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
     cudaEvent_t done = nullptr;   // recorded after every queued sort: orders the

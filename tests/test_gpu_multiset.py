@@ -171,3 +171,33 @@ def test_device_array_in_place(capi, cuda, case, offset):
     assert np.array_equal(got, np.sort(keys)), case
     if case != "distinct" and oracle.REFERENCE is not None:
         assert np.array_equal(got, _reference(keys, is_unsigned))
+
+
+def test_device_array_speculated_range(capi, cuda):
+    """An in-place device-array bws_sort without a hint plans for the range the
+    previous such sort's keys had instead of running K0 (KB3 folds the largest
+    key). Sequences that grow, shrink and repeat the range, with repeats and
+    signed keys in between: every result against numpy; a sort whose keys
+    outgrow the speculated range is redone from the intact keys."""
+    rng = np.random.default_rng(77)
+    n = (1 << 22) + 1
+    def distinct(m):
+        return rng.choice(m, size=n, replace=False).astype(np.uint32)
+    seq = [
+        ("first", distinct(1 << 23), 1),
+        ("same range", distinct(1 << 23), 1),
+        ("grown 2x", distinct(1 << 24), 1),           # beyond the speculated range: redone in place
+        ("grown 16x", distinct(1 << 27), 1),          # beyond it again, and too wide for the slab
+        ("shrunk", distinct(1 << 23), 1),             # inside it: sorted on the wide plan
+        ("shrunk again", distinct(1 << 23), 1),       # now planned for 2^23
+        ("one key above", np.concatenate([distinct(1 << 23)[:-1], [np.uint32((1 << 30) + 5)]]).astype(np.uint32), 1),
+        ("repeats", rng.integers(0, 1 << 23, size=n, dtype=np.uint64).astype(np.uint32), 1),
+        ("signed", rng.integers(-(1 << 22), 1 << 22, size=n, dtype=np.int64).astype(np.int32), 0),
+        ("unsigned after signed", distinct(1 << 24), 1),
+        ("top of the range", (np.uint32(0xffffffff) - distinct(1 << 23)).astype(np.uint32), 1),
+        ("small after top", distinct(1 << 23), 1),
+    ]
+    for name, keys, is_unsigned in seq:
+        for offset in (0, 1):
+            got = _sort_device(capi, cuda, keys, is_unsigned, offset)
+            assert np.array_equal(got, np.sort(keys)), name
