@@ -133,7 +133,7 @@ typedef enum bws_scatter_mode {
 BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
 
 /* Sort pipeline for bws_sort / bws_sort_u32_range / bws_gpu_sort_device_async
- * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed|fused|fused_direct).
+ * (default BWS_PATH_AUTO, or env BITSORT_PATH=auto|direct|bucketed|fused|fused_direct|small).
  *   DIRECT   : K2 global-bitset scatter + K3 decoupled-lookback scan
  *   BUCKETED : key-range bucketing (coalesced) + per-bucket SMEM bitset +
  *              fused extraction; no global bitset
@@ -144,14 +144,19 @@ BITSORT_API bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode);
  *   FUSED_DIRECT : one persistent kernel: keys ORed into the global bitset
  *              (L2-resident), a grid barrier, then every SM counts and
  *              extracts its slice in shared memory (small sorts)
- *   AUTO     : FUSED_DIRECT for hinted sorts of 2^16..2^20 keys whose range
- *              fits it, else BUCKETED for n >= 2^21 and DIRECT below */
+ *   SMALL    : one cooperative launch for small sorts with a range hint: keys
+ *              ORed into the global bitset, a grid barrier, every SM counts
+ *              its slice in registers, tagged count exchange, extraction
+ *              straight from registers (ranges up to 2^27 on a 148-SM B200)
+ *   AUTO     : BUCKETED for n >= 2^21; below, SMALL when a range hint of at
+ *              most 2^25 is given, else DIRECT */
 typedef enum bws_path {
     BWS_PATH_AUTO = 0,
     BWS_PATH_DIRECT = 1,
     BWS_PATH_BUCKETED = 2,
     BWS_PATH_FUSED = 3,
-    BWS_PATH_FUSED_DIRECT = 4
+    BWS_PATH_FUSED_DIRECT = 4,
+    BWS_PATH_SMALL = 5
 } bws_path;
 BITSORT_API bws_status bws_gpu_set_path(bws_path path);
 

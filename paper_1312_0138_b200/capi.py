@@ -62,6 +62,7 @@ class Path(enum.IntEnum):
     BUCKETED = 2
     FUSED = 3
     FUSED_DIRECT = 4
+    SMALL = 5
 
 
 class BitsortError(RuntimeError):

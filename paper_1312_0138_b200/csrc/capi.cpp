@@ -84,6 +84,7 @@ int current_path() {
     if (env && std::strcmp(env, "bucketed") == 0) p = BWS_PATH_BUCKETED;
     if (env && std::strcmp(env, "fused") == 0) p = BWS_PATH_FUSED;
     if (env && std::strcmp(env, "fused_direct") == 0) p = BWS_PATH_FUSED_DIRECT;
+    if (env && std::strcmp(env, "small") == 0) p = BWS_PATH_SMALL;
     g_path.store(p);
     return p;
 }
@@ -516,6 +517,75 @@ void enqueue_fused(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
     record_done(ctx, stream);
 }
 
+// KS: one cooperative launch for a small hinted sort (small.cu). The last CTA
+// writes the control block, so nothing is reset before the launch.
+void enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out, uint64_t key_range,
+                   const bws_gpu::SmallPlan& plan, cudaStream_t stream, uint32_t key_lo = 0) {
+    NvtxRange nvtx_range("bitsort:small KS");
+    wait_done(ctx, stream);
+    preserve_pending(ctx, stream);
+    ctx.ensure_bits();
+    if (ctx.bits_dirty) {
+        cuda_check(cudaMemsetAsync(ctx.bits, 0, kMaxWords * sizeof(uint32_t), stream), "bitset reset");
+        ctx.bits_dirty = false;
+    }
+    const uint32_t epoch = ctx.next_small_epoch(stream);
+    bws_gpu::KeySplit ks;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
+    size_t n_head = ((16 - (addr & 15)) & 15) / 4;
+    if (n_head > count) n_head = count;
+    ks.nv = (count - n_head) / 4;
+    ks.body = reinterpret_cast<const uint4*>(keys + n_head);
+    ks.head = keys;
+    ks.n_head = static_cast<int>(n_head);
+    ks.tail = keys + n_head + 4 * ks.nv;
+    ks.n_tail = static_cast<int>(count - n_head - 4 * ks.nv);
+    // BITSORT_KS_TRACE=1: per-CTA phase timestamps after every KS sort, on
+    // stderr (synchronous; a debugging aid). BITSORT_KS_PREFETCH=0: no L2
+    // prefetch of the bitset slices (A/B).
+    static const bool trace_on = std::getenv("BITSORT_KS_TRACE") != nullptr;
+    static const int prefetch = [] {
+        const char* e = std::getenv("BITSORT_KS_PREFETCH");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    unsigned long long* trace = nullptr;
+    const size_t trace_bytes = static_cast<size_t>(bws_gpu::KS_MAXG) * bws_gpu::KS_TRACE_WORDS * 8;
+    if (trace_on) {
+        static unsigned long long* buf = nullptr;
+        if (!buf) cuda_check(cudaMalloc(&buf, trace_bytes), "cudaMalloc(trace)");
+        cuda_check(cudaMemsetAsync(buf, 0, trace_bytes, stream), "trace reset");
+        trace = buf;
+    }
+    cuda_check(timed_launch("small_sort", stream,
+                            [&] {
+                                return bws_gpu::launch_small_sort(ks, key_range, key_lo, out, ctx.ctrl(), ctx.small,
+                                                                  epoch, plan, ctx.bits, stream, trace, prefetch);
+                            }),
+               "small sort launch");
+    g_launches.fetch_add(1);
+    if (trace) {
+        std::vector<unsigned long long> h(static_cast<size_t>(plan.G) * bws_gpu::KS_TRACE_WORDS);
+        cuda_check(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, stream), "trace readback");
+        cuda_check(cudaStreamSynchronize(stream), "trace readback");
+        const char* names[] = {"start", "scattered", "barrier", "counted", "offsets", "end"};
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < plan.G; ++c) t0 = std::min(t0, h[c * bws_gpu::KS_TRACE_WORDS]);
+        std::fprintf(stderr, "[KS trace] n=%zu per=%u:", count, plan.per);
+        for (int ph = 0; ph < 6; ++ph) {
+            std::vector<double> v;
+            for (int c = 0; c < plan.G; ++c) {
+                const unsigned long long t = h[c * bws_gpu::KS_TRACE_WORDS + ph];
+                if (t) v.push_back((t - t0) / 1e3);
+            }
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, " %s %.1f/%.1f/%.1f", names[ph], v.front(), v[v.size() / 2], v.back());
+        }
+        std::fprintf(stderr, " us (min/med/max over CTAs)\n");
+    }
+    record_done(ctx, stream);
+}
+
 // One sort of distinct keys on the chosen pipeline. Returns the key range it
 // sorted with (0: derived on the device by the direct pipeline, ctrl->max_key).
 uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out,
@@ -550,7 +620,19 @@ uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
             return key_range;
         }
     }
-    // FUSED / FUSED_DIRECT with a range they cannot hold fall back to AUTO's choice
+    // KS for hinted sorts below the bucketed threshold whose range a CTA slice
+    // holds in registers (C1: one launch instead of K2 + K3)
+    if (ctx.geo.small_ctas > 0 && key_range != 0 &&
+        (path == BWS_PATH_SMALL ||
+         ((path == BWS_PATH_AUTO || path == BWS_PATH_FUSED || path == BWS_PATH_FUSED_DIRECT) &&
+          count < kBucketedMinKeys && key_range <= kSmallMaxRange))) {
+        const bws_gpu::SmallPlan plan = bws_gpu::plan_small(key_range, ctx.geo.small_ctas);
+        if (plan.ok && count < (size_t(1) << 32)) {
+            enqueue_small(ctx, keys, count, out, key_range, plan, stream, key_lo);
+            return key_range;
+        }
+    }
+    // FUSED / FUSED_DIRECT / SMALL with a range they cannot hold fall back to AUTO's choice
     const bool bucketed = key_lo != 0 || (count < (size_t(1) << 32) &&
                                           (path == BWS_PATH_BUCKETED ||
                                            (path != BWS_PATH_DIRECT && count >= kBucketedMinKeys)));
@@ -567,7 +649,8 @@ Ctrl read_ctrl(DeviceCtx& ctx, cudaStream_t stream) {
                "control block readback");
     if (c.error != 0) {  // KF ring / chunk-table protocol timeout: reset the ring state
         ctx.fused_dirty = true;
-        ctx.bits_dirty = true;  // a KD sort may have stopped before taking its slices
+        ctx.small_dirty = true;
+        ctx.bits_dirty = true;  // a KD / KS sort may have stopped before taking its slices
         throw internal_error("sort protocol timeout (a kernel gave up waiting; state reset)");
     }
     return c;
@@ -1460,7 +1543,7 @@ bws_status bws_gpu_set_scatter_mode(bws_scatter_mode mode) {
 
 bws_status bws_gpu_set_path(bws_path path) {
     return wrap([&] {
-        if (path < BWS_PATH_AUTO || path > BWS_PATH_FUSED_DIRECT) throw config_error("unknown path");
+        if (path < BWS_PATH_AUTO || path > BWS_PATH_SMALL) throw config_error("unknown path");
         g_path.store(static_cast<int>(path));
     });
 }

@@ -61,6 +61,9 @@ constexpr size_t kCtrlBytes = sizeof(Ctrl) + 4 * kMaxTiles * sizeof(unsigned lon
 extern std::atomic<uint64_t> g_launches;
 extern std::atomic<int> g_scatter_mode;
 constexpr size_t kBucketedMinKeys = size_t(1) << 21;
+constexpr size_t kSmallMaxRange = size_t(1) << 25;    // AUTO: KS for hinted sorts below kBucketedMinKeys keys
+                                                       // whose range is at most this (2 bitset vectors per thread;
+                                                       // at 7 per thread, M = 2^27, KS measured no faster than K2 + K3)
 constexpr size_t kFusedMinKeys = size_t(1) << 16;        // AUTO: KD from here ...
 constexpr size_t kFusedDirectMaxKeys = 0;  // ... up to here (0: AUTO never takes KD: a tie with K2+K3 on C1)
 
@@ -87,6 +90,9 @@ struct DeviceCtx {
     void* width_scratch = nullptr;      // 8/16-bit histogram + prefix, 64-bit min/max
     void* fused = nullptr;              // KF ring state (persistent; re-initialised after a fault)
     bool fused_dirty = true;
+    void* small = nullptr;              // KS arrival counter + tagged counts (zeroed once)
+    uint32_t small_epoch = 0;           // KS launches since the state was zeroed
+    bool small_dirty = true;            // zero the KS state before the next launch (first use, fault, wrap)
     uint32_t* fused_saved = nullptr;    // KF pass-0 slices
     size_t fused_saved_words = 0;
     // the most recent bws_gpu_sort_(range_)device_async on this device, checked
@@ -123,6 +129,7 @@ struct DeviceCtx {
         cuda_check(bws_gpu::configure_scan2(dev, &geo), "scan kernel configuration");
         cuda_check(bws_gpu::configure_width_kernels(dev, &geo), "width kernel configuration");
         cuda_check(bws_gpu::configure_fused(dev, &geo), "fused kernel configuration");
+        cuda_check(bws_gpu::configure_small(dev, &geo), "small-sort kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes + sizeof(Ctrl)), "cudaMalloc(control block)");
         pending = AsyncSort{};
@@ -214,6 +221,20 @@ struct DeviceCtx {
         }
     }
 
+    // KS state, ready for the next launch; returns that launch's epoch.
+    uint32_t next_small_epoch(cudaStream_t s) {
+        if (!small) {
+            cuda_check(cudaMalloc(&small, bws_gpu::small_state_bytes()), "cudaMalloc(small-sort state)");
+            small_dirty = true;
+        }
+        if (small_dirty || small_epoch >= 0xfffffff0u) {
+            cuda_check(cudaMemsetAsync(small, 0, bws_gpu::small_state_bytes(), s), "small-sort state reset");
+            small_dirty = false;
+            small_epoch = 0;
+        }
+        return small_epoch++;
+    }
+
     void ensure_bounce() {
         if (bounce[0]) return;
         for (int i = 0; i < 2; ++i) {
@@ -239,6 +260,9 @@ struct DeviceCtx {
         if (bucket_scratch) cudaFree(bucket_scratch);
         if (wide) cudaFree(wide);
         if (width_scratch) cudaFree(width_scratch);
+        if (small) cudaFree(small);
+        small = nullptr;
+        small_dirty = true;
         if (fused) cudaFree(fused);
         if (fused_saved) cudaFree(fused_saved);
         fused = nullptr;

@@ -93,6 +93,7 @@ struct LaunchGeometry {
     int multiset_blocks = 0;                       // KB4m CTAs (one per SM)
     int fused_ctas = 0;                            // KF CTAs (one per SM; 0: no cooperative launch)
     std::size_t fused_smem_limit = 0;              // KF dynamic SMEM ceiling
+    int small_ctas = 0;                            // KS CTAs (one per SM; 0: no cooperative launch)
 };
 
 // A key array as seen by the bucketed kernels: 16-byte-aligned uint4 body plus
@@ -342,6 +343,45 @@ cudaError_t launch_fused_sort(const KeySplit& ks, std::uint64_t key_range, std::
                               unsigned long long* trace = nullptr, std::uint32_t* gbits = nullptr);
 constexpr int KF_TRACE_WORDS = 15;  // per CTA: start, prod0, cons0, prod1, cons1, counts, end, spins x2,
                                     // producer thread 0 clocks: wait, rank, barrier A, scan, scatter, store
+
+// KS (small.cu): a small sort in one cooperative launch — keys ORed into the
+// cached global bitset, a grid barrier, per-CTA slices counted from registers,
+// tagged count exchange, extraction straight from registers.
+constexpr int KS_MAXG = 1024;    // CTAs (one per SM) the state is sized for
+constexpr int KS_MAX_PER = 8;    // 16-byte bitset vectors per thread
+struct SmallPlan {
+    bool ok = false;
+    int G = 0;                   // CTAs
+    std::uint32_t per = 0;       // vectors per thread
+    std::uint32_t total_v = 0;   // vectors covering the key range
+};
+struct SmallArgs {
+    KeySplit ks;
+    std::uint32_t lo;            // keys x with (x ^ xr) - lo > range_m1 are bad
+    std::uint32_t range_m1;
+    std::uint32_t* gbits;        // all-zero global bitset (>= total_v vectors); all-zero again afterwards
+    std::uint32_t per, total_v;
+    std::uint32_t* out;
+    Ctrl* ctrl;                  // zeroed by CTA 0 before the barrier (no memset needed)
+    std::uint32_t* sync;         // monotonic arrival counter
+    std::uint32_t* ghist;        // 2 x KS_MAXG: keys per owning slice, by launch parity (the other
+                                 // parity's entries are zeroed for the next launch)
+    std::uint32_t per_magic;     // ceil(2^32 / per): slice of key offset x = umulhi(x >> 17, per_magic)
+    std::uint32_t arrive_target; // sync value when all CTAs of this launch have arrived
+    std::uint32_t tag;           // this launch's tag (never 0)
+    unsigned long long* trace;   // optional: KS_TRACE_WORDS globaltimer stamps per CTA
+    int prefetch;                // prefetch the CTA's bitset slice into L2 before the REDs
+};
+constexpr int KS_TRACE_WORDS = 8;  // start, scattered, barrier passed, counted (offset known), -, end
+SmallPlan plan_small(std::uint64_t key_range, int ctas);
+std::size_t small_state_bytes();  // zeroed once; see launch_small_sort's epoch
+cudaError_t configure_small(int device, LaunchGeometry* geo);
+// epoch: launches since the state was zeroed (the caller counts them; the
+// state must be zeroed again before epoch + 1 wraps to 0, and after a fault).
+cudaError_t launch_small_sort(const KeySplit& ks, std::uint64_t key_range, std::uint32_t key_lo,
+                              std::uint32_t* out, Ctrl* ctrl, void* state, std::uint32_t epoch,
+                              const SmallPlan& plan, std::uint32_t* gbits, cudaStream_t stream,
+                              unsigned long long* trace = nullptr, int prefetch = 1);
 
 // K0: ctrl->max_key = max(keys) (only for sorts without a key-range hint).
 cudaError_t launch_key_max(const std::uint32_t* keys, std::size_t n, Ctrl* ctrl,

@@ -1,5 +1,5 @@
-"""GPU parity of the fused single-launch sort (KF, csrc/fused.cu) through the
-C ABI: ring laps across many launches, both pass counts, ragged and
+"""GPU parity of the single-launch sorts (KF / KD, csrc/fused.cu; KS,
+csrc/small.cu) through the C ABI: ring laps across many launches, both pass counts, ragged and
 misaligned arrays, skewed owners, out-of-range keys and repeats, against the
 oracle / np.sort (distinct keys have one ascending order, bitsort.hpp:84-136).
 """
@@ -21,10 +21,10 @@ def capi(cuda):
     return c
 
 
-@pytest.fixture(autouse=True, params=["FUSED", "FUSED_DIRECT"])
+@pytest.fixture(autouse=True, params=["FUSED", "FUSED_DIRECT", "SMALL"])
 def _fused(capi, request):
-    """KF (ring mode) and KD (direct mode); ranges a mode cannot hold take
-    AUTO's pipeline."""
+    """KF (ring mode), KD (direct mode) and KS (small sorts, bitset words in
+    registers); ranges a mode cannot hold take AUTO's pipeline."""
     capi.set_path(getattr(capi.Path, request.param))
     yield
     capi.set_path(capi.Path.AUTO)
@@ -168,3 +168,20 @@ def test_configs_vs_reference_anchors(capi, cuda, anchors, name):
         total, got = _device_sort(capi, cuda, keys, cfg.key_range)
         assert total == cfg.n
         assert fnv1a64(got) == anchors[name]["fnv1a64_sorted"], rep
+
+
+@pytest.mark.parametrize("count", [10_240, 10_241, 50_000, 131_072])
+def test_one_slice_small_range(capi, cuda, count):
+    """Every key inside one 2^17-key slice of a 2^24 range (KS: one CTA holds
+    all the keys; at most 10240 leave through the SMEM stage, more by direct
+    stores), the slice full at 131072 keys; then a spread-out sort to show the
+    cached bitset was left all-zero."""
+    rng = np.random.default_rng(count)
+    keys = (rng.permutation(1 << 17)[:count].astype(np.uint32) + (5 << 17)).astype(np.uint32)
+    for off in (0, 1):
+        total, got = _device_sort(capi, cuda, keys, 1 << 24, off)
+        assert total == count
+        assert np.array_equal(got, np.sort(keys))
+    k2 = _distinct(rng, 200_000, 1 << 24)
+    total, got = _device_sort(capi, cuda, k2, 1 << 24)
+    assert total == k2.size and np.array_equal(got, np.sort(k2))

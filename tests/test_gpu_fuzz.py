@@ -43,7 +43,7 @@ def test_random_sweep(cuda):
             key_range = int(min(1 << 32, (1 << int(rng.integers(lo_bits, 33))) - int(rng.integers(0, 3))))
             key_range = max(key_range, n)
             layout = str(rng.choice(["uniform", "sorted", "reverse", "blocks"]))
-            path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED", "FUSED", "FUSED_DIRECT"]))
+            path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED", "FUSED", "FUSED_DIRECT", "SMALL"]))
             offset = int(rng.integers(0, 4))
             signed = bool(rng.random() < 0.2) and key_range == 1 << 32
             keys = _keys(rng, n, key_range, layout)
@@ -92,7 +92,7 @@ def test_random_sweep_full_contract(cuda):
             udt = np.dtype(f"uint{info.bits}")
             keys = (base + (r & mask)).astype(udt).view(dt)
             lo, hi = int(base), span_bits
-            path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED", "FUSED", "FUSED_DIRECT"]))
+            path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED", "FUSED", "FUSED_DIRECT", "SMALL"]))
             capi.set_path(getattr(capi.Path, path))
             ctx = f"{dt} n={n} base={lo} span=2^{hi} path={path}"
             if rng.random() < 0.5:

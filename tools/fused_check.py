@@ -82,7 +82,7 @@ for name, keys, M in cases:
     allok &= ok
 for n, M in [(1 << 16, 1 << 24), (1 << 20, 1 << 24), (1 << 22, 1 << 26), (1 << 22, 1 << 27)]:
     keys = rng.choice(M, size=n, replace=False).astype(np.uint32)
-    for path in (capi.Path.FUSED_DIRECT, capi.Path.DIRECT, capi.Path.BUCKETED):
+    for path in (capi.Path.SMALL, capi.Path.FUSED_DIRECT, capi.Path.DIRECT, capi.Path.BUCKETED):
         ok, t = run(keys, M, reps=2, time_it=True, path=path)
         print(f"n=2^{n.bit_length()-1} M=2^{M.bit_length()-1} {path.name}: {'ok' if ok else 'FAIL'} {t*1000:.1f} us", flush=True)
         allok &= ok
@@ -90,6 +90,9 @@ for cname in ["C1", "C2"]:
     cfg = configs.CONFIGS[cname]
     keys = cfg.generate()
     if cname == "C1":
+        oks, ts = run(keys, cfg.key_range, reps=20, time_it=True, path=capi.Path.SMALL)
+        print(f"C1 small (KS): {'ok' if oks else 'FAIL'}  {ts*1000:.1f} us  {cfg.n / ts / 1e6:.1f} Gkeys/s", flush=True)
+        allok &= oks
         okd, td = run(keys, cfg.key_range, reps=5, time_it=True, path=capi.Path.FUSED_DIRECT)
         print(f"C1 fused_direct: {'ok' if okd else 'FAIL'}  {td*1000:.1f} us  {cfg.n / td / 1e6:.1f} Gkeys/s", flush=True)
         allok &= okd

@@ -38,7 +38,7 @@ def one_case(rng):
             off = np.unique(off)
             rng.shuffle(off)
     keys = (base + off).astype(udt).view(dt)
-    path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED", "FUSED", "FUSED_DIRECT"]))
+    path = str(rng.choice(["AUTO", "DIRECT", "BUCKETED", "FUSED", "FUSED_DIRECT", "SMALL"]))
     on_device = rng.random() < 0.5
     offset = int(rng.integers(0, 3))
     return dt, keys, path, on_device, offset
