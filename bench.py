@@ -123,6 +123,8 @@ def kernel_alg_bytes(kernel: str, n: int, key_range: int, world: int = 1) -> int
     words_bytes = (key_range + 31) // 32 * 4
     return {
         "fused_sort": 4 * n * (fused_passes(key_range) + 1),  # read keys once per pass, write sorted keys
+        "fused_direct": 8 * n,                # KD: read keys, write sorted keys (the bitset stays in L2)
+        "small_sort": 8 * n,                  # KS: read keys, write sorted keys (the bitset stays in L2)
         "bucket_hist": 4 * n,                 # read keys
         "bucket_colscan": 0,
         "bucket_partition": 8 * n,            # read keys, write bucketed keys
