@@ -305,6 +305,9 @@ __device__ void compute_kb4_order(const uint32_t* __restrict__ tot, int nb, uint
 // (0: not allocated yet), allocated from pool chunk nb upwards. Tiles claim
 // runs in a bucket with one atomicAdd on its fill counter, as in the slab
 // layout; the claim that holds a chunk's first slot allocates it, others wait.
+__device__ __forceinline__ uint32_t chunk_base(uint32_t id, uint32_t cs, uint32_t pad) {
+    return (id << cs) + id * pad;  // (pool slots stay below 2^32: chunk_slots)
+}
 __device__ __forceinline__ uint32_t chunk_alloc(const SlabArgs& sa, int nb, uint32_t b, uint32_t j) {
     if (j == 0) return b;
     const uint32_t id = static_cast<uint32_t>(nb) + atomicAdd(sa.pool_next, 1u);
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                         const uint32_t j = pos >> cs;
                         if (j < sa.max_chunks) {
                             const uint32_t id = (pos & cm) == 0 ? chunk_alloc(sa, nb, b, j) : chunk_get(sa, b, j);
-                            parted[(static_cast<size_t>(id) << cs) + (pos & cm)] = e;
+                            parted[static_cast<size_t>(chunk_base(id, cs, sa.chunk_pad)) + (pos & cm)] = e;
                         } else {
                             sa.ctrl->overflow = 1u;
                         }
@@ -678,7 +681,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 }
                 const uint32_t id = id0[q] ? id0[q] - 1u : chunk_get(sa, b, j0);
                 const uint32_t st = s_start[b];
-                s_delta[b] = (id << cs) + (cl & cm) - st;
+                s_delta[b] = chunk_base(id, cs, sa.chunk_pad) + (cl & cm) - st;
                 // tile position where the run leaves its first chunk (0x7fff: never;
                 // a crossing lies inside the tile, so it fits 15 bits), with the
                 // next chunk's index above it for the slow path
@@ -722,7 +725,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 if (i >= (x & 0x7fffu)) {  // past the run's first chunk (rare)
                     const uint32_t k2 = i - (x & 0x7fffu);
                     const uint32_t id = chunk_get(sa, b, (x >> 15) + (k2 >> sa.chunk_shift));
-                    dst = (static_cast<size_t>(id) << sa.chunk_shift) + (k2 & ((1u << sa.chunk_shift) - 1u));
+                    dst = static_cast<size_t>(chunk_base(id, sa.chunk_shift, sa.chunk_pad)) + (k2 & ((1u << sa.chunk_shift) - 1u));
                 }
                 st_hint(parted + dst, key, pol);
             }
@@ -1076,7 +1079,8 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                        const unsigned long long* __restrict__ g_base, BucketMap bm, int nb,
                        uint32_t src_cap, uint32_t* __restrict__ out, Ctrl* __restrict__ ctrl,
                        const uint32_t* __restrict__ order, int all_or_nothing,
-                       const uint32_t* __restrict__ chunk_tab, uint32_t max_chunks, uint32_t chunk_shift) {
+                       const uint32_t* __restrict__ chunk_tab, uint32_t max_chunks, uint32_t chunk_shift,
+                       uint32_t chunk_pad) {
     // in-place sorts: a slab that lost runs (repeated keys overflowed a
     // bucket) writes nothing, so the input stays intact for the counting pass
     if (all_or_nothing && *reinterpret_cast<volatile const uint32_t*>(&ctrl->overflow)) return;
@@ -1150,7 +1154,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         const uint32_t CH = 1u << chunk_shift;
         auto chunk_src = [&](uint32_t j) {
             const uint32_t id = j == 0 ? b : chunk_tab[static_cast<size_t>(b) * max_chunks + j] - 1u;
-            return parted + (static_cast<size_t>(id) << chunk_shift);
+            return parted + static_cast<size_t>(chunk_base(id, chunk_shift, chunk_pad));
         };
         if (chunk_tab && (sparse || cnt <= 2 * CH)) {
             for (uint32_t j = 0; j * CH < cnt; ++j) {
@@ -1793,6 +1797,20 @@ uint64_t slab_slots(const BucketPlan& plan, size_t n) {
 
 // Chunked layout (the packed layout's replacement for distinct-key sorts:
 // no KB1 histogram read, no KB2): pool slots for n keys in nb buckets.
+// Pool chunk id starts at slot id * (2^shift + pad), pad = BITSORT_CHUNK_PAD
+// slots (default 0). An experiment knob: C4's KB3 measures 105 us when the
+// pool is allocated before the 512 MiB cached bitset and 151 us when after it
+// (a C1 sort first); taking the chunk starts off their power-of-two stride
+// (pad 32 .. 1056) changed neither figure, so the stride is not the cause
+// (profiles/r02_order_probe.log).
+uint32_t chunk_pad_slots() {
+    static const uint32_t pad = [] {
+        const char* e = std::getenv("BITSORT_CHUNK_PAD");
+        const long v = e ? std::atol(e) : 0;
+        return static_cast<uint32_t>(v < 0 ? 0 : (v > 4096 ? 4096 : v)) & ~3u;
+    }();
+    return pad;
+}
 constexpr uint32_t kMaxChunksPerBucket = (1u << MAX_BUCKET_SHIFT) / KC_CHUNK_MIN + 2;
 // Chunk size: about a quarter of a bucket's mean key count (few allocations,
 // at most a quarter-bucket of pool slots wasted per bucket), 2^13 .. 2^16.
@@ -1815,7 +1833,7 @@ uint64_t chunk_slots(const BucketPlan& plan, size_t n) {
     if (off || plan.partition_only || plan.nb > MAX_BUCKETS) return 0;
     const uint64_t ch = uint64_t(1) << chunk_shift(plan, n);
     const uint64_t chunks = static_cast<uint64_t>(n) / ch + plan.nb + 2;  // implicit chunk 0 per bucket
-    const uint64_t slots = chunks * ch;
+    const uint64_t slots = chunks * (ch + chunk_pad_slots());
     return slots < (1ull << 32) - ch ? slots : 0;
 }
 
@@ -1905,6 +1923,7 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.gcnt = gcnt;
         sa.gtrue = nullptr;
         sa.chunk_shift = chunk_shift(plan, n);
+        sa.chunk_pad = chunk_pad_slots();
         sa.cap = maxc << sa.chunk_shift;  // more slots means repeated keys: the bucket sorts nothing
         sa.dump = 0xffffffffu;
         sa.limit = limit;
@@ -2031,11 +2050,11 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     if (plan.shift >= MAX_BUCKET_SHIFT)
         bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
             parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
-            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift);
+            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift, sa.chunk_pad);
     else  // narrower buckets: two 512-thread CTAs per SM
         bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
             parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
-            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift);
+            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift, sa.chunk_pad);
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;

@@ -152,6 +152,8 @@ struct SlabArgs {
     std::uint32_t max_chunks = 0;
     std::uint32_t* pool_next = nullptr;    // chunked layout: next free pool chunk - nb (zeroed)
     std::uint32_t chunk_shift = 13;        // chunked layout: log2 slots per pool chunk
+    std::uint32_t chunk_pad = 0;           // chunked layout: pool chunk id starts at slot id * (2^shift + pad)
+                                           // (a multiple of 4): chunk starts off the power-of-two stride
 };
 constexpr std::uint32_t KC_CHUNK_MIN = 8192;      // smallest pool chunk (chunked layout)
 constexpr std::uint32_t KC_DROP = 0xffffffffu;    // a dropped (overflowed) run
