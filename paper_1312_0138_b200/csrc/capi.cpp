@@ -529,7 +529,7 @@ void enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
         cuda_check(cudaMemsetAsync(ctx.bits, 0, kMaxWords * sizeof(uint32_t), stream), "bitset reset");
         ctx.bits_dirty = false;
     }
-    const uint32_t epoch = ctx.next_small_epoch(stream);
+    ctx.ensure_small(stream);
     bws_gpu::KeySplit ks;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(keys);
     size_t n_head = ((16 - (addr & 15)) & 15) / 4;
@@ -559,7 +559,7 @@ void enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
     cuda_check(timed_launch("small_sort", stream,
                             [&] {
                                 return bws_gpu::launch_small_sort(ks, key_range, key_lo, out, ctx.ctrl(), ctx.small,
-                                                                  epoch, plan, ctx.bits, stream, trace, prefetch);
+                                                                  plan, ctx.bits, stream, trace, prefetch);
                             }),
                "small sort launch");
     g_launches.fetch_add(1);

@@ -91,8 +91,7 @@ struct DeviceCtx {
     void* fused = nullptr;              // KF ring state (persistent; re-initialised after a fault)
     bool fused_dirty = true;
     void* small = nullptr;              // KS arrival counter + tagged counts (zeroed once)
-    uint32_t small_epoch = 0;           // KS launches since the state was zeroed
-    bool small_dirty = true;            // zero the KS state before the next launch (first use, fault, wrap)
+    bool small_dirty = true;            // zero the KS state before the next launch (first use, fault)
     uint32_t* fused_saved = nullptr;    // KF pass-0 slices
     size_t fused_saved_words = 0;
     // the most recent bws_gpu_sort_(range_)device_async on this device, checked
@@ -221,18 +220,16 @@ struct DeviceCtx {
         }
     }
 
-    // KS state, ready for the next launch; returns that launch's epoch.
-    uint32_t next_small_epoch(cudaStream_t s) {
+    // KS state (arrival counter + slice histograms), zeroed on first use and after a fault.
+    void ensure_small(cudaStream_t s) {
         if (!small) {
             cuda_check(cudaMalloc(&small, bws_gpu::small_state_bytes()), "cudaMalloc(small-sort state)");
             small_dirty = true;
         }
-        if (small_dirty || small_epoch >= 0xfffffff0u) {
+        if (small_dirty) {
             cuda_check(cudaMemsetAsync(small, 0, bws_gpu::small_state_bytes(), s), "small-sort state reset");
             small_dirty = false;
-            small_epoch = 0;
         }
-        return small_epoch++;
     }
 
     void ensure_bounce() {

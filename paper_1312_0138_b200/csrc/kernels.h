@@ -365,23 +365,20 @@ struct SmallArgs {
     std::uint32_t per, total_v;
     std::uint32_t* out;
     Ctrl* ctrl;                  // zeroed by CTA 0 before the barrier (no memset needed)
-    std::uint32_t* sync;         // monotonic arrival counter
+    unsigned long long* sync;    // monotonic arrival counter (G per launch)
     std::uint32_t* ghist;        // 2 x KS_MAXG: keys per owning slice, by launch parity (the other
                                  // parity's entries are zeroed for the next launch)
     std::uint32_t per_magic;     // ceil(2^32 / per): slice of key offset x = umulhi(x >> 17, per_magic)
-    std::uint32_t arrive_target; // sync value when all CTAs of this launch have arrived
-    std::uint32_t tag;           // this launch's tag (never 0)
     unsigned long long* trace;   // optional: KS_TRACE_WORDS globaltimer stamps per CTA
     int prefetch;                // prefetch the CTA's bitset slice into L2 before the REDs
 };
 constexpr int KS_TRACE_WORDS = 8;  // start, scattered, barrier passed, counted (offset known), -, end
 SmallPlan plan_small(std::uint64_t key_range, int ctas);
-std::size_t small_state_bytes();  // zeroed once; see launch_small_sort's epoch
+std::size_t small_state_bytes();
 cudaError_t configure_small(int device, LaunchGeometry* geo);
-// epoch: launches since the state was zeroed (the caller counts them; the
-// state must be zeroed again before epoch + 1 wraps to 0, and after a fault).
+// state: small_state_bytes() bytes, zeroed once (and again after a fault).
 cudaError_t launch_small_sort(const KeySplit& ks, std::uint64_t key_range, std::uint32_t key_lo,
-                              std::uint32_t* out, Ctrl* ctrl, void* state, std::uint32_t epoch,
+                              std::uint32_t* out, Ctrl* ctrl, void* state,
                               const SmallPlan& plan, std::uint32_t* gbits, cudaStream_t stream,
                               unsigned long long* trace = nullptr, int prefetch = 1);
 

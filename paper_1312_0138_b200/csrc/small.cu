@@ -13,7 +13,9 @@
 //      shared-memory histogram, which the CTA then adds to a global one (G
 //      REDs); keys >= the range are counted as bad;
 //   B  grid barrier (all CTAs are co-resident: cooperative launch, one CTA
-//      per SM; a monotonic arrival counter, no reset);
+//      per SM; a monotonic 64-bit arrival counter, no reset: the launch
+//      generation is the counter / G read at kernel start, so nothing
+//      launch-specific comes from the host and captured graphs replay);
 //   C  CTA c takes slice c of the bitset — thread t the `per` consecutive
 //      16-byte vectors [t per, (t + 1) per) of it, kept in registers when
 //      per == 1 — and popcounts it; its output offset is the histogram's
@@ -28,7 +30,7 @@
 //
 // HBM traffic: 4n (keys) + 4n (output); the bitset stays in L2. CTA 0 zeroes
 // the control block before the barrier (no memset precedes the launch); the
-// histogram has two parities and each launch zeroes the next one's. A wait
+// histogram has two parities (generation & 1) and each launch zeroes the next one's. A wait
 // that exceeds 2 s is a protocol fault: ctrl->error, and the host resets the
 // state (capi.cpp read_ctrl).
 #include <cuda_runtime.h>
@@ -47,9 +49,9 @@ constexpr int KS_THREADS = 1024;
 constexpr uint32_t KS_STAGE = 10240;  // keys a CTA stages in SMEM for coalesced output stores
 constexpr unsigned long long kKsTimeoutNs = 2000000000ull;
 
-__device__ __forceinline__ uint32_t ks_ld_acquire(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ks_ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ unsigned long long ks_ld_relaxed64(const unsigned long long* p) {
@@ -75,24 +77,30 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
     __shared__ uint32_t s_bad;
     __shared__ uint32_t s_fail;
     __shared__ unsigned long long s_base;
+    __shared__ unsigned long long s_gen;
     const uint32_t G = gridDim.x, c = blockIdx.x;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long* tr = a.trace ? a.trace + static_cast<size_t>(c) * KS_TRACE_WORDS : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = ks_now();
-    uint32_t* ghist = a.ghist + (a.tag & 1u) * KS_MAXG;          // this launch's slice histogram
-    uint32_t* ghist_next = a.ghist + ((a.tag & 1u) ^ 1u) * KS_MAXG;  // the next launch's: zeroed here
     for (uint32_t i = threadIdx.x; i < G; i += KS_THREADS) s_hist[i] = 0;
     if (threadIdx.x == 0) {
         s_bad = 0;
         s_fail = 0;
         s_base = 0;
-        ghist_next[c] = 0;
+        // The launch generation, from the arrival counter itself: every earlier
+        // launch added exactly G, and a CTA reads it before it arrives, so all
+        // CTAs of this launch see a value in [gen G, (gen + 1) G). Nothing
+        // launch-specific comes from the host: a captured graph replays correctly.
+        s_gen = ks_ld_relaxed64(a.sync) / G;
         if (c == 0) {  // the whole control block: no memset before the launch
             Ctrl r = {};
             *a.ctrl = r;
         }
     }
     __syncthreads();
+    const unsigned long long gen = s_gen;
+    uint32_t* ghist = a.ghist + (gen & 1u) * KS_MAXG;          // this launch's slice histogram
+    if (threadIdx.x == 0) a.ghist[((gen & 1u) ^ 1u) * KS_MAXG + c] = 0;  // the next launch's: zeroed here
 
     // ------------------------------------------------------------ A: scatter
     // the CTA's slice of the bitset into L2 first (cold after an L2 flush: a
@@ -147,17 +155,17 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
         const uint32_t h = s_hist[i];
         if (h) atomicAdd(ghist + i, h);
     }
-    if (threadIdx.x == 0 && s_bad) atomicAdd(&a.ctrl->bad_keys, s_bad);
     __threadfence();  // this thread's REDs are performed before the CTA arrives
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[1] = ks_now();
 
     // ------------------------------------------------------- B: grid barrier
     if (threadIdx.x == 0) {
-        atomicAdd(a.sync, 1u);
+        atomicAdd(a.sync, 1ull);
+        const unsigned long long target = (gen + 1ull) * G;
         const unsigned long long t0 = ks_now();
         uint32_t spins = 0;
-        while (static_cast<int32_t>(ks_ld_acquire(a.sync) - a.arrive_target) < 0) {
+        while (ks_ld_acquire64(a.sync) < target) {
             if ((++spins & 1023u) == 0 && ks_now() - t0 > kKsTimeoutNs) {
                 s_fail = 1;
                 break;
@@ -209,7 +217,10 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
         before_thread = __shfl_sync(kFull, wi - wv, warp) + (incl - cnt);
         cta_total = __shfl_sync(kFull, wi, 31);
     }
-    if (threadIdx.x == 0 && cta_total) atomicAdd(&a.ctrl->total, static_cast<unsigned long long>(cta_total));
+    if (threadIdx.x == 0) {  // (after the barrier: CTA 0 zeroed the control block before it arrived)
+        if (cta_total) atomicAdd(&a.ctrl->total, static_cast<unsigned long long>(cta_total));
+        if (s_bad) atomicAdd(&a.ctrl->bad_keys, s_bad);
+    }
     const unsigned long long base = s_base;
     if (tr && threadIdx.x == 0) tr[3] = ks_now();
 
@@ -291,7 +302,7 @@ cudaError_t configure_small(int device, LaunchGeometry* geo) {
 }
 
 cudaError_t launch_small_sort(const KeySplit& ks, std::uint64_t key_range, std::uint32_t key_lo,
-                              std::uint32_t* out, Ctrl* ctrl, void* state, std::uint32_t epoch,
+                              std::uint32_t* out, Ctrl* ctrl, void* state,
                               const SmallPlan& plan, std::uint32_t* gbits, cudaStream_t stream,
                               unsigned long long* trace, int prefetch) {
     if (!plan.ok) return cudaErrorInvalidValue;
@@ -304,11 +315,9 @@ cudaError_t launch_small_sort(const KeySplit& ks, std::uint64_t key_range, std::
     a.total_v = plan.total_v;
     a.out = out;
     a.ctrl = ctrl;
-    a.sync = static_cast<std::uint32_t*>(state);
+    a.sync = static_cast<unsigned long long*>(state);
     a.ghist = reinterpret_cast<std::uint32_t*>(static_cast<unsigned char*>(state) + 64);
     a.per_magic = static_cast<std::uint32_t>(((std::uint64_t(1) << 32) + plan.per - 1) / plan.per);
-    a.arrive_target = (epoch + 1u) * static_cast<std::uint32_t>(plan.G);
-    a.tag = epoch + 1u;
     a.trace = trace;
     a.prefetch = prefetch;
     cudaLaunchConfig_t cfg = {};

@@ -185,3 +185,34 @@ def test_one_slice_small_range(capi, cuda, count):
     k2 = _distinct(rng, 200_000, 1 << 24)
     total, got = _device_sort(capi, cuda, k2, 1 << 24)
     assert total == k2.size and np.array_equal(got, np.sort(k2))
+
+
+def test_small_sort_graph_replay(capi, cuda):
+    """A hinted small sort captured in a CUDA graph and replayed with new keys
+    in the same buffers, interleaved with direct calls: the KS grid barrier
+    takes its generation from the device-side arrival counter, so nothing
+    launch-specific is baked into the captured kernel node."""
+    n, key_range = 300_000, 1 << 24
+    rng = np.random.default_rng(41)
+    t = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    out = cuda.empty_like(t)
+    s = cuda.cuda.Stream()
+    k0 = _distinct(rng, n, key_range)
+    t.copy_(cuda.from_numpy(k0.view(np.int32)))
+    with cuda.cuda.stream(s):
+        capi.sort_device_async(t.data_ptr(), n, out.data_ptr(), key_range, s.cuda_stream)  # warm-up
+    s.synchronize()
+    g = cuda.cuda.CUDAGraph()
+    with cuda.cuda.graph(g, stream=s):
+        capi.sort_device_async(t.data_ptr(), n, out.data_ptr(), key_range, s.cuda_stream)
+    for rep in range(7):
+        keys = _distinct(rng, n, key_range)
+        t.copy_(cuda.from_numpy(keys.view(np.int32)))
+        out.zero_()
+        cuda.cuda.synchronize()
+        g.replay()
+        s.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), np.sort(keys)), rep
+        if rep % 3 == 1:  # a direct call between replays
+            total, got = _device_sort(capi, cuda, k0, key_range)
+            assert total == n and np.array_equal(got, np.sort(k0))
