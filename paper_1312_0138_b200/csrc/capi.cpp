@@ -97,6 +97,10 @@ class CopyPool {
     CopyPool() {
         const unsigned hw = std::thread::hardware_concurrency();
         n_ = static_cast<int>(hw >= 16 ? 8 : (hw >= 4 ? hw / 2 : 1));
+        if (const char* e = std::getenv("BITSORT_COPY_THREADS")) {  // staging copies of pageable arrays
+            const int v = std::atoi(e);
+            if (v >= 1 && v <= 64) n_ = v;
+        }
         for (int i = 1; i < n_; ++i) workers_.emplace_back([this, i] { loop(i); });
     }
     ~CopyPool() {

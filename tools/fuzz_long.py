@@ -59,7 +59,24 @@ def main():
         info = np.iinfo(dt)
         capi.set_path(getattr(capi.Path, path))
         ctx = f"seed={seed} dtype={dt} n={keys.size} path={path} device={on_device} offset={offset}"
-        if on_device:
+        hinted = dt == np.uint32 and keys.size > 0 and np.unique(keys).size == keys.size and \
+            np.random.default_rng(seed ^ 1).random() < 0.5
+        if hinted:
+            # the range-hint extension (bws_gpu_sort_device_async): KS / KD / KF / K2+K3 / KB3+KB4
+            # by path and size, output to a second buffer with guard words
+            key_range = min(1 << 32, int(keys.max()) + 1 + int(np.random.default_rng(seed ^ 2).integers(0, 1000)))
+            src = torch.zeros(keys.size + offset, dtype=torch.int32, device="cuda")
+            src[offset:].copy_(torch.from_numpy(keys.view(np.int32).copy()))
+            out = torch.full((keys.size + 4,), -1, dtype=torch.int32, device="cuda")
+            s = torch.cuda.current_stream().cuda_stream
+            capi.sort_device_async(src[offset:].data_ptr(), keys.size, out.data_ptr(), key_range, s)
+            total = capi.sort_check(s)
+            res = out.cpu().numpy().view(np.uint32)
+            got = res[: keys.size]
+            untouched = res[keys.size:].tolist() == [0xFFFFFFFF] * 4 and total == keys.size
+            st = capi.Status.OK
+            ctx += f" hinted range={key_range}"
+        elif on_device:
             buf = torch.zeros(keys.nbytes + (offset + 2) * keys.itemsize, dtype=torch.uint8, device="cuda")
             view = buf[offset * keys.itemsize: offset * keys.itemsize + keys.nbytes]
             view.copy_(torch.from_numpy(keys.view(np.uint8).copy()))

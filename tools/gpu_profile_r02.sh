@@ -11,6 +11,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:buck
     python tools/run_one.py --config C2 --iters 1 > gpurun_out/r02_ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused -c 1 -f -o gpurun_out/r02_prof_kf_c2 \
     python tools/run_one.py --config C2 --path FUSED --iters 1 > gpurun_out/r02_ncu_kf.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:small_sort -c 1 -f -o gpurun_out/r02_prof_ks_c1 \
+    python tools/run_one.py --config C1 --path SMALL --iters 1 > gpurun_out/r02_ncu_ks.log 2>&1
+timeout 600 python bench.py --config C1 > gpurun_out/r02_bench_c1_ks.json 2> gpurun_out/r02_bench_c1_ks.err
+timeout 600 python bench.py --config C4 --no-cpu-baseline > gpurun_out/r02_bench_c4_chunked.json 2> gpurun_out/r02_bench_c4.err
+timeout 600 python bench.py --config C5 --no-cpu-baseline > gpurun_out/r02_bench_c5_chunked.json 2> gpurun_out/r02_bench_c5.err
+timeout 300 python tools/width_bench.py > gpurun_out/r02_width_bench.jsonl 2>&1
 for c in C1 C2 C3 C4 C5; do
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -c 10 --csv \
       --log-file gpurun_out/r02_traffic_$c.csv python tools/run_one.py --config $c --path AUTO --iters 1 > gpurun_out/r02_traffic_$c.log 2>&1
