@@ -523,7 +523,10 @@ void enqueue_fused(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
 
 // KS: one cooperative launch for a small hinted sort (small.cu). The last CTA
 // writes the control block, so nothing is reset before the launch.
-void enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out, uint64_t key_range,
+// Returns false (nothing queued, KS disabled on this device from now on) when
+// the driver refuses the cooperative launch — e.g. a context with fewer SMs
+// than the device reports (MPS partitions): the caller takes the direct path.
+bool enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t* out, uint64_t key_range,
                    const bws_gpu::SmallPlan& plan, cudaStream_t stream, uint32_t key_lo = 0) {
     NvtxRange nvtx_range("bitsort:small KS");
     wait_done(ctx, stream);
@@ -560,12 +563,17 @@ void enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
         cuda_check(cudaMemsetAsync(buf, 0, trace_bytes, stream), "trace reset");
         trace = buf;
     }
-    cuda_check(timed_launch("small_sort", stream,
-                            [&] {
-                                return bws_gpu::launch_small_sort(ks, key_range, key_lo, out, ctx.ctrl(), ctx.small,
-                                                                  plan, ctx.bits, stream, trace, prefetch);
-                            }),
-               "small sort launch");
+    const cudaError_t lerr = timed_launch("small_sort", stream, [&] {
+        return bws_gpu::launch_small_sort(ks, key_range, key_lo, out, ctx.ctrl(), ctx.small, plan, ctx.bits, stream,
+                                          trace, prefetch);
+    });
+    if (lerr == cudaErrorCooperativeLaunchTooLarge || lerr == cudaErrorNotSupported ||
+        lerr == cudaErrorLaunchOutOfResources) {
+        cudaGetLastError();
+        ctx.geo.small_ctas = 0;
+        return false;
+    }
+    cuda_check(lerr, "small sort launch");
     g_launches.fetch_add(1);
     if (trace) {
         std::vector<unsigned long long> h(static_cast<size_t>(plan.G) * bws_gpu::KS_TRACE_WORDS);
@@ -588,6 +596,7 @@ void enqueue_small(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32_t*
         std::fprintf(stderr, " us (min/med/max over CTAs)\n");
     }
     record_done(ctx, stream);
+    return true;
 }
 
 // One sort of distinct keys on the chosen pipeline. Returns the key range it
@@ -631,10 +640,9 @@ uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
          ((path == BWS_PATH_AUTO || path == BWS_PATH_FUSED || path == BWS_PATH_FUSED_DIRECT) &&
           count < kBucketedMinKeys && key_range <= kSmallMaxRange))) {
         const bws_gpu::SmallPlan plan = bws_gpu::plan_small(key_range, ctx.geo.small_ctas);
-        if (plan.ok && count < (size_t(1) << 32)) {
-            enqueue_small(ctx, keys, count, out, key_range, plan, stream, key_lo);
+        if (plan.ok && count < (size_t(1) << 32) &&
+            enqueue_small(ctx, keys, count, out, key_range, plan, stream, key_lo))
             return key_range;
-        }
     }
     // FUSED / FUSED_DIRECT / SMALL with a range they cannot hold fall back to AUTO's choice
     const bool bucketed = key_lo != 0 || (count < (size_t(1) << 32) &&
