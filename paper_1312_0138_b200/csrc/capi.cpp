@@ -29,6 +29,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -841,7 +842,25 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     };
     // signed keys (xr) always take the bucketed pipeline, which applies the XOR
     uint64_t sorted_range = key_range;  // the range the bitset pass used (0: derived on the device)
+    // Small unhinted sorts (count < 2^21, AUTO): K2 + K3 derive the range on the
+    // device; once a sort has told the host its keys' range (K2 and KS fold the
+    // largest key), the next one runs KS planned for that range — one launch
+    // instead of two. Keys beyond it are counted as bad: the pass is redone
+    // with K2 + K3 (the device copy is intact or re-uploaded).
+    bool small_spec = false;  // the bitset pass ran KS on the speculated range
+    const bool small_unhinted = hinted_range == 0 && xr == 0 && span_limit == 0 && count < kBucketedMinKeys &&
+                                current_path() == BWS_PATH_AUTO;
     auto enqueue = [&](const uint32_t* in, uint32_t* out) {
+        small_spec = false;
+        if (small_unhinted && key_range == 0 && ctx.geo.small_ctas > 0 && speculate_range() &&
+            ctx.spec_small != 0 && ctx.spec_small <= kSmallMaxRange) {
+            const bws_gpu::SmallPlan plan = bws_gpu::plan_small(ctx.spec_small, ctx.geo.small_ctas);
+            if (plan.ok && enqueue_small(ctx, in, count, out, ctx.spec_small, plan, ctx.stream)) {
+                sorted_range = ctx.spec_small;
+                small_spec = true;
+                return;
+            }
+        }
         if (xr) {
             if (count >= (size_t(1) << 32)) throw std::out_of_range("signed sorts take fewer than 2^32 keys");
             sorted_range = enqueue_bucketed(ctx, in, count, out, key_range, ctx.stream, 0, xr);
@@ -852,9 +871,21 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     // after the bitset pass: true if the keys repeat and the counting-sort
     // pass must run (its key range: the max key the first pass folded)
     uint64_t ms_range = 0;
-    auto needs_multiset = [&]() {
-        const Ctrl c = read_ctrl(ctx, ctx.stream);
+    // restore_input: brings `in` back when the pass sorted in place (host
+    // arrays: upload again); called before a pass is redone
+    auto needs_multiset = [&](const uint32_t* in, uint32_t* out, const std::function<void()>& restore_input) {
+        Ctrl c = read_ctrl(ctx, ctx.stream);
+        if (small_spec && c.bad_keys != 0) {  // the keys outgrew the speculated range
+            ctx.spec_small = 0;
+            restore_input();
+            enqueue(in, out);
+            c = read_ctrl(ctx, ctx.stream);
+        }
         throw_bad_keys(c, key_range ? key_range : kMaxKeyRange);
+        if (small_unhinted && key_range == 0) {
+            const uint64_t r = spec_round(static_cast<uint64_t>(c.max_key) + 1);
+            ctx.spec_small = r <= kSmallMaxRange ? r : 0;
+        }
         if (c.total == count) return false;
         if (!multiset)
             throw data_error("keys are not distinct: " + std::to_string(count) + " keys, " +
@@ -935,7 +966,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     out_of_place:
         ctx.ensure_keys(count);
         enqueue(keys, ctx.keys);
-        if (needs_multiset()) {
+        if (needs_multiset(keys, ctx.keys, [] {})) {
             enqueue_multiset(keys, keys);
             return;
         }
@@ -958,7 +989,7 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
     upload();
     check_span(ctx.keys);
     enqueue(ctx.keys, ctx.keys);
-    if (needs_multiset()) {
+    if (needs_multiset(ctx.keys, ctx.keys, upload)) {
         upload();  // the host array is untouched until the write-back
         enqueue_multiset(ctx.keys, ctx.keys);
     }

@@ -108,6 +108,7 @@ struct DeviceCtx {
     // planned for (0: none yet, K0 derives it): the range the previous such
     // sort's keys really had, rounded up — see sort_u32
     uint64_t spec_range = 0;
+    uint64_t spec_small = 0;  // likewise for unhinted sorts below 2^21 keys (KS instead of K2 + K3)
     void* bounce[2] = {nullptr, nullptr};  // pinned staging for pageable host arrays
     cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
     cudaEvent_t done = nullptr;   // recorded after every queued sort: orders the

@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
     __shared__ uint32_t s_stage[KS_STAGE];
     __shared__ uint32_t s_warp[KS_THREADS / 32];
     __shared__ uint32_t s_bad;
+    __shared__ uint32_t s_max;
     __shared__ uint32_t s_fail;
     __shared__ unsigned long long s_base;
     __shared__ unsigned long long s_gen;
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
     for (uint32_t i = threadIdx.x; i < G; i += KS_THREADS) s_hist[i] = 0;
     if (threadIdx.x == 0) {
         s_bad = 0;
+        s_max = 0;
         s_fail = 0;
         s_base = 0;
         // The launch generation, from the arrival counter itself: every earlier
@@ -116,9 +118,10 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
     }
     {
         const size_t vlo = a.ks.nv * c / G, vhi = a.ks.nv * (c + 1) / G;
-        uint32_t bad = 0;
+        uint32_t bad = 0, kmax = 0;
         auto put = [&](uint32_t k) {
             const uint32_t x = (k ^ a.ks.xr) - a.lo;
+            kmax = max(kmax, k ^ a.ks.xr);  // like K0 / K2: the host tracks the range of unhinted sorts
             if (x > a.range_m1) {
                 ++bad;
                 return;
@@ -149,6 +152,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
         }
         bad = __reduce_add_sync(kFull, bad);
         if (lane == 0 && bad) atomicAdd(&s_bad, bad);
+        kmax = __reduce_max_sync(kFull, kmax);
+        if (lane == 0 && kmax) atomicMax(&s_max, kmax);
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < G; i += KS_THREADS) {
@@ -224,6 +229,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) small_sort_kernel(SmallArgs a) 
     if (threadIdx.x == 0) {  // (after the barrier: CTA 0 zeroed the control block before it arrived)
         if (cta_total) atomicAdd(&a.ctrl->total, static_cast<unsigned long long>(cta_total));
         if (s_bad) atomicAdd(&a.ctrl->bad_keys, s_bad);
+        if (s_max) atomicMax(&a.ctrl->max_key, s_max);
     }
     const unsigned long long base = s_base;
     if (tr && threadIdx.x == 0) tr[3] = ks_now();

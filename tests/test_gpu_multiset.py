@@ -201,3 +201,36 @@ def test_device_array_speculated_range(capi, cuda):
         for offset in (0, 1):
             got = _sort_device(capi, cuda, keys, is_unsigned, offset)
             assert np.array_equal(got, np.sort(keys)), name
+
+
+def test_small_unhinted_speculation(capi, cuda):
+    """bws_sort on arrays below 2^21 keys: the first sort runs K2 + K3 and
+    reports the keys' range; the next ones run the single-launch KS planned
+    for it. Host and device arrays through sequences that keep, outgrow
+    (redo with K2 + K3) and shrink the range, with repeats and a range above
+    KS's limit in between."""
+    rng = np.random.default_rng(91)
+    def distinct(n, m):
+        return rng.choice(m, size=n, replace=False).astype(np.uint32)
+    seq = [
+        distinct(100_000, 1 << 20),
+        distinct(100_000, 1 << 20),                       # same range: KS
+        distinct(300_001, 1 << 24),                       # outgrown: redone
+        distinct(300_001, 1 << 24),                       # KS
+        distinct(5, 1 << 10),                             # shrunk
+        distinct(5, 1 << 10),
+        rng.integers(0, 1 << 12, size=50_000, dtype=np.uint64).astype(np.uint32),   # repeats on the KS pass
+        distinct(70_000, 1 << 18),
+        (distinct(1000, 1 << 16).astype(np.uint64) + (1 << 31)).astype(np.uint32),  # beyond KS's AUTO range
+        distinct(70_000, 1 << 18),
+        np.array([7], dtype=np.uint32),
+        np.array([0xffffffff, 0, 5], dtype=np.uint32),
+        distinct((1 << 21) - 1, 1 << 22),
+    ]
+    for i, keys in enumerate(seq):
+        expected = np.sort(keys)
+        assert np.array_equal(_sort_host(capi, keys), expected), ("host", i)
+        assert np.array_equal(_sort_device(capi, cuda, keys, offset=i % 3), expected), ("device", i)
+    t = cuda.from_numpy(seq[3].view(np.int32).copy()).pin_memory()  # pinned host array
+    assert capi.sort_raw(t.data_ptr(), seq[3].size, 32, 1, 0) == capi.Status.OK, capi.last_error()
+    assert np.array_equal(t.numpy().view(np.uint32), np.sort(seq[3]))
