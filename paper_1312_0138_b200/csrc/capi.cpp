@@ -656,10 +656,12 @@ uint64_t enqueue_sort(DeviceCtx& ctx, const uint32_t* keys, size_t count, uint32
 
 // Synchronises and reads the control block back.
 Ctrl read_ctrl(DeviceCtx& ctx, cudaStream_t stream) {
-    cuda_check(cudaStreamSynchronize(stream), "sort execution");
-    Ctrl c;
-    cuda_check(cudaMemcpy(&c, ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost),
+    // one stream-ordered copy into pinned memory and one wait (a blocking
+    // cudaMemcpy after the synchronise cost a second host round trip)
+    cuda_check(cudaMemcpyAsync(ctx.host_ctrl, ctx.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost, stream),
                "control block readback");
+    cuda_check(cudaStreamSynchronize(stream), "sort execution");
+    const Ctrl c = *ctx.host_ctrl;
     if (c.error != 0) {  // KF ring / chunk-table protocol timeout: reset the ring state
         ctx.fused_dirty = true;
         ctx.small_dirty = true;

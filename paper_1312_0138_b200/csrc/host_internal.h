@@ -80,6 +80,7 @@ struct DeviceCtx {
     uint32_t* bits = nullptr;  // kMaxWords words; all-zero between sorts unless bits_dirty
     bool bits_dirty = true;
     unsigned char* ctrl_mem = nullptr;  // Ctrl followed by the K3 tile-status array
+    Ctrl* host_ctrl = nullptr;          // pinned landing buffer of the control block read-back
     uint32_t* keys = nullptr;           // staging for host arrays
     size_t keys_cap = 0;
     uint32_t* parted = nullptr;         // bucketed path: keys grouped by bucket
@@ -132,6 +133,7 @@ struct DeviceCtx {
         cuda_check(bws_gpu::configure_small(dev, &geo), "small-sort kernel configuration");
         cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaMalloc(&ctrl_mem, kCtrlBytes + sizeof(Ctrl)), "cudaMalloc(control block)");
+        cuda_check(cudaHostAlloc(&host_ctrl, sizeof(Ctrl), cudaHostAllocDefault), "cudaHostAlloc(control block)");
         pending = AsyncSort{};
         cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
         bws_gpu::BucketPlan widest;
@@ -253,6 +255,8 @@ struct DeviceCtx {
         }
         if (bits) cudaFree(bits);
         cudaFree(ctrl_mem);
+        if (host_ctrl) cudaFreeHost(host_ctrl);
+        host_ctrl = nullptr;
         if (keys) cudaFree(keys);
         if (parted) cudaFree(parted);
         if (bucket_scratch) cudaFree(bucket_scratch);
