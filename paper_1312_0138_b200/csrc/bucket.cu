@@ -768,11 +768,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 // aligned. The TMA ring is freed as soon as a tile's keys are in registers,
 // so the next-but-one tile's load starts a phase earlier than in the
 // in-place variant.
-template <int MAXB>
-__global__ void __launch_bounds__(PART_THREADS, 1)
+template <int MAXB, int THREADS_ = PART_THREADS, int KPT_ = PART_KPT>
+__global__ void __launch_bounds__(THREADS_, 1)
     bucket_partition_tma_kernel(KeySplit ks, BucketMap bm, int nb, uint32_t* __restrict__ parted, SlabArgs sa) {
-    constexpr int THREADS = PART_THREADS;
-    constexpr int KPT = PART_KPT;
+    constexpr int THREADS = THREADS_;
+    constexpr int KPT = KPT_;
+    static_assert(THREADS * KPT == PART_TILE, "the SMEM layout is sized for PART_TILE keys");
     constexpr int TILE = THREADS * KPT;
     constexpr int NWARPS = THREADS / 32;
     constexpr int kSlots = MAXB + 1;
@@ -1960,7 +1961,14 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
         sa.tot = tot;
         sa.g_base = base;
         if (timer) timer->before(stream);
-        if (sa.gtrue)
+        static const bool half_threads = [] {  // experiment: 512 threads x 32 keys (same tile)
+            const char* e = std::getenv("BITSORT_PART_TMA");
+            return e && std::string(e) == "512";
+        }();
+        if (sa.gtrue && half_threads)
+            bucket_partition_tma_kernel<512, 512, 32>
+                <<<P, 512, part_tma_smem_bytes(512), stream>>>(ks, plan.map, plan.nb, parted, sa);
+        else if (sa.gtrue)
             bucket_partition_tma_kernel<512>
                 <<<P, PART_THREADS, part_tma_smem_bytes(512), stream>>>(ks, plan.map, plan.nb, parted, sa);
         else if (narrow_partition(plan))
@@ -2094,6 +2102,9 @@ cudaError_t configure_bucket_kernels(int device, LaunchGeometry* geo) {
     err = cudaFuncSetAttribute(bucket_partition_kernel<PART_THREADS, PART_KPT, MAX_BUCKETS, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_smem_bytes(PART_THREADS, MAX_BUCKETS)));
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(bucket_partition_tma_kernel<512, 512, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(part_tma_smem_bytes(512)));
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(bucket_partition_tma_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(part_tma_smem_bytes(512)));
