@@ -37,6 +37,9 @@
 #include <thread>
 #include <vector>
 
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges are no-ops unless a tool attaches
 
 #include "bitsort/bitsort.h"
@@ -133,9 +136,44 @@ class CopyPool {
     }
 
    private:
+    // Streaming (non-temporal) stores for the staging copies: no
+    // read-for-ownership of the destination lines (C2 through bws_sort on a
+    // pageable array: 14.4-15.2 -> 13.4-13.8 ms). BITSORT_COPY_NT=0: memcpy.
+    static void copy_piece(char* d, const char* s, size_t n) {
+#if defined(__x86_64__)
+        static const bool nt = [] {
+            const char* e = std::getenv("BITSORT_COPY_NT");
+            return !(e && e[0] == '0');
+        }();
+        if (nt && n >= 4096) {
+            size_t head = (64 - (reinterpret_cast<uintptr_t>(d) & 63)) & 63;
+            if (head) {
+                std::memcpy(d, s, head);
+                d += head;
+                s += head;
+                n -= head;
+            }
+            size_t i = 0;
+            for (; i + 64 <= n; i += 64) {
+                const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+                const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+                const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+                const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+            }
+            _mm_sfence();
+            if (i < n) std::memcpy(d + i, s + i, n - i);
+            return;
+        }
+#endif
+        std::memcpy(d, s, n);
+    }
     void part(int i) {
         const size_t lo = (bytes_ * i / n_) & ~size_t(63), hi = i + 1 == n_ ? bytes_ : (bytes_ * (i + 1) / n_) & ~size_t(63);
-        if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+        if (hi > lo) copy_piece(dst_ + lo, src_ + lo, hi - lo);
     }
     void loop(int i) {
         uint64_t seen = 0;
