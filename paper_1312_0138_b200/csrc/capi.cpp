@@ -964,7 +964,10 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
             // one KB3 and is redone from the intact keys with K0's range.
             bool speculated = false;
             if (key_range == 0) {
-                if (ctx.spec_range != 0 && speculate_range()) {
+                // (two misses in a row — a caller alternating between ranges —
+                // switch speculation off for the next 16 sorts: a miss costs a KB3)
+                if (ctx.spec_cooldown > 0) --ctx.spec_cooldown;
+                if (ctx.spec_range != 0 && ctx.spec_cooldown == 0 && speculate_range()) {
                     key_range = ctx.spec_range;
                     speculated = true;
                 } else {
@@ -978,7 +981,12 @@ void sort_u32(void* data, size_t count, uint64_t key_range, uint32_t xr = 0, boo
             if (bucketed_slab(ctx, count, key_range, xr)) {
                 enqueue_bucketed(ctx, keys, count, keys, key_range, ctx.stream, 0, xr, false, /*inplace=*/1);
                 Ctrl c = read_ctrl(ctx, ctx.stream);
+                if (speculated && c.bad_keys == 0) ctx.spec_misses = 0;
                 if (speculated && c.bad_keys != 0) {  // the keys outgrew the speculated range
+                    if (++ctx.spec_misses >= 2) {
+                        ctx.spec_misses = 0;
+                        ctx.spec_cooldown = 16;
+                    }
                     ctx.spec_range = 0;
                     key_range = derive_range(ctx, keys, count, ctx.stream, xr);
                     speculated = false;

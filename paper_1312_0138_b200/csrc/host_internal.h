@@ -109,6 +109,8 @@ struct DeviceCtx {
     // planned for (0: none yet, K0 derives it): the range the previous such
     // sort's keys really had, rounded up — see sort_u32
     uint64_t spec_range = 0;
+    int spec_misses = 0;      // consecutive sorts whose keys outgrew spec_range
+    int spec_cooldown = 0;    // sorts left that run K0 without speculating (after two misses in a row)
     uint64_t spec_small = 0;  // likewise for unhinted sorts below 2^21 keys (KS instead of K2 + K3)
     void* bounce[2] = {nullptr, nullptr};  // pinned staging for pageable host arrays
     cudaEvent_t bounce_ev[2] = {nullptr, nullptr};

@@ -234,3 +234,16 @@ def test_small_unhinted_speculation(capi, cuda):
     t = cuda.from_numpy(seq[3].view(np.int32).copy()).pin_memory()  # pinned host array
     assert capi.sort_raw(t.data_ptr(), seq[3].size, 32, 1, 0) == capi.Status.OK, capi.last_error()
     assert np.array_equal(t.numpy().view(np.uint32), np.sort(seq[3]))
+
+
+def test_device_array_alternating_ranges(capi, cuda):
+    """A caller alternating between a narrow and a wide key range on one
+    device: every second sort outgrows the speculated range; after two misses
+    in a row the library stops speculating for a while. All results exact."""
+    rng = np.random.default_rng(5)
+    n = (1 << 22) + 7
+    narrow = rng.choice(1 << 23, size=n, replace=False).astype(np.uint32)
+    wide = rng.choice(1 << 24, size=n, replace=False).astype(np.uint32)
+    for i in range(24):
+        keys = wide if i % 2 else narrow
+        assert np.array_equal(_sort_device(capi, cuda, keys, 1, i % 2), np.sort(keys)), i
