@@ -749,6 +749,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 tma_load_bytes(buf, ks.body + v2, static_cast<unsigned>(nv2 * 16), &s_bar[p]);
         }
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if constexpr (SLAB) slab_finish(sa, nb, bad, kmax, s_cur, s_base64, s_scratch, &s_last);
 }
 
@@ -995,6 +996,9 @@ __global__ void __launch_bounds__(THREADS_, 1)
         }
         if (stores_pending) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+    // the dependent KB4 may start its prologue (it waits for this grid's completion
+    // before reading anything KB3 wrote)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (stores_pending) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     slab_finish(sa, nb, bad, kmax, s_cnt, reinterpret_cast<unsigned long long*>(s_sorted), s_scratch, &s_last);
 }
@@ -1084,7 +1088,6 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
                        uint32_t chunk_pad) {
     // in-place sorts: a slab that lost runs (repeated keys overflowed a
     // bucket) writes nothing, so the input stays intact for the counting pass
-    if (all_or_nothing && *reinterpret_cast<volatile const uint32_t*>(&ctrl->overflow)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t W = bm.width >> 5;  // words per bucket bitset (>= 1024; 2^k or a multiple of 4096)
     uint32_t* s_bits = reinterpret_cast<uint32_t*>(smem_raw);
@@ -1131,11 +1134,21 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
         }
     };
     for (uint32_t i = threadIdx.x; i < W / 32; i += NT) s_sum[i] = 0u;
+    {  // the first bucket's clean bitset
+        uint4* b4 = reinterpret_cast<uint4*>(s_bits);
+        for (uint32_t i = threadIdx.x; i < W / 4; i += NT) b4[i] = make_uint4(0, 0, 0, 0);
+    }
+    // Programmatic dependent launch: everything above (barrier init, 100+ KB of
+    // SMEM zeroing) ran while KB3's last CTAs were finishing; KB3's results
+    // (totals, offsets, order, the control block) are read only below this
+    // wait. Without the launch attribute the wait returns at once.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (all_or_nothing && *reinterpret_cast<volatile const uint32_t*>(&ctrl->overflow)) return;
     if (threadIdx.x == 0) {
         if (order && order[nb] == 0u) order = nullptr;  // identity: no per-ticket lookup
         fetch(0);
     }
-    bool dirty = true;  // block-uniform: bitset needs zeroing before the next bucket
+    bool dirty = false;  // block-uniform: bitset needs zeroing before the next bucket
     for (unsigned it = 0;; ++it) {
         const int slot = static_cast<int>(it & 1u);
         if (dirty) {  // the previous bucket's readers finished at the loop-end barrier
@@ -2055,14 +2068,37 @@ cudaError_t launch_bucket_sort(const uint32_t* keys, size_t n, uint64_t key_rang
     }
     if (timer) timer->before(stream);
     const size_t smem = bucket_sort_smem_bytes(plan.shift);
+    // KB4 directly after KB3 on the stream: programmatic dependent launch (its
+    // prologue overlaps KB3's tail). Not with per-kernel timing events in between.
+    static const bool pdl_off = [] {
+        const char* e = std::getenv("BITSORT_PDL");
+        return e && std::string(e) == "0";
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(geo.bucket_blocks[plan.shift]));
+    cfg.blockDim = dim3(plan.shift >= MAX_BUCKET_SHIFT ? BUCKET_THREADS : 512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute pdl_attr[1];
+    pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+    if (!timer && !pdl_off && nlaunch > 0) {
+        cfg.attrs = pdl_attr;
+        cfg.numAttrs = 1;
+    }
+    const int aon = inplace_mode == 1 && use_slab;
+    const uint32_t* ctab = use_chunk ? sa.chunk_tab : nullptr;
     if (plan.shift >= MAX_BUCKET_SHIFT)
-        bucket_sort_kernel<BUCKET_STAGE><<<geo.bucket_blocks[plan.shift], BUCKET_THREADS, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
-            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift, sa.chunk_pad);
+        err = cudaLaunchKernelEx(&cfg, bucket_sort_kernel<BUCKET_STAGE>, static_cast<const uint32_t*>(parted),
+                                 static_cast<const uint32_t*>(tot), static_cast<const unsigned long long*>(base),
+                                 plan.map, plan.nb, src_cap, out, ctrl, static_cast<const uint32_t*>(kb4_order), aon,
+                                 ctab, sa.max_chunks, sa.chunk_shift, sa.chunk_pad);
     else  // narrower buckets: two 512-thread CTAs per SM
-        bucket_sort_kernel<BUCKET_STAGE, 512><<<geo.bucket_blocks[plan.shift], 512, smem, stream>>>(
-            parted, tot, base, plan.map, plan.nb, src_cap, out, ctrl, kb4_order, inplace_mode == 1 && use_slab,
-            use_chunk ? sa.chunk_tab : nullptr, sa.max_chunks, sa.chunk_shift, sa.chunk_pad);
+        err = cudaLaunchKernelEx(&cfg, bucket_sort_kernel<BUCKET_STAGE, 512>, static_cast<const uint32_t*>(parted),
+                                 static_cast<const uint32_t*>(tot), static_cast<const unsigned long long*>(base),
+                                 plan.map, plan.nb, src_cap, out, ctrl, static_cast<const uint32_t*>(kb4_order), aon,
+                                 ctab, sa.max_chunks, sa.chunk_shift, sa.chunk_pad);
+    if (err != cudaSuccess) return err;
     if (timer) timer->after("bucket_sort", stream);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if (launches) *launches = nlaunch + 1;
